@@ -1,0 +1,184 @@
+/*
+ * owqs.h — C-ABI of the B200-native OWQS/EOWQS array executor (libowqs.so).
+ *
+ * What the library computes: the array (state-vector) execution of a one-way quantum computer
+ * measurement pattern P = (V, I, O, A) (§2.2): commands N, E, M^alpha, X^s, Z^s
+ * (L69-81), measurement angles adapted by Eq. 2 (L77), each measured qubit eliminated from the
+ * state with the operators of Eqs. 11-12 (L193-195, §4.2), commands reordered by PROA (Eq. 18,
+ * §4.3) and executed by fused sm_100a kernels (§4.4's implicit actions). "It takes a
+ * pattern ... as well as the state of the input qubits ... the state of the output qubits is
+ * reported" (L153, Fig. 1). EOWQS (L370-372): outcomes pre-selected to 0, no probabilities,
+ * sqrt(2) renormalisation per measurement.
+ *
+ * Conventions:
+ *  - Measurement basis: <+-a| = (<0| +- e^{-i a}<1|)/sqrt2 (reading R-1, Eqs. 9-12).
+ *  - Amplitude index: bit k <-> inputs[k] (input state) / outputs[k] (output state); inputs[0]
+ *    and outputs[0] are the least significant bit (Eq. 8 layout, L157-161).
+ *  - Qubit ids are arbitrary non-negative int32. A non-input qubit used before an explicit N
+ *    gets an implicit N at first use (reading R-11).
+ *  - Sampled outcomes: u_M = (splitmix64(seed ^ splitmix64(ord)) >> 11) * 2^-53, ord = ordinal
+ *    of the M command in the GIVEN list; outcome 0 iff u_M <= prob0 (Fig. 6, reading R-5).
+ *  - Arrays indexed "per M" ([n_measure]) use that same given-order ordinal.
+ *
+ * Ownership and errors: every call returns owqs_status (0 = OK). The caller owns every buffer
+ * it passes; the library copies what it needs during the call and never keeps caller pointers.
+ * On error, owqs_last_error() describes the failure (string owned by the context, valid until
+ * the next call on it). A context is single-writer (not thread-safe). Device memory is owned
+ * by the context and released by owqs_destroy.
+ */
+#ifndef OWQS_H
+#define OWQS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct owqs_ctx owqs_ctx; /* opaque */
+
+typedef enum {
+  OWQS_OK = 0,
+  OWQS_E_ARG = 1,               /* bad argument (NULL, size mismatch, unknown enum)          */
+  OWQS_E_PATTERN = 2,           /* rules D0-D3 (L83-91), duplicate E, E(u,u), second N, ...  */
+  OWQS_E_NO_GFLOW = 3,          /* reserved: EOWQS gflow pre-check (L372)                     */
+  OWQS_E_BRANCH = 4,            /* forced outcome whose probability is < 1e-12               */
+  OWQS_E_STATE = 5,             /* call order (run before set_input, output before run, ...)  */
+  OWQS_E_NOMEM = 6,             /* state width exceeds device memory                          */
+  OWQS_E_CUDA = 7,              /* CUDA runtime error                                         */
+  OWQS_E_NCCL = 8,              /* NCCL error (multi-rank)                                    */
+  OWQS_E_NOT_DETERMINISTIC = 9  /* EOWQS run whose final norm is not 1: some prob0 != 1/2     */
+} owqs_status;
+
+typedef enum { OWQS_CMD_N = 0, OWQS_CMD_E = 1, OWQS_CMD_M = 2, OWQS_CMD_X = 3, OWQS_CMD_Z = 4 } owqs_kind;
+
+/* One command (L69-81). Layout fixed: 40 bytes.
+ *  kind  : owqs_kind
+ *  q0    : target qubit (u for E)           q1 : second qubit (E only, else ignored)
+ *  s_off, s_len : s-signal domain = domain_pool[s_off .. s_off+s_len) (M, X, Z)
+ *  t_off, t_len : t-signal domain (M only)
+ *  angle : base angle alpha of Eq. 2, radians (M only) */
+typedef struct {
+  int32_t kind, q0, q1;
+  int32_t s_off, s_len, t_off, t_len;
+  int32_t reserved;
+  double angle;
+} owqs_cmd;
+
+/* Context configuration.
+ *  precision : 64 -> complex64 amplitudes (fp32 arithmetic, fp64 reductions);
+ *              128 -> complex128 (fp64)
+ *  n_ranks, rank : SPMD sharding of the top log2(n_ranks) slot bits (1 = single GPU)
+ *  device    : CUDA device ordinal
+ *  nccl_id   : pointer to a 128-byte ncclUniqueId shared by all ranks (n_ranks > 1), else NULL
+ *  flags     : OWQS_FLAG_* bit set
+ *  stream    : cudaStream_t to run on (NULL: the library creates a non-blocking stream) */
+typedef struct {
+  int32_t precision;
+  int32_t n_ranks, rank, device;
+  const void* nccl_id;
+  uint32_t flags;
+  int32_t reserved;
+  void* stream;
+} owqs_config;
+
+#define OWQS_FLAG_NO_GRAPH    0x1u /* launch passes one by one instead of replaying a CUDA graph */
+#define OWQS_FLAG_NO_FUSE     0x2u /* at most one measurement butterfly per state pass          */
+#define OWQS_FLAG_GIVEN_ORDER 0x4u /* skip PROA: execute measurements in the given order         */
+#define OWQS_FLAG_NO_TUNE     0x8u /* PROA with the initial weights only (no L487 tuning loop)   */
+
+typedef enum { OWQS_SAMPLED = 0, OWQS_FORCED = 1, OWQS_EOWQS = 2 } owqs_mode;
+
+/* Statistics (layout fixed). Valid after owqs_load_pattern; run fields after owqs_run. */
+typedef struct {
+  int64_t n_commands;        /* commands after implicit-N insertion                          */
+  int64_t n_measure;         /* K = |V| - |O|                                                 */
+  int32_t paper_m;           /* max PROA measurement state-space MS (append-then-measure m)   */
+  int32_t phys_bits;         /* max physical width of the compiled program (slot reuse)      */
+  int32_t n_passes;          /* full-state kernel passes in the compiled program (last mode) */
+  int32_t n_grow, n_shrink, n_reduce;
+  int32_t n_launches;        /* kernel launches per owqs_run (last mode)                      */
+  int32_t n_swaps;           /* global<->local slot swaps (multi-rank)                        */
+  double bytes_per_run;      /* analytic HBM bytes per owqs_run (all ranks' shards, this rank) */
+  double last_run_ms;        /* device time of the last owqs_run (CUDA events)               */
+  double schedule_ms;        /* host time spent in PROA + compile for the last mode          */
+  double reserved[4];
+} owqs_stats_t;
+
+/* Create / destroy a context on cfg->device. */
+owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out);
+void owqs_destroy(owqs_ctx* ctx);
+
+/* Load a pattern in its GIVEN (execution) order (L67; right-to-left notation already reversed).
+ * Validates D0-D3 (L83-91), inserts implicit N, builds the dependency DAG of non-commuting
+ * commands (Eqs. 14-16) and runs PROA (Eq. 18 with the tuning of L487). No device work.
+ * inputs[n_in], outputs[n_out] : qubit ids; bit k of the input/output index is inputs[k]/outputs[k].
+ * domain_pool[pool_len]        : qubit ids referenced by the cmds' signal domains.
+ * Errors: OWQS_E_ARG, OWQS_E_PATTERN (message names the command index). */
+owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in,
+                              const int32_t* outputs, int32_t n_out,
+                              const owqs_cmd* cmds, int64_t n_cmds,
+                              const int32_t* domain_pool, int64_t pool_len);
+
+/* Input state of the input qubits (L153). amps: HOST array of n_amps = 2^n_in complex128 values,
+ * interleaved (re, im). Copied to the device (converted to complex64 at precision 64).
+ * Errors: OWQS_E_ARG (size), OWQS_E_STATE (no pattern), OWQS_E_NOMEM, OWQS_E_CUDA. */
+owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps);
+
+/* Same from a DEVICE buffer on the context's device. precision 64: interleaved float pairs;
+ * 128: interleaved double pairs. The buffer is read during the call only. */
+owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t precision, int64_t n_amps);
+
+/* Device-generated Haar-random input (documented counter generator, workloads/inputs.py):
+ * amp_j = sqrt(-2 ln u1) e^{2 pi i u2} from splitmix64 of (seed, j), then normalised. */
+owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed);
+
+/* Execute the loaded pattern on the current input (consumes it: the state becomes the output).
+ * mode OWQS_SAMPLED : outcomes drawn as in the conventions above from `seed`;
+ *      OWQS_FORCED  : forced[n_measure] gives each outcome (given-order ordinal);
+ *                     OWQS_E_BRANCH if a forced branch has probability < 1e-12;
+ *      OWQS_EOWQS   : every outcome 0, no probability computation, sqrt2 per M (L372);
+ *                     OWQS_E_NOT_DETERMINISTIC if the final norm^2 differs from 1 by more than
+ *                     1e-8 (precision 128) / 1e-3 (precision 64).
+ * outcomes_out[n_measure] (may be NULL): s_v per M (given-order ordinal).
+ * prob0_out[n_measure] (may be NULL): <psi|P_0|psi> at that measurement (Eq. 3/13), -1 in EOWQS. */
+owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced,
+                     uint8_t* outcomes_out, double* prob0_out);
+
+/* Output state over O (L153, L419): HOST array of n_amps >= 2^n_out complex128, interleaved,
+ * bit k <-> outputs[k]. Multi-rank: filled on rank 0 only (amps may be NULL elsewhere). */
+owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps);
+
+/* Output into a DEVICE buffer (precision 64: float pairs, 128: double pairs), n_amps >= 2^n_out
+ * (single rank). */
+owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precision, int64_t n_amps);
+
+/* <a|b> of the output states of two contexts with the same output qubits, on the device. */
+owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im);
+
+/* Recognition problem (L33): the unitary implemented by the loaded (deterministic) pattern.
+ * Column k = EOWQS run on basis input |k> (all outcomes 0, sqrt2 per M: a linear map).
+ * U: HOST array of n = 2^n_out * 2^n_in complex128 (interleaved), column-major.
+ * max_unitarity_err (may be NULL): max |(U^dag U - I)_ij|. Overwrites the current input. */
+owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err);
+
+/* Sizes after owqs_load_pattern (any pointer may be NULL). n_passes is for the sampled plan. */
+owqs_status owqs_pattern_info(owqs_ctx* ctx, int64_t* n_measure, int32_t* paper_m, int32_t* phys_bits,
+                              int32_t* n_passes);
+
+/* PROA result for `mode`: measured qubit ids in plan order (qubits[n_measure]) and the MS of each
+ * step (ms[n_measure], may be NULL). */
+owqs_status owqs_plan_order(owqs_ctx* ctx, owqs_mode mode, int32_t* qubits, int32_t* ms, int64_t n);
+
+/* Override the PROA weights (alpha, beta, gamma, delta of Eq. 18) for subsequent plans; tune != 0
+ * re-enables the L487 loop that decrements alpha |O| times starting from these values. */
+owqs_status owqs_set_proa_weights(owqs_ctx* ctx, double a, double b, double g, double d, int32_t tune);
+
+owqs_status owqs_stats(owqs_ctx* ctx, owqs_stats_t* out);
+const char* owqs_last_error(const owqs_ctx* ctx);
+const char* owqs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OWQS_H */

@@ -1,0 +1,56 @@
+/*
+ * owqs_host.h — host-only introspection of the scheduler in libowqs.so (no CUDA calls; usable on
+ * a machine without a GPU). It exposes what owqs_load_pattern computes before any device work:
+ * the validated pattern (rules D0-D3), the PROA plan (Eq. 18, §4.3,
+ * tuning L487) and the compiled device step program, so that tests can check
+ * PROA against Table I / Eq. 23 / §4.6 and the slot-reuse compiler against the oracle on CPU.
+ *
+ * Ownership: owqs_host_compile allocates a handle that the caller releases with owqs_host_free.
+ * All output buffers are caller-owned; sizes come from owqs_host_info. Errors: OWQS_E_ARG,
+ * OWQS_E_PATTERN (message via owqs_host_error).
+ */
+#ifndef OWQS_HOST_H
+#define OWQS_HOST_H
+
+#include <stdint.h>
+
+#include "owqs.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct owqs_host_plan owqs_host_plan; /* opaque */
+
+typedef struct {
+  int64_t n_steps;      /* device steps (kernel launches) of the compiled program          */
+  int64_t n_measure;
+  int64_t sig_len;      /* entries of the signal pool (given-order M ordinals)             */
+  int32_t paper_m;      /* max MS of the plan                                               */
+  int32_t phys_bits;    /* max physical width                                               */
+  int32_t in_width, n_out;
+  int32_t step_bytes;   /* sizeof(StepDesc), for layout checks                              */
+  int32_t mstatic_bytes;/* sizeof(MStatic)                                                  */
+  int32_t n_passes, n_grow, n_shrink, n_reduce;
+  double bytes_per_run; /* analytic HBM bytes of one run at `precision`                     */
+} owqs_host_info;
+
+/* Validate + PROA + compile for `mode` (owqs_mode) at `precision` (64/128) with `flags`
+ * (OWQS_FLAG_*). weights: NULL (paper defaults and tuning) or {alpha, beta, gamma, delta}. */
+owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t* outputs, int32_t n_out,
+                              const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool, int64_t pool_len,
+                              int32_t mode, int32_t precision, uint32_t flags, const double* weights,
+                              owqs_host_plan** out);
+owqs_status owqs_host_info_get(const owqs_host_plan* h, owqs_host_info* info);
+/* Copy out the program. Any pointer may be NULL. steps: n_steps * step_bytes bytes; mst:
+ * n_measure * mstatic_bytes bytes; sig: sig_len int32; out_slot: n_out int32 (slot of outputs[k]);
+ * plan_qubits / plan_ms: n_measure int32 (measured qubit ids in plan order and their MS). */
+owqs_status owqs_host_program(const owqs_host_plan* h, void* steps, void* mst, int32_t* sig, int32_t* out_slot,
+                              int32_t* plan_qubits, int32_t* plan_ms);
+const char* owqs_host_error(const owqs_host_plan* h);
+void owqs_host_free(owqs_host_plan* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OWQS_HOST_H */

@@ -1,0 +1,88 @@
+// Host-only introspection API (include/owqs_host.h): validation + PROA + compile, no CUDA calls.
+#include <string.h>
+
+#include <string>
+
+#include "owqs_host.h"
+#include "scheduler.h"
+
+using namespace owqs;
+
+struct owqs_host_plan {
+  std::string err;
+  HostPattern hp;
+  Plan plan;
+  Program prog;
+  int elem = 16;
+};
+
+extern "C" {
+
+owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t* outputs, int32_t n_out,
+                              const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool, int64_t pool_len,
+                              int32_t mode, int32_t precision, uint32_t flags, const double* weights,
+                              owqs_host_plan** out) {
+  if (!out) return OWQS_E_ARG;
+  *out = nullptr;
+  if ((precision != 64 && precision != 128) || mode < 0 || mode > 2) return OWQS_E_ARG;
+  owqs_host_plan* h = new owqs_host_plan();
+  *out = h;
+  std::string e = validate_pattern(inputs, n_in, outputs, n_out, cmds, n_cmds, domain_pool, pool_len, h->hp);
+  if (!e.empty()) {
+    h->err = e;
+    return OWQS_E_PATTERN;
+  }
+  ProaWeights w;
+  if (weights) {
+    w.a = weights[0];
+    w.b = weights[1];
+    w.g = weights[2];
+    w.d = weights[3];
+  }
+  if (flags & OWQS_FLAG_NO_TUNE) w.tune = false;
+  h->plan = make_plan(h->hp, mode == 2, (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w);
+  h->prog = compile_program(h->hp, h->plan, mode, precision == 64 ? 6 : 5, !(flags & OWQS_FLAG_NO_FUSE));
+  h->elem = precision == 64 ? 8 : 16;
+  return OWQS_OK;
+}
+
+owqs_status owqs_host_info_get(const owqs_host_plan* h, owqs_host_info* info) {
+  if (!h || !info) return OWQS_E_ARG;
+  memset(info, 0, sizeof(*info));
+  info->n_steps = (int64_t)h->prog.steps.size();
+  info->n_measure = h->hp.n_measure;
+  info->sig_len = (int64_t)h->prog.sig_pool.size();
+  info->paper_m = h->plan.paper_m;
+  info->phys_bits = h->prog.phys_bits;
+  info->in_width = h->prog.in_width;
+  info->n_out = (int32_t)h->hp.outputs.size();
+  info->step_bytes = (int32_t)sizeof(StepDesc);
+  info->mstatic_bytes = (int32_t)sizeof(MStatic);
+  info->n_passes = h->prog.n_passes;
+  info->n_grow = h->prog.n_grow;
+  info->n_shrink = h->prog.n_shrink;
+  info->n_reduce = h->prog.n_reduce;
+  info->bytes_per_run = h->prog.bytes_per_run(h->elem);
+  return OWQS_OK;
+}
+
+owqs_status owqs_host_program(const owqs_host_plan* h, void* steps, void* mst, int32_t* sig, int32_t* out_slot,
+                              int32_t* plan_qubits, int32_t* plan_ms) {
+  if (!h) return OWQS_E_ARG;
+  if (steps && !h->prog.steps.empty()) memcpy(steps, h->prog.steps.data(), h->prog.steps.size() * sizeof(StepDesc));
+  if (mst && !h->prog.mst.empty()) memcpy(mst, h->prog.mst.data(), h->prog.mst.size() * sizeof(MStatic));
+  if (sig && !h->prog.sig_pool.empty()) memcpy(sig, h->prog.sig_pool.data(), h->prog.sig_pool.size() * sizeof(int32_t));
+  if (out_slot)
+    for (size_t k = 0; k < h->prog.out_slot.size(); ++k) out_slot[k] = h->prog.out_slot[k];
+  for (size_t i = 0; i < h->plan.m_cmds.size(); ++i) {
+    if (plan_qubits) plan_qubits[i] = h->hp.ext_id[h->hp.cmds[h->plan.m_cmds[i]].q0];
+    if (plan_ms) plan_ms[i] = h->plan.ms[i];
+  }
+  return OWQS_OK;
+}
+
+const char* owqs_host_error(const owqs_host_plan* h) { return h ? h->err.c_str() : "NULL handle"; }
+
+void owqs_host_free(owqs_host_plan* h) { delete h; }
+
+}  // extern "C"

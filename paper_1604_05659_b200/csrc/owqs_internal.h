@@ -1,0 +1,86 @@
+// Internal definitions shared by the host scheduler (C++) and the sm_100a kernels (CUDA).
+// Plain-old-data only: the compiled pass program is uploaded / passed by value to kernels.
+#pragma once
+#include <stdint.h>
+
+namespace owqs {
+
+// ---- device op encoding (16 bytes) ------------------------------------------------------------
+enum OpType : uint8_t {
+  OP_NONE = 0,
+  OP_DIAG_E = 1,  // CZ sign flip on slots (a, b)               PAPER §4.4.1, Fig. 5 (E action)
+  OP_DIAG_Z = 2,  // Z^s on slot a (sign on bit a = 1)
+  OP_X = 3,       // X^s on slot a (swap pairs)
+  OP_BFLY = 4,    // measurement butterfly on slot a, M record m (slot reuse: the new qubit takes
+                  // slot a; Eqs. 11-12 with N_o E_io folded in)
+};
+
+struct Op {
+  uint8_t type;
+  uint8_t a;
+  uint8_t b;
+  uint8_t cond;     // 1: conditional on the XOR of outcomes sig_pool[sig_off .. sig_off+sig_len)
+  int32_t sig_off;
+  int32_t sig_len;
+  int32_t m;        // M plan index (OP_BFLY)
+};
+static_assert(sizeof(Op) == 16, "Op layout");
+
+constexpr int MAX_OPS = 40;      // ops per pass
+constexpr int KMAX_HI = 4;       // group slots above the warp segment per pass
+constexpr int MAX_BFLY = 24;     // butterflies per pass (fused mode)
+
+enum StepKind : int32_t { ST_PASS = 0, ST_GROW = 1, ST_SHRINK = 2 };
+enum RedKind : int32_t { RED_NONE = 0, RED_NORM = 1, RED_RHO = 2 };
+
+// One device step. Passed by value as a kernel parameter.
+struct StepDesc {
+  int32_t kind;        // StepKind
+  int32_t width;       // state width (bits) when the step runs
+  int32_t nb_hi;       // number of group slots >= segment bits
+  int32_t bhi[KMAX_HI];
+  int32_t n_ops;
+  int32_t red_kind;    // reduction of the step's OUTPUT state (RedKind)
+  int32_t red_slot;    // slot for RED_RHO
+  int32_t slot;        // GROW: new top slot; SHRINK: measured slot
+  int32_t shrink_m;    // SHRINK: M plan index
+  int32_t n_bfly;      // number of OP_BFLY in ops
+  int32_t first_uses_red;  // 1: the first butterfly (or the SHRINK) decides from red_result
+  int32_t first_full_rho;  // 1: red_result holds (n0, n1, Re c, Im c) of the measured slot
+  int32_t pad;
+  Op ops[MAX_OPS];
+};
+
+// Static record of one measurement (plan order). Uploaded once per compiled plan.
+struct MStatic {
+  double alpha;       // base angle of Eq. 2
+  int32_t ord;        // ordinal of the M in the GIVEN list (outcome / prob0 / draw index)
+  int32_t s_off, s_len, t_off, t_len;  // domains as given-order ordinals in sig_pool
+  int32_t reuse;      // 1: slot-reuse butterfly (fresh |+> neighbour folded), 0: elimination
+  int32_t structural; // 1: prob0 = ||psi||^2 / 2 exactly (a fresh |+> neighbour dephases it)
+};
+
+// Run parameters in device memory (written by the host before each run).
+struct RunParams {
+  int32_t mode;       // owqs_mode
+  int32_t pad;
+  uint64_t seed;
+};
+
+// Device-side pointers, passed by value to kernels.
+struct DevPtrs {
+  void* state;                 // float2* (complex64) or double2* (complex128)
+  const MStatic* mst;          // [n_measure] plan order
+  double* coef;                // [n_measure][8]: resolved 2x2 (EOWQS precomputed on host)
+  uint8_t* outcome;            // [n_measure] given-order ordinal
+  double* prob0;               // [n_measure] given-order ordinal
+  const uint8_t* forced;       // [n_measure] given-order ordinal
+  const int32_t* sig_pool;     // domains as given-order ordinals
+  const RunParams* run;
+  double* partials;            // [max_blocks][4]
+  unsigned int* counter;       // last-block-done counter
+  double* red_result;          // [4]
+  int32_t* err;                // device error flag (1 = forced branch with prob < 1e-12)
+};
+
+}  // namespace owqs

@@ -1,0 +1,771 @@
+// Host scheduler: validation, dependency DAG (Eqs. 14-16), PROA (Eq. 18,
+// tuning L487) and the slot-reuse compiler.
+#include "scheduler.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <unordered_map>
+#include <unordered_set>
+
+#include "owqs.h"
+
+namespace owqs {
+
+namespace {
+std::string fmt_cmd(int64_t i) {
+  std::ostringstream os;
+  os << "command " << i;
+  return os.str();
+}
+}  // namespace
+
+// ------------------------------------------------------------------------------------------------
+// Validation. States: 0 unprepared, 1 live, 2 measured. D0: signals only reference measured
+// qubits. D1: no action on a measured qubit. D2: non-inputs are prepared before use (implicit N
+// at first use, reading R-11). D3: measured iff not output.
+// ------------------------------------------------------------------------------------------------
+std::string validate_pattern(const int32_t* inputs, int n_in, const int32_t* outputs, int n_out,
+                             const void* cmds_v, int64_t n_cmds, const int32_t* pool,
+                             int64_t pool_len, HostPattern& hp) {
+  const owqs_cmd* cmds = static_cast<const owqs_cmd*>(cmds_v);
+  hp = HostPattern();
+  std::unordered_map<int32_t, int> dense;
+  auto idx = [&](int32_t ext) -> int {
+    auto it = dense.find(ext);
+    if (it != dense.end()) return it->second;
+    int d = (int)hp.ext_id.size();
+    dense.emplace(ext, d);
+    hp.ext_id.push_back(ext);
+    return d;
+  };
+  if (n_in < 0 || n_out < 0 || n_cmds < 0 || pool_len < 0) return "negative size";
+  if ((n_in > 0 && !inputs) || (n_out > 0 && !outputs) || (n_cmds > 0 && !cmds)) return "NULL array";
+  for (int i = 0; i < n_in; ++i) {
+    if (inputs[i] < 0) return "negative qubit id in inputs";
+    if (dense.count(inputs[i])) return "duplicate input qubit";
+    hp.inputs.push_back(idx(inputs[i]));
+  }
+  std::unordered_set<int32_t> outset;
+  for (int i = 0; i < n_out; ++i) {
+    if (outputs[i] < 0) return "negative qubit id in outputs";
+    if (!outset.insert(outputs[i]).second) return "duplicate output qubit";
+  }
+  // first pass: register ids in order of appearance
+  for (int64_t c = 0; c < n_cmds; ++c) {
+    const owqs_cmd& k = cmds[c];
+    if (k.kind < 0 || k.kind > 4) return fmt_cmd(c) + ": unknown kind";
+    if (k.q0 < 0) return fmt_cmd(c) + ": negative qubit id";
+    idx(k.q0);
+    if (k.kind == OWQS_CMD_E) {
+      if (k.q1 < 0) return fmt_cmd(c) + ": negative qubit id";
+      if (k.q1 == k.q0) return fmt_cmd(c) + ": E on a single qubit";
+      idx(k.q1);
+    }
+    auto chk = [&](int32_t off, int32_t len) -> bool {
+      return len == 0 || (off >= 0 && len > 0 && off + (int64_t)len <= pool_len && pool);
+    };
+    if (k.kind == OWQS_CMD_M || k.kind == OWQS_CMD_X || k.kind == OWQS_CMD_Z) {
+      if (!chk(k.s_off, k.s_len)) return fmt_cmd(c) + ": s-domain out of domain_pool";
+    }
+    if (k.kind == OWQS_CMD_M && !chk(k.t_off, k.t_len)) return fmt_cmd(c) + ": t-domain out of domain_pool";
+    if (k.kind == OWQS_CMD_M && !std::isfinite(k.angle)) return fmt_cmd(c) + ": non-finite angle";
+  }
+  for (int i = 0; i < n_out; ++i) hp.outputs.push_back(idx(outputs[i]));
+  hp.nq = (int)hp.ext_id.size();
+  hp.is_output.assign(hp.nq, 0);
+  hp.is_input.assign(hp.nq, 0);
+  for (int o : hp.outputs) hp.is_output[o] = 1;
+  for (int i : hp.inputs) hp.is_input[i] = 1;
+
+  std::vector<int> st(hp.nq, 0);
+  for (int i : hp.inputs) st[i] = 1;
+  std::unordered_set<uint64_t> epairs;
+  hp.m_ord_of_qubit.assign(hp.nq, -1);
+  auto need_live = [&](int q, int64_t c, std::string& err) {
+    if (st[q] == 2) {
+      err = fmt_cmd(c) + ": D1 violated (action on measured qubit " + std::to_string(hp.ext_id[q]) + ")";
+      return;
+    }
+    if (st[q] == 0) {  // implicit N at first use (R-11)
+      HCmd n;
+      n.kind = H_N;
+      n.q0 = q;
+      hp.cmds.push_back(n);
+      st[q] = 1;
+    }
+  };
+  auto dom = [&](int32_t off, int32_t len, std::vector<int>& out, int64_t c, std::string& err) {
+    for (int32_t j = 0; j < len; ++j) {
+      int32_t e = pool[off + j];
+      auto it = dense.find(e);
+      if (it == dense.end() || st[it->second] != 2) {
+        err = fmt_cmd(c) + ": D0 violated (signal on unmeasured qubit " + std::to_string(e) + ")";
+        return;
+      }
+      out.push_back(it->second);
+    }
+  };
+  for (int64_t c = 0; c < n_cmds; ++c) {
+    const owqs_cmd& k = cmds[c];
+    std::string err;
+    HCmd h;
+    h.kind = k.kind;
+    h.q0 = dense[k.q0];
+    if (k.kind == OWQS_CMD_N) {
+      if (st[h.q0] != 0) return fmt_cmd(c) + ": N on a prepared, input or measured qubit";
+      st[h.q0] = 1;
+      hp.cmds.push_back(h);
+      continue;
+    }
+    if (k.kind == OWQS_CMD_E) {
+      h.q1 = dense[k.q1];
+      need_live(h.q0, c, err);
+      if (err.empty()) need_live(h.q1, c, err);
+      if (!err.empty()) return err;
+      uint64_t a = std::min(h.q0, h.q1), b = std::max(h.q0, h.q1);
+      if (!epairs.insert((a << 32) | b).second) return fmt_cmd(c) + ": duplicate E on one qubit pair";
+      hp.cmds.push_back(h);
+      continue;
+    }
+    need_live(h.q0, c, err);
+    if (!err.empty()) return err;
+    dom(k.s_off, k.s_len, h.sdom, c, err);
+    if (!err.empty()) return err;
+    if (k.kind == OWQS_CMD_M) {
+      dom(k.t_off, k.t_len, h.tdom, c, err);
+      if (!err.empty()) return err;
+      if (hp.is_output[h.q0]) return fmt_cmd(c) + ": D3 violated (output qubit measured)";
+      h.angle = k.angle;
+      hp.m_ord_of_qubit[h.q0] = hp.n_measure++;
+      hp.cmds.push_back(h);
+      st[h.q0] = 2;
+      continue;
+    }
+    hp.cmds.push_back(h);  // X / Z
+  }
+  for (int q = 0; q < hp.nq; ++q) {
+    if (!hp.is_output[q] && st[q] != 2)
+      return "D3 violated: non-output qubit " + std::to_string(hp.ext_id[q]) + " is never measured";
+    if (hp.is_output[q] && st[q] == 0) {  // output never touched: |+> (R-11)
+      HCmd n;
+      n.kind = H_N;
+      n.q0 = q;
+      hp.cmds.push_back(n);
+      st[q] = 1;
+    }
+  }
+  hp.m_ord_of_cmd.assign(hp.cmds.size(), -1);
+  for (size_t c = 0; c < hp.cmds.size(); ++c)
+    if (hp.cmds[c].kind == H_M) hp.m_ord_of_cmd[c] = hp.m_ord_of_qubit[hp.cmds[c].q0];
+  return "";
+}
+
+// ------------------------------------------------------------------------------------------------
+// DAG of non-commuting commands on a shared qubit (Eqs. 14-16 and the Pauli relations) plus
+// signal edges M_v -> (command whose domain contains v) (D0, L79).
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+bool commute_on_shared(int ka, int kb) {
+  if (ka == H_N || kb == H_N || ka == H_M || kb == H_M) return false;
+  auto diag = [](int k) { return k == H_E || k == H_Z; };
+  if (diag(ka) && diag(kb)) return true;     // E-E (Eq. 15), E-Z, Z-Z
+  if (ka == H_X && kb == H_X) return true;   // X-X
+  return false;                              // E-X, X-Z (anticommute: phase)
+}
+
+struct Dag {
+  std::vector<std::vector<int>> pred;
+  std::vector<char> active;  // command participates in this mode's plan
+};
+
+Dag build_dag(const HostPattern& hp, bool eowqs) {
+  const int nc = (int)hp.cmds.size();
+  Dag g;
+  g.pred.assign(nc, {});
+  g.active.assign(nc, 1);
+  std::vector<std::vector<int>> on_qubit(hp.nq);
+  std::vector<int> m_cmd_of_qubit(hp.nq, -1);
+  for (int c = 0; c < nc; ++c) {
+    const HCmd& h = hp.cmds[c];
+    if (eowqs && (h.kind == H_X || h.kind == H_Z)) {  // signals are 0: corrections are identity
+      g.active[c] = 0;
+      continue;
+    }
+    int qs[2] = {h.q0, h.kind == H_E ? h.q1 : -1};
+    for (int qi = 0; qi < 2; ++qi) {
+      int q = qs[qi];
+      if (q < 0) continue;
+      for (int p : on_qubit[q])
+        if (!commute_on_shared(hp.cmds[p].kind, h.kind)) g.pred[c].push_back(p);
+      on_qubit[q].push_back(c);
+    }
+    if (!eowqs) {
+      for (int v : h.sdom) g.pred[c].push_back(m_cmd_of_qubit[v]);
+      for (int v : h.tdom) g.pred[c].push_back(m_cmd_of_qubit[v]);
+    }
+    if (h.kind == H_M) m_cmd_of_qubit[h.q0] = c;
+    auto& P = g.pred[c];
+    std::sort(P.begin(), P.end());
+    P.erase(std::unique(P.begin(), P.end()), P.end());
+  }
+  return g;
+}
+
+struct ProaRun {
+  Plan plan;
+};
+
+Plan proa_once(const HostPattern& hp, const Dag& g, bool eowqs, double A, double B, double G, double D) {
+  const int nc = (int)hp.cmds.size();
+  const int K = hp.n_measure;
+  const int words = (K + 63) / 64;
+  // M-ancestor bitsets (given order is a topological order)
+  std::vector<uint64_t> anc((size_t)nc * std::max(words, 1), 0);
+  for (int c = 0; c < nc; ++c) {
+    if (!g.active[c]) continue;
+    uint64_t* a = &anc[(size_t)c * words];
+    for (int p : g.pred[c]) {
+      const uint64_t* ap = &anc[(size_t)p * words];
+      for (int w = 0; w < words; ++w) a[w] |= ap[w];
+      int mo = hp.m_ord_of_cmd[p];
+      if (mo >= 0) a[mo >> 6] |= 1ull << (mo & 63);
+    }
+  }
+  std::vector<int> mcmd(K, -1);
+  for (int c = 0; c < nc; ++c)
+    if (hp.m_ord_of_cmd[c] >= 0) mcmd[hp.m_ord_of_cmd[c]] = c;
+  std::vector<int> blocked(K, 0);
+  std::vector<char> ready(K, 0), mdone(K, 0);
+  for (int k = 0; k < K; ++k) {
+    const uint64_t* a = &anc[(size_t)mcmd[k] * words];
+    int cnt = 0;
+    for (int w = 0; w < words; ++w) cnt += __builtin_popcountll(a[w]);
+    blocked[k] = cnt;
+    ready[k] = cnt == 0;
+  }
+  // incidence data for OS / flag / SS
+  std::vector<std::vector<int>> e_of_qubit(hp.nq);
+  std::vector<std::vector<int>> dependents(hp.nq);  // cmds whose domain contains the qubit
+  for (int c = 0; c < nc; ++c) {
+    if (!g.active[c]) continue;
+    const HCmd& h = hp.cmds[c];
+    if (h.kind == H_E) {
+      e_of_qubit[h.q0].push_back(c);
+      e_of_qubit[h.q1].push_back(c);
+    }
+    if (!eowqs) {
+      for (int v : h.sdom) dependents[v].push_back(c);
+      for (int v : h.tdom) dependents[v].push_back(c);
+    }
+  }
+  std::vector<char> done(nc, 0), measured(hp.nq, 0);
+  std::vector<int> visit_mark(nc, -1);
+  int live = (int)hp.inputs.size();
+  Plan plan;
+  plan.paper_m = live;
+  std::vector<int> stack, closure;
+  auto collect = [&](int root, int tag) {
+    closure.clear();
+    stack.clear();
+    stack.push_back(root);
+    visit_mark[root] = tag;
+    while (!stack.empty()) {
+      int c = stack.back();
+      stack.pop_back();
+      closure.push_back(c);
+      for (int p : g.pred[c])
+        if (!done[p] && visit_mark[p] != tag) {
+          visit_mark[p] = tag;
+          stack.push_back(p);
+        }
+    }
+  };
+  int tag = 0;
+  for (int step = 0; step < K; ++step) {
+    int best = -1;
+    double best_cost = 0;
+    int best_ms = 0;
+    for (int k = 0; k < K; ++k) {
+      if (!ready[k] || mdone[k]) continue;
+      collect(mcmd[k], ++tag);
+      int n_new = 0;
+      for (int c : closure)
+        if (hp.cmds[c].kind == H_N) ++n_new;
+      int v = hp.cmds[mcmd[k]].q0;
+      int ms = live + n_new;  // MS(v): width of the state that measuring v creates
+      int os = 0, flag = 0;
+      for (int e : e_of_qubit[v]) {
+        int w = hp.cmds[e].q0 == v ? hp.cmds[e].q1 : hp.cmds[e].q0;
+        if (!done[e] && hp.is_output[w]) ++os;
+        if (measured[w]) flag = 1;
+      }
+      std::unordered_set<int> ss;
+      for (int c : dependents[v])
+        if (!done[c]) ss.insert(hp.cmds[c].q0);
+      double cost = flag ? A * ms + B * os - G * (double)ss.size()
+                         : A * ((ms + 1) * D) + B * os - G * (double)ss.size();
+      bool better = best < 0 || cost < best_cost - 1e-12 ||
+                    (std::fabs(cost - best_cost) <= 1e-12 && hp.ext_id[v] < hp.ext_id[hp.cmds[mcmd[best]].q0]);
+      if (better) {
+        best = k;
+        best_cost = cost;
+        best_ms = ms;
+      }
+    }
+    // execute the closure of the chosen M in given order, then the M
+    collect(mcmd[best], ++tag);
+    std::sort(closure.begin(), closure.end());
+    for (int c : closure) {
+      done[c] = 1;
+      plan.order.push_back(c);
+      if (hp.cmds[c].kind == H_N) ++live;
+    }
+    plan.paper_m = std::max(plan.paper_m, best_ms);
+    plan.ms.push_back(best_ms);
+    plan.m_cmds.push_back(mcmd[best]);
+    measured[hp.cmds[mcmd[best]].q0] = 1;
+    --live;
+    mdone[best] = 1;
+    for (int k = 0; k < K; ++k) {
+      if (mdone[k] || ready[k]) continue;
+      const uint64_t* a = &anc[(size_t)mcmd[k] * words];
+      if (a[best >> 6] & (1ull << (best & 63))) {
+        if (--blocked[k] == 0) ready[k] = 1;
+      }
+    }
+  }
+  for (int c = 0; c < nc; ++c)
+    if (g.active[c] && !done[c]) {
+      done[c] = 1;
+      plan.order.push_back(c);
+      if (hp.cmds[c].kind == H_N) ++live;
+      plan.paper_m = std::max(plan.paper_m, live);
+    }
+  return plan;
+}
+
+}  // namespace
+
+Plan make_plan(const HostPattern& hp, bool eowqs, bool given_order, const ProaWeights& w) {
+  Dag g = build_dag(hp, eowqs);
+  if (given_order) {
+    Plan p;
+    int live = (int)hp.inputs.size();
+    p.paper_m = live;
+    for (size_t c = 0; c < hp.cmds.size(); ++c) {
+      if (!g.active[c]) continue;
+      p.order.push_back((int)c);
+      if (hp.cmds[c].kind == H_N) p.paper_m = std::max(p.paper_m, ++live);
+      if (hp.cmds[c].kind == H_M) {
+        p.m_cmds.push_back((int)c);
+        p.ms.push_back(live);
+        --live;
+      }
+    }
+    return p;
+  }
+  const double O = (double)hp.outputs.size();
+  double A0 = w.a >= 0 ? w.a : O, B0 = w.b >= 0 ? w.b : O, G0 = w.g, D0 = w.d >= 0 ? w.d : O;
+  if (A0 <= 0) A0 = 1;
+  if (D0 <= 0) D0 = 1;
+  int iters = w.tune ? std::max(1, (int)O) : 1;
+  Plan best;
+  bool have = false;
+  for (int it = 0; it < iters; ++it) {  // L487: alpha decreased by one |O| times, keep the best
+    double A = A0 - it;
+    if (A <= 0) break;
+    Plan p = proa_once(hp, g, eowqs, A, B0, G0, D0);
+    if (!have || p.paper_m < best.paper_m) {
+      best = std::move(p);
+      have = true;
+    }
+  }
+  return best;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Compiler: plan -> logical op stream with slot reuse -> device steps.
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+struct LOp {
+  int type;  // 1 DIAG_E, 2 DIAG_Z, 3 X, 4 BFLY, 10 GROW, 11 SHRINK
+  int a = -1, b = -1, m = -1;
+  std::vector<int> sig;  // given-order ordinals
+};
+
+struct Emitter {
+  const HostPattern& hp;
+  bool eowqs;
+  std::vector<int> qs;        // 0 unprepared, 1 fresh (N done, not in the array), 2 live, 3 measured
+  std::vector<int> slot_of;
+  std::vector<int> qubit_at;  // slot -> qubit
+  std::vector<std::vector<int>> pend;   // fresh q -> qubits with a pending E to q
+  std::vector<std::vector<int>> pnb;    // any q -> fresh qubits that have a pending E to q
+  std::vector<std::vector<std::vector<int>>> pendZ;  // fresh q -> pending Z signals
+  int width = 0, max_width = 0;
+  std::vector<LOp> ops;
+  std::vector<MStatic> mst;
+  std::vector<int32_t> pool;
+
+  Emitter(const HostPattern& h, bool e) : hp(h), eowqs(e) {
+    qs.assign(hp.nq, 0);
+    slot_of.assign(hp.nq, -1);
+    pend.assign(hp.nq, {});
+    pnb.assign(hp.nq, {});
+    pendZ.assign(hp.nq, {});
+    for (size_t k = 0; k < hp.inputs.size(); ++k) {
+      int q = hp.inputs[k];
+      qs[q] = 2;
+      slot_of[q] = (int)k;
+      qubit_at.push_back(q);
+    }
+    width = max_width = (int)hp.inputs.size();
+  }
+  std::vector<int> sig_of(const std::vector<int>& dom) const {
+    std::vector<int> s;
+    for (int v : dom) s.push_back(hp.m_ord_of_qubit[v]);
+    return s;
+  }
+  void diag_e(int u, int v) {
+    LOp o;
+    o.type = 1;
+    o.a = slot_of[u];
+    o.b = slot_of[v];
+    ops.push_back(o);
+  }
+  void diag_z(int q, const std::vector<int>& sig) {
+    LOp o;
+    o.type = 2;
+    o.a = slot_of[q];
+    o.sig = sig;
+    ops.push_back(o);
+  }
+  // apply a fresh qubit's deferred E's (to live qubits) and Z's after it got a slot
+  void flush_pending(int q, int skip) {
+    for (int w : pend[q]) {
+      if (w == skip) continue;
+      if (qs[w] == 2) diag_e(q, w);
+      // a fresh w keeps the edge in pend[w]
+    }
+    pend[q].clear();
+    for (auto& s : pendZ[q]) diag_z(q, s);
+    pendZ[q].clear();
+  }
+  void materialize(int q) {  // N made real: append |+> at the top slot (GROW)
+    LOp o;
+    o.type = 10;
+    o.a = width;
+    ops.push_back(o);
+    slot_of[q] = width;
+    qubit_at.push_back(q);
+    ++width;
+    max_width = std::max(max_width, width);
+    qs[q] = 2;
+    flush_pending(q, -1);
+  }
+  std::vector<int> fresh_neighbours(int v) {
+    std::vector<int> f;
+    for (int u : pnb[v])
+      if (qs[u] == 1 && std::find(pend[u].begin(), pend[u].end(), v) != pend[u].end() &&
+          std::find(f.begin(), f.end(), u) == f.end())
+        f.push_back(u);
+    return f;
+  }
+  void add_pending_edge(int u, int v) {  // at least one of u, v is fresh
+    if (qs[u] == 1) {
+      pend[u].push_back(v);
+      pnb[v].push_back(u);
+    }
+    if (qs[v] == 1) {
+      pend[v].push_back(u);
+      pnb[u].push_back(v);
+    }
+  }
+  void measure(int v, const HCmd& h) {
+    if (qs[v] == 1) materialize(v);
+    std::vector<int> F = fresh_neighbours(v);
+    MStatic ms{};
+    ms.alpha = h.angle;
+    ms.ord = hp.m_ord_of_qubit[v];
+    std::vector<int> s = eowqs ? std::vector<int>() : sig_of(h.sdom);
+    std::vector<int> t = eowqs ? std::vector<int>() : sig_of(h.tdom);
+    ms.s_off = (int)pool.size();
+    ms.s_len = (int)s.size();
+    pool.insert(pool.end(), s.begin(), s.end());
+    ms.t_off = (int)pool.size();
+    ms.t_len = (int)t.size();
+    pool.insert(pool.end(), t.begin(), t.end());
+    int m = (int)mst.size();
+    int b = slot_of[v];
+    if (!F.empty()) {
+      int o = F[0];
+      for (size_t i = 1; i < F.size(); ++i) materialize(F[i]);
+      ms.reuse = 1;
+      ms.structural = 1;
+      mst.push_back(ms);
+      LOp op;
+      op.type = 4;
+      op.a = b;
+      op.m = m;
+      ops.push_back(op);
+      qs[v] = 3;
+      slot_of[v] = -1;
+      qs[o] = 2;
+      slot_of[o] = b;
+      qubit_at[b] = o;
+      flush_pending(o, v);
+    } else {
+      ms.reuse = 0;
+      ms.structural = 0;
+      mst.push_back(ms);
+      LOp op;
+      op.type = 11;
+      op.a = b;
+      op.m = m;
+      ops.push_back(op);
+      int top = width - 1;
+      int tq = qubit_at[top];
+      qubit_at[b] = tq;
+      slot_of[tq] = b;
+      qubit_at.pop_back();
+      --width;
+      qs[v] = 3;
+      slot_of[v] = -1;
+    }
+  }
+  void run(const Plan& plan) {
+    for (int c : plan.order) {
+      const HCmd& h = hp.cmds[c];
+      switch (h.kind) {
+        case H_N:
+          qs[h.q0] = 1;
+          break;
+        case H_E:
+          if (qs[h.q0] == 2 && qs[h.q1] == 2)
+            diag_e(h.q0, h.q1);
+          else
+            add_pending_edge(h.q0, h.q1);
+          break;
+        case H_Z: {
+          if (eowqs || h.sdom.empty()) break;
+          auto s = sig_of(h.sdom);
+          if (qs[h.q0] == 2)
+            diag_z(h.q0, s);
+          else
+            pendZ[h.q0].push_back(s);
+          break;
+        }
+        case H_X: {
+          if (eowqs || h.sdom.empty()) break;
+          auto s = sig_of(h.sdom);
+          int q = h.q0;
+          if (qs[q] == 1) {
+            if (pend[q].empty() && pendZ[q].empty()) break;  // X|+> = |+>
+            materialize(q);
+          }
+          // X_q E_uq = E_uq X_q Z_u: deferred E's with fresh u pick up a conditional Z_u
+          for (int u : fresh_neighbours(q)) pendZ[u].push_back(s);
+          LOp o;
+          o.type = 3;
+          o.a = slot_of[q];
+          o.sig = s;
+          ops.push_back(o);
+          break;
+        }
+        case H_M:
+          measure(h.q0, h);
+          break;
+      }
+    }
+    for (int o : hp.outputs)
+      if (qs[o] == 1) materialize(o);
+  }
+};
+
+}  // namespace
+
+double Program::bytes_per_run(int eb) const {
+  double b = 0;
+  for (const auto& s : steps) {
+    double S = std::ldexp((double)eb, s.width);
+    if (s.kind == ST_PASS)
+      b += s.n_ops > 0 ? 2 * S : S;
+    else if (s.kind == ST_GROW)
+      b += 3 * S;
+    else
+      b += 1.5 * S;
+  }
+  return b;
+}
+
+Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse) {
+  const bool eowqs = mode == 2;
+  Emitter em(hp, eowqs);
+  em.run(plan);
+  Program pr;
+  pr.mst = em.mst;
+  pr.sig_pool = em.pool;
+  pr.phys_bits = em.max_width;
+  pr.in_width = (int)hp.inputs.size();
+  for (int o : hp.outputs) pr.out_slot.push_back(em.slot_of[o]);
+
+  // ---- pack into steps ----
+  int width = pr.in_width;
+  StepDesc cur{};
+  bool cur_open = false;
+  auto open = [&]() {
+    cur = StepDesc{};
+    cur.kind = ST_PASS;
+    cur.width = width;
+    cur.red_slot = -1;
+    cur.shrink_m = -1;
+    cur.slot = -1;
+    cur_open = true;
+  };
+  auto emit = [&](const StepDesc& s) {
+    pr.steps.push_back(s);
+    if (s.kind == ST_PASS) ++pr.n_passes;
+    if (s.kind == ST_GROW) ++pr.n_grow;
+    if (s.kind == ST_SHRINK) ++pr.n_shrink;
+  };
+  auto flush = [&](int red_kind, int red_slot) {
+    if (!cur_open) open();
+    if (cur.n_ops > 0 || red_kind != RED_NONE) {
+      cur.red_kind = red_kind;
+      cur.red_slot = red_slot;
+      emit(cur);
+    }
+    cur_open = false;
+  };
+  auto has_slot = [&](int a) {
+    if (a < SB) return true;
+    for (int j = 0; j < cur.nb_hi; ++j)
+      if (cur.bhi[j] == a) return true;
+    return false;
+  };
+  auto add_slot = [&](int a) -> bool {  // false if no room
+    if (has_slot(a)) return true;
+    if (cur.nb_hi >= KMAX_HI) return false;
+    int j = cur.nb_hi++;
+    cur.bhi[j] = a;
+    std::sort(cur.bhi, cur.bhi + cur.nb_hi);
+    return true;
+  };
+  auto push = [&](const LOp& l) {
+    Op o{};
+    o.type = (uint8_t)l.type;
+    o.a = (uint8_t)std::max(l.a, 0);
+    o.b = (uint8_t)std::max(l.b, 0);
+    o.m = l.m;
+    o.cond = l.sig.empty() ? 0 : 1;
+    o.sig_off = (int32_t)pr.sig_pool.size();
+    o.sig_len = (int32_t)l.sig.size();
+    pr.sig_pool.insert(pr.sig_pool.end(), l.sig.begin(), l.sig.end());
+    cur.ops[cur.n_ops++] = o;
+    if (l.type == 4) ++cur.n_bfly;
+  };
+  // Request a reduction of the state produced by the last emitted step (NORM), creating a
+  // read-only pass if the program has not emitted anything yet.
+  auto need_norm_before = [&]() {
+    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE) {
+      pr.steps.back().red_kind = RED_NORM;
+      return;
+    }
+    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NORM) return;
+    StepDesc r{};
+    r.kind = ST_PASS;
+    r.width = width;
+    r.red_kind = RED_NORM;
+    r.red_slot = -1;
+    r.slot = -1;
+    r.shrink_m = -1;
+    emit(r);
+  };
+  open();
+  for (const LOp& l : em.ops) {
+    if (l.type == 1 || l.type == 2) {
+      if (cur.n_ops >= MAX_OPS) flush(RED_NONE, -1), open();
+      push(l);
+    } else if (l.type == 3) {
+      if (cur.n_ops >= MAX_OPS || !add_slot(l.a)) {
+        flush(RED_NONE, -1);
+        open();
+        add_slot(l.a);
+      }
+      push(l);
+    } else if (l.type == 4) {  // slot-reuse butterfly
+      const MStatic& ms = pr.mst[l.m];
+      bool join = fuse && cur_open && cur.n_bfly > 0 && cur.n_bfly < MAX_BFLY && cur.n_ops < MAX_OPS &&
+                  (eowqs || ms.structural) && add_slot(l.a);
+      if (!join) {
+        if (!cur_open) open();
+        // everything before this butterfly goes into the previous pass (SURVEY §8(a) a6 rule)
+        flush(RED_NONE, -1);
+        if (!eowqs) need_norm_before();
+        open();
+        cur.first_uses_red = eowqs ? 0 : 1;
+        add_slot(l.a);
+      }
+      push(l);
+    } else if (l.type == 10) {  // GROW
+      flush(RED_NONE, -1);
+      StepDesc g{};
+      g.kind = ST_GROW;
+      g.width = width;  // old width; writes slot `width`
+      g.slot = l.a;
+      g.red_slot = -1;
+      g.shrink_m = -1;
+      emit(g);
+      ++width;
+      open();
+    } else if (l.type == 11) {  // SHRINK: needs rho of the measured slot (OWQS)
+      if (!eowqs) {
+        if (!cur_open) open();
+        if (cur.n_ops < MAX_OPS && add_slot(l.a)) {
+          flush(RED_RHO, l.a);
+        } else {
+          flush(RED_NONE, -1);
+          open();
+          add_slot(l.a);
+          flush(RED_RHO, l.a);
+        }
+      } else {
+        flush(RED_NONE, -1);
+      }
+      StepDesc s{};
+      s.kind = ST_SHRINK;
+      s.width = width;
+      s.slot = l.a;
+      s.shrink_m = l.m;
+      s.red_slot = -1;
+      s.first_uses_red = eowqs ? 0 : 1;
+      s.first_full_rho = eowqs ? 0 : 1;
+      emit(s);
+      --width;
+      open();
+    }
+  }
+  flush(RED_NONE, -1);
+  // final norm of the output state (EOWQS determinism check / drift report), fused when possible
+  if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE)
+    pr.steps.back().red_kind = RED_NORM;
+  else if (pr.steps.empty() || pr.steps.back().red_kind != RED_NORM) {
+    StepDesc r{};
+    r.kind = ST_PASS;
+    r.width = width;
+    r.red_kind = RED_NORM;
+    r.red_slot = -1;
+    r.slot = -1;
+    r.shrink_m = -1;
+    emit(r);
+  }
+  for (const auto& s : pr.steps)
+    if (s.red_kind != RED_NONE) ++pr.n_reduce;
+  return pr;
+}
+
+}  // namespace owqs

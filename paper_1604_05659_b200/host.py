@@ -1,0 +1,55 @@
+"""Binding of include/owqs_host.h: the scheduler's output (PROA plan, compiled step program) without a
+GPU. Marshalling only; the scheduler itself is C++ inside libowqs.so."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+from . import _capi
+from .owqs import OwqsError, lib, marshal_pattern
+
+MODE_IDS = _capi.MODES
+
+
+@dataclass
+class HostProgram:
+    info: dict
+    steps: List[_capi.StepDesc]
+    mst: List[_capi.MStatic]
+    sig: List[int]
+    out_slot: List[int]
+    plan_qubits: List[int]
+    plan_ms: List[int]
+
+
+def compile_host(pattern, mode: str = "sampled", precision: int = 128, flags: int = 0,
+                 weights: Optional[Sequence[float]] = None) -> HostProgram:
+    L = lib()
+    i, o, arr, pool, plen = marshal_pattern(pattern.inputs, pattern.outputs, pattern.cmds)
+    w = (C.c_double * 4)(*weights) if weights is not None else None
+    h = C.c_void_p()
+    st = L.owqs_host_compile(i, len(pattern.inputs), o, len(pattern.outputs), arr, len(pattern.cmds), pool, plen,
+                             MODE_IDS[mode], precision, flags, w, C.byref(h))
+    try:
+        if st != 0:
+            msg = L.owqs_host_error(h) if h else b""
+            raise OwqsError(st, msg.decode() if msg else "")
+        info = _capi.owqs_host_info()
+        L.owqs_host_info_get(h, C.byref(info))
+        assert info.step_bytes == C.sizeof(_capi.StepDesc), "StepDesc layout mismatch"
+        assert info.mstatic_bytes == C.sizeof(_capi.MStatic), "MStatic layout mismatch"
+        steps = (_capi.StepDesc * max(1, info.n_steps))()
+        mst = (_capi.MStatic * max(1, info.n_measure))()
+        sig = (C.c_int32 * max(1, info.sig_len))()
+        out_slot = (C.c_int32 * max(1, info.n_out))()
+        pq = (C.c_int32 * max(1, info.n_measure))()
+        pm = (C.c_int32 * max(1, info.n_measure))()
+        L.owqs_host_program(h, steps, mst, sig, out_slot, pq, pm)
+        d = {k: getattr(info, k) for k, _ in _capi.owqs_host_info._fields_}
+        K = info.n_measure
+        return HostProgram(d, list(steps)[:info.n_steps], list(mst)[:K], list(sig)[:info.sig_len],
+                           list(out_slot)[:info.n_out], list(pq)[:K], list(pm)[:K])
+    finally:
+        if h:
+            L.owqs_host_free(h)

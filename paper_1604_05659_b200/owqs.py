@@ -1,0 +1,162 @@
+"""Thin Python binding of libowqs.so (include/owqs.h). Marshalling only: every step of the hot path
+runs in the library's sm_100a kernels; there is no CPU fallback."""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional, Sequence, Tuple
+
+import numpy as np
+
+from . import _capi
+from ._capi import MODES, STATUS_NAMES, owqs_cmd, owqs_config, owqs_stats_t
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        _lib = _capi.load_library()
+    return _lib
+
+
+class OwqsError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+        self.status_name = STATUS_NAMES.get(status, str(status))
+
+
+def _i32(a: Sequence[int]):
+    arr = (C.c_int32 * max(1, len(a)))(*a)
+    return arr
+
+
+def marshal_pattern(inputs, outputs, cmds):
+    """cmds: objects with kind, q0, q1, angle, sdom, tdom (workloads.patterns.Cmd or alike)."""
+    pool = []
+    arr = (owqs_cmd * max(1, len(cmds)))()
+    for i, c in enumerate(cmds):
+        x = arr[i]
+        x.kind, x.q0, x.q1 = int(c.kind), int(c.q0), int(c.q1)
+        x.angle = float(c.angle)
+        sd, td = tuple(getattr(c, "sdom", ()) or ()), tuple(getattr(c, "tdom", ()) or ())
+        x.s_off, x.s_len = len(pool), len(sd)
+        pool += [int(v) for v in sd]
+        x.t_off, x.t_len = len(pool), len(td)
+        pool += [int(v) for v in td]
+    return _i32(inputs), _i32(outputs), arr, _i32(pool), len(pool)
+
+
+class Simulator:
+    """One owqs context (one GPU, one pattern at a time)."""
+
+    def __init__(self, precision: int = 128, device: int = 0, flags: int = 0, stream: Optional[int] = None):
+        self._lib = lib()
+        cfg = owqs_config()
+        cfg.precision = precision
+        cfg.n_ranks, cfg.rank, cfg.device = 1, 0, device
+        cfg.flags = flags
+        cfg.stream = stream
+        h = C.c_void_p()
+        st = self._lib.owqs_create(C.byref(cfg), C.byref(h))
+        if st != 0:
+            raise OwqsError(st, "owqs_create failed (is a CUDA device visible?)")
+        self._h = h
+        self.precision = precision
+        self.n_in = self.n_out = 0
+        self.n_measure = 0
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.owqs_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st != 0:
+            msg = self._lib.owqs_last_error(self._h)
+            raise OwqsError(st, msg.decode() if msg else "")
+
+    # -- boundary calls ------------------------------------------------------------------------
+    def load_pattern(self, inputs, outputs, cmds):
+        i, o, arr, pool, plen = marshal_pattern(inputs, outputs, cmds)
+        self._check(self._lib.owqs_load_pattern(self._h, i, len(inputs), o, len(outputs), arr, len(cmds), pool, plen))
+        self.n_in, self.n_out = len(inputs), len(outputs)
+        nm = C.c_int64()
+        self._check(self._lib.owqs_pattern_info(self._h, C.byref(nm), None, None, None))
+        self.n_measure = nm.value
+
+    def load(self, pattern):
+        self.load_pattern(pattern.inputs, pattern.outputs, pattern.cmds)
+
+    def set_input(self, amps: np.ndarray):
+        a = np.ascontiguousarray(amps, dtype=np.complex128)
+        self._check(self._lib.owqs_set_input(self._h, a.ctypes.data_as(C.POINTER(C.c_double)), a.size))
+
+    def set_input_device(self, ptr: int, precision: int, n: int):
+        self._check(self._lib.owqs_set_input_device(self._h, C.c_void_p(ptr), precision, n))
+
+    def set_input_random(self, seed: int):
+        self._check(self._lib.owqs_set_input_random(self._h, C.c_uint64(seed)))
+
+    def run(self, mode: str = "sampled", seed: int = 0, forced: Optional[Sequence[int]] = None,
+            want: bool = True) -> Tuple[Optional[np.ndarray], Optional[np.ndarray]]:
+        K = self.n_measure
+        f = None
+        if forced is not None:
+            fa = np.ascontiguousarray(np.asarray(forced, dtype=np.uint8))
+            if fa.size != K:
+                raise ValueError("forced must have one entry per M")
+            f = fa.ctypes.data_as(C.POINTER(C.c_uint8))
+        out = np.zeros(max(K, 1), dtype=np.uint8) if want else None
+        p0 = np.zeros(max(K, 1), dtype=np.float64) if want else None
+        st = self._lib.owqs_run(self._h, MODES[mode], C.c_uint64(seed & (2 ** 64 - 1)), f,
+                                out.ctypes.data_as(C.POINTER(C.c_uint8)) if want else None,
+                                p0.ctypes.data_as(C.POINTER(C.c_double)) if want else None)
+        self._check(st)
+        return (out[:K], p0[:K]) if want else (None, None)
+
+    def get_output(self) -> np.ndarray:
+        out = np.empty(2 ** self.n_out, dtype=np.complex128)
+        self._check(self._lib.owqs_get_output(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+        return out
+
+    def get_output_device(self, ptr: int, precision: int, n: int):
+        self._check(self._lib.owqs_get_output_device(self._h, C.c_void_p(ptr), precision, n))
+
+    def inner(self, other: "Simulator") -> complex:
+        re, im = C.c_double(), C.c_double()
+        self._check(self._lib.owqs_output_inner(self._h, other._h, C.byref(re), C.byref(im)))
+        return complex(re.value, im.value)
+
+    def recognize(self) -> Tuple[np.ndarray, float]:
+        U = np.empty((2 ** self.n_in, 2 ** self.n_out), dtype=np.complex128)  # column-major storage
+        err = C.c_double()
+        self._check(self._lib.owqs_recognize(self._h, U.ctypes.data_as(C.POINTER(C.c_double)), U.size, C.byref(err)))
+        return U.T.copy(), err.value
+
+    def pattern_info(self) -> dict:
+        nm, pm, pb, npass = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
+        self._check(self._lib.owqs_pattern_info(self._h, C.byref(nm), C.byref(pm), C.byref(pb), C.byref(npass)))
+        return {"n_measure": nm.value, "paper_m": pm.value, "phys_bits": pb.value, "n_passes": npass.value}
+
+    def plan_order(self, mode: str = "sampled") -> Tuple[list, list]:
+        K = self.n_measure
+        q = (C.c_int32 * max(1, K))()
+        ms = (C.c_int32 * max(1, K))()
+        self._check(self._lib.owqs_plan_order(self._h, MODES[mode], q, ms, K))
+        return list(q)[:K], list(ms)[:K]
+
+    def set_proa_weights(self, a: float, b: float, g: float, d: float, tune: bool = True):
+        self._check(self._lib.owqs_set_proa_weights(self._h, a, b, g, d, int(tune)))
+
+    def stats(self) -> dict:
+        s = owqs_stats_t()
+        self._check(self._lib.owqs_stats(self._h, C.byref(s)))
+        return {k: getattr(s, k) for k, _ in owqs_stats_t._fields_ if k != "reserved"}

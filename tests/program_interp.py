@@ -1,0 +1,162 @@
+"""TEST-ONLY numpy interpreter of the compiled device step program (include/owqs_host.h).
+
+It executes the steps exactly as the kernels define them (ops on slots, decisions in the pass
+prologue, reductions of the step output, grow / shrink), so that the host scheduler + compiler
+can be checked against the oracle on a machine without a GPU. It is not a product path (the
+product has no CPU fallback) and it shares no code with the oracle.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+OP_DIAG_E, OP_DIAG_Z, OP_X, OP_BFLY = 1, 2, 3, 4
+ST_PASS, ST_GROW, ST_SHRINK = 0, 1, 2
+RED_NONE, RED_NORM, RED_RHO = 0, 1, 2
+
+
+def _splitmix64(x):
+    m = (1 << 64) - 1
+    z = (x + 0x9E3779B97F4A7C15) & m
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & m
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & m
+    return z ^ (z >> 31)
+
+
+def _draw(seed, ord_):
+    return (_splitmix64(seed ^ _splitmix64(ord_)) >> 11) * 2.0 ** -53
+
+
+class Interp:
+    def __init__(self, prog, mode: str, seed: int = 0, forced=None):
+        self.p = prog
+        self.mode = {"sampled": 0, "forced": 1, "eowqs": 2}[mode]
+        self.seed = seed
+        K = prog.info["n_measure"]
+        self.forced = np.zeros(K, np.uint8) if forced is None else np.asarray(forced, np.uint8)
+        self.outcome = np.zeros(K, np.uint8)
+        self.prob0 = np.zeros(K)
+        self.red = np.zeros(4)
+        self.err = 0
+
+    def parity(self, off, ln, loc):
+        s = 0
+        for o in self.p.sig[off:off + ln]:
+            s ^= loc[o] if o in loc else int(self.outcome[o])
+        return s & 1
+
+    def decide(self, m, use_red, full, loc):
+        ms = self.p.mst[m]
+        s = t = 0
+        if self.mode != 2:
+            s = self.parity(ms.s_off, ms.s_len, loc)
+            t = self.parity(ms.t_off, ms.t_len, loc)
+        theta = (-ms.alpha if s else ms.alpha) + (math.pi if t else 0.0)
+        e = complex(math.cos(theta), -math.sin(theta))
+        outc, pS, P0 = 0, 0.5, -1.0
+        if self.mode != 2:
+            if full:
+                tot = self.red[0] + self.red[1]
+                P0 = 0.5 * tot + (e * complex(self.red[2], self.red[3])).real
+                P0 = min(max(P0, 0.0), tot)
+                P1 = tot - P0
+            else:
+                nrm = self.red[0] if use_red else 1.0
+                P0 = P1 = 0.5 * nrm
+            outc = (0 if _draw(self.seed, ms.ord) <= P0 else 1) if self.mode == 0 else int(self.forced[ms.ord]) & 1
+            pS = P1 if outc else P0
+            if pS < 1e-12:
+                self.err = 1
+                pS = 1.0
+        sg = -1.0 if outc else 1.0
+        if ms.reuse:
+            k = (1 / math.sqrt(2)) if self.mode == 2 else 0.5 / math.sqrt(pS)
+            U = np.array([[k, k * sg * e], [k, -k * sg * e]])
+        else:
+            k = 1.0 if self.mode == 2 else 1 / math.sqrt(2 * pS)
+            U = np.array([[k, k * sg * e], [0, 0]])
+        self.outcome[ms.ord] = outc
+        self.prob0[ms.ord] = P0
+        loc[ms.ord] = outc
+        return U
+
+    def run(self, psi):
+        st = np.zeros(2 ** self.p.info["phys_bits"], dtype=np.complex128)
+        st[: psi.size] = psi
+        for d in self.p.steps:
+            w = d.width
+            n = 1 << w
+            if d.kind == ST_PASS:
+                loc, coefs, conds = {}, {}, {}
+                bi = 0
+                for i in range(d.n_ops):
+                    op = d.ops[i]
+                    if op.type == OP_BFLY:
+                        coefs[i] = self.decide(op.m, bi == 0 and d.first_uses_red, False, loc)
+                        bi += 1
+                    else:
+                        conds[i] = self.parity(op.sig_off, op.sig_len, loc) if op.cond else 1
+                v = st[:n].copy()
+                idx = np.arange(n)
+                for i in range(d.n_ops):
+                    op = d.ops[i]
+                    if op.type in (OP_DIAG_E, OP_DIAG_Z):
+                        if not conds[i]:
+                            continue
+                        b = op.b if op.type == OP_DIAG_E else op.a
+                        mask = ((idx >> op.a) & (idx >> b) & 1).astype(bool)
+                        v[mask] = -v[mask]
+                    else:
+                        if op.type == OP_X and not conds[i]:
+                            continue
+                        U = coefs[i] if op.type == OP_BFLY else np.array([[0, 1], [1, 0]])
+                        a = op.a
+                        i0 = idx[((idx >> a) & 1) == 0]
+                        i1 = i0 | (1 << a)
+                        x0, x1 = v[i0].copy(), v[i1].copy()
+                        v[i0] = U[0, 0] * x0 + U[0, 1] * x1
+                        v[i1] = U[1, 0] * x0 + U[1, 1] * x1
+                if d.n_ops > 0:
+                    st[:n] = v
+                self._reduce(d, v, idx)
+            elif d.kind == ST_GROW:
+                x = st[:n] / math.sqrt(2)
+                st[:n] = x
+                st[n:2 * n] = x
+                if d.red_kind == RED_NORM:
+                    self.red[:] = [np.vdot(st[:2 * n], st[:2 * n]).real, 0, 0, 0]
+            else:
+                U = self.decide(d.shrink_m, True, bool(d.first_full_rho), {})
+                b, top = d.slot, w - 1
+                v = st[:n].copy()
+                idx = np.arange(n)
+                if b == top:
+                    h = n // 2
+                    st[:h] = U[0, 0] * v[:h] + U[0, 1] * v[h:]
+                else:
+                    r = idx[(((idx >> b) & 1) == 0) & (((idx >> top) & 1) == 0)]
+                    B, T = 1 << b, 1 << top
+                    st[r] = U[0, 0] * v[r] + U[0, 1] * v[r | B]
+                    st[r | B] = U[0, 0] * v[r | T] + U[0, 1] * v[r | B | T]
+                if d.red_kind == RED_NORM:
+                    h = n // 2
+                    self.red[:] = [np.vdot(st[:h], st[:h]).real, 0, 0, 0]
+        n_out = self.p.info["n_out"]
+        j = np.arange(2 ** n_out)
+        src = np.zeros_like(j)
+        for k, s in enumerate(self.p.out_slot):
+            src |= ((j >> k) & 1) << s
+        return st[src]
+
+    def _reduce(self, d, v, idx):
+        if d.red_kind == RED_NORM:
+            self.red[:] = [np.vdot(v, v).real, 0, 0, 0]
+        elif d.red_kind == RED_RHO:
+            r = d.red_slot
+            b = ((idx >> r) & 1).astype(bool)
+            n0 = np.vdot(v[~b], v[~b]).real
+            n1 = np.vdot(v[b], v[b]).real
+            i0 = idx[~b]
+            c = np.vdot(v[i0], v[i0 | (1 << r)])
+            self.red[:] = [n0, n1, c.real, c.imag]

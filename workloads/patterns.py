@@ -303,3 +303,71 @@ def config_pattern(name: str, seed: int = 1) -> Pattern:
         raise KeyError(name)
     p.meta["seed"] = seed
     return p
+
+
+def random_general_pattern(seed: int, n_in: int = 2, n_total: int = 9, n_out: int = 2,
+                           max_live: int = 7, p_corr: float = 0.3) -> Pattern:
+    """A random pattern that obeys D0-D3 but is neither standard-form nor
+    deterministic: interleaved N / E / M / X / Z commands with random signal domains over the
+    qubits measured so far. Used to drive every branch of the scheduler (grow, shrink, pending
+    E's and Z's, corrections on fresh qubits) against the oracle."""
+    rng = np.random.default_rng(seed)
+    qubits = list(range(n_total))
+    outputs = [int(q) for q in rng.choice(qubits, size=n_out, replace=False)]
+    inputs = list(range(n_in))
+    prepared = set(inputs)
+    measured: list = []
+    edges = set()
+    cmds: List[Cmd] = []
+
+    def dom():
+        if not measured or rng.uniform() < 0.4:
+            return ()
+        k = int(rng.integers(1, min(3, len(measured)) + 1))
+        return tuple(int(x) for x in rng.choice(measured, size=k, replace=False))
+
+    to_measure = [q for q in qubits if q not in outputs]
+    guard = 0
+    while to_measure and guard < 10000:
+        guard += 1
+        live = [q for q in prepared if q not in measured]
+        unprep = [q for q in qubits if q not in prepared]
+        r = rng.uniform()
+        if r < 0.25 and unprep and len(live) < max_live:
+            q = int(rng.choice(unprep))
+            cmds.append(N(q))
+            prepared.add(q)
+        elif r < 0.55 and len(live) + (1 if unprep else 0) >= 2:
+            pool = live + ([int(rng.choice(unprep))] if unprep and len(live) < max_live else [])
+            if len(pool) < 2:
+                continue
+            a, b = (int(x) for x in rng.choice(pool, size=2, replace=False))
+            key = (min(a, b), max(a, b))
+            if key in edges:
+                continue
+            edges.add(key)
+            cmds.append(E(a, b))
+            prepared.update((a, b))
+        elif r < 0.55 + p_corr * 0.5 and live:
+            q = int(rng.choice(live))
+            d = dom()
+            if d:
+                cmds.append((X if rng.uniform() < 0.5 else Z)(q, d))
+        else:
+            cand = [q for q in live if q in to_measure]
+            if not cand:
+                continue
+            q = int(rng.choice(cand))
+            cmds.append(M(q, float(rng.uniform(0, 2 * math.pi)), dom(), dom()))
+            measured.append(q)
+            to_measure.remove(q)
+    # remaining non-outputs that were never prepared: prepare + measure
+    for q in to_measure:
+        cmds.append(M(q, float(rng.uniform(0, 2 * math.pi))))
+        measured.append(q)
+    live_out = [q for q in outputs]
+    for q in live_out:
+        d = dom()
+        if d and rng.uniform() < 0.5:
+            cmds.append((X if rng.uniform() < 0.5 else Z)(q, d))
+    return Pattern(inputs, outputs, cmds, f"random{seed}")
