@@ -86,6 +86,15 @@ typedef struct {
 #define OWQS_FLAG_NO_FUSE     0x2u /* at most one measurement butterfly per state pass          */
 #define OWQS_FLAG_GIVEN_ORDER 0x4u /* skip PROA: execute measurements in the given order         */
 #define OWQS_FLAG_NO_TUNE     0x8u /* PROA with the initial weights only (no L487 tuning loop)   */
+#define OWQS_FLAG_PROFILE     0x10u /* record a CUDA event after every kernel of owqs_run (event
+                                       record nodes in the graph); see owqs_launch_profile       */
+
+/* Kernel classes reported by owqs_launch_profile. */
+#define OWQS_KCLASS_PASS   0 /* fused warp-segment pass kernel (read + write the state)          */
+#define OWQS_KCLASS_SMALL  1 /* one-CTA shared-memory pass for widths <= 12                      */
+#define OWQS_KCLASS_GROW   2 /* append |+> (N without a measurement to absorb it)                 */
+#define OWQS_KCLASS_SHRINK 3 /* measurement with elimination (no fresh neighbour)                 */
+#define OWQS_KCLASS_REDUCE 4 /* read-only pass: probability / norm reduction only                 */
 
 typedef enum { OWQS_SAMPLED = 0, OWQS_FORCED = 1, OWQS_EOWQS = 2 } owqs_mode;
 
@@ -175,6 +184,12 @@ owqs_status owqs_plan_order(owqs_ctx* ctx, owqs_mode mode, int32_t* qubits, int3
 owqs_status owqs_set_proa_weights(owqs_ctx* ctx, double a, double b, double g, double d, int32_t tune);
 
 owqs_status owqs_stats(owqs_ctx* ctx, owqs_stats_t* out);
+
+/* Per-launch profile of the last owqs_run of a context created with OWQS_FLAG_PROFILE: for launch
+ * i (i < n, n >= stats.n_launches) its kernel class (OWQS_KCLASS_*), its algorithmic HBM bytes
+ * (read + write of the state it sweeps) and its device duration in ms measured by
+ * CUDA events on the library's stream. Any pointer may be NULL. OWQS_E_STATE if not profiled. */
+owqs_status owqs_launch_profile(owqs_ctx* ctx, int32_t* kclass, double* bytes, float* ms, int64_t n);
 const char* owqs_last_error(const owqs_ctx* ctx);
 const char* owqs_version(void);
 

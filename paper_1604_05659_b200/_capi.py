@@ -12,13 +12,14 @@ STATUS_NAMES = {0: "OWQS_OK", 1: "OWQS_E_ARG", 2: "OWQS_E_PATTERN", 3: "OWQS_E_N
                 5: "OWQS_E_STATE", 6: "OWQS_E_NOMEM", 7: "OWQS_E_CUDA", 8: "OWQS_E_NCCL",
                 9: "OWQS_E_NOT_DETERMINISTIC"}
 MODES = {"sampled": 0, "forced": 1, "eowqs": 2}
-FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE = 1, 2, 4, 8
+FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE = 1, 2, 4, 8, 16
+KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = ["owqs_create", "owqs_destroy", "owqs_load_pattern", "owqs_set_input", "owqs_set_input_device",
             "owqs_set_input_random", "owqs_run", "owqs_get_output", "owqs_get_output_device",
             "owqs_output_inner", "owqs_recognize", "owqs_pattern_info", "owqs_plan_order",
-            "owqs_set_proa_weights", "owqs_stats", "owqs_last_error", "owqs_version"]
+            "owqs_set_proa_weights", "owqs_stats", "owqs_launch_profile", "owqs_last_error", "owqs_version"]
 
 
 class owqs_cmd(C.Structure):
@@ -67,6 +68,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "owqs_plan_order": (C.c_int, [ctx, C.c_int, P(C.c_int32), P(C.c_int32), C.c_int64]),
         "owqs_set_proa_weights": (C.c_int, [ctx, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32]),
         "owqs_stats": (C.c_int, [ctx, P(owqs_stats_t)]),
+        "owqs_launch_profile": (C.c_int, [ctx, P(C.c_int32), P(C.c_double), P(C.c_float), C.c_int64]),
         "owqs_last_error": (C.c_char_p, [ctx]),
         "owqs_version": (C.c_char_p, []),
     }

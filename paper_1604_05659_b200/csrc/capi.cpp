@@ -23,6 +23,7 @@ cudaError_t launch_convert_in(const void* src, int src_prec, void* state, int pr
 cudaError_t launch_basis(void* state, int prec, uint64_t n, uint64_t k, cudaStream_t s);
 cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, cudaStream_t s);
 cudaError_t launch_dot(const DevPtrs& p, const void* a, const void* b, uint64_t n, cudaStream_t s);
+int step_kclass(const StepDesc& d, int prec);
 }  // namespace owqs
 
 using namespace owqs;
@@ -69,6 +70,8 @@ struct owqs_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   owqs_stats_t stats{};
   int last_cm = 0;
+  std::vector<cudaEvent_t> prof_ev;  // OWQS_FLAG_PROFILE: event after every launch (+1 start)
+  int prof_cm = -1;
 };
 
 namespace {
@@ -194,16 +197,42 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
   CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int32_t), ctx->stream));
   DevPtrs p = dev_ptrs(ctx, m);
   const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH);
+  const bool prof = (ctx->cfg.flags & OWQS_FLAG_PROFILE) != 0;
+  if (prof) {
+    if (ctx->prof_cm != cmi) {
+      // event lists are per compiled mode: rebuild (and drop this mode's graph) on a mode switch
+      if (m.gexec) {
+        cudaGraphExecDestroy(m.gexec);
+        m.gexec = nullptr;
+      }
+    }
+    while (ctx->prof_ev.size() < m.prog.steps.size() + 1) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      ctx->prof_ev.push_back(e);
+    }
+    ctx->prof_cm = cmi;
+  }
+  auto launch_all = [&](bool capturing) -> cudaError_t {
+    cudaError_t e = cudaSuccess;
+    if (prof) e = capturing ? cudaEventRecordWithFlags(ctx->prof_ev[0], ctx->stream, cudaEventRecordExternal)
+                            : cudaEventRecord(ctx->prof_ev[0], ctx->stream);
+    for (size_t i = 0; i < m.prog.steps.size() && e == cudaSuccess; ++i) {
+      e = launch_step(m.prog.steps[i], p, ctx->prec, ctx->stream);
+      if (e == cudaSuccess && prof)
+        e = capturing ? cudaEventRecordWithFlags(ctx->prof_ev[i + 1], ctx->stream, cudaEventRecordExternal)
+                      : cudaEventRecord(ctx->prof_ev[i + 1], ctx->stream);
+    }
+    return e;
+  };
   if (use_graph && !m.gexec) {
     cudaGraph_t g = nullptr;
     CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    for (const auto& s : m.prog.steps) {
-      cudaError_t e = launch_step(s, p, ctx->prec, ctx->stream);
-      if (e != cudaSuccess) {
-        cudaStreamEndCapture(ctx->stream, &g);
-        if (g) cudaGraphDestroy(g);
-        return fail(ctx, OWQS_E_CUDA, std::string("launch during capture: ") + cudaGetErrorString(e));
-      }
+    cudaError_t e = launch_all(true);
+    if (e != cudaSuccess) {
+      cudaStreamEndCapture(ctx->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      return fail(ctx, OWQS_E_CUDA, std::string("launch during capture: ") + cudaGetErrorString(e));
     }
     CU(cudaStreamEndCapture(ctx->stream, &g));
     CU(cudaGraphInstantiate(&m.gexec, g, 0));
@@ -213,7 +242,7 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
   if (use_graph) {
     CU(cudaGraphLaunch(m.gexec, ctx->stream));
   } else {
-    for (const auto& s : m.prog.steps) CU(launch_step(s, p, ctx->prec, ctx->stream));
+    CU(launch_all(false));
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -237,16 +266,27 @@ owqs_status output_to_device(owqs_ctx* ctx, void* dst, int dst_prec, uint64_t j0
   return OWQS_OK;
 }
 
+bool is_pinned_host(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
   const uint64_t n = 1ull << ctx->hp.outputs.size();
   const uint64_t chunk = kStagingBytes / 16;
+  const bool pinned = is_pinned_host(amps);  // page-locked caller buffer: DMA straight into it
   for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
     uint64_t cnt = std::min(chunk, n - j0);
     owqs_status s = output_to_device(ctx, ctx->d_staging, 1, j0, cnt);
     if (s != OWQS_OK) return s;
-    CU(cudaMemcpyAsync(ctx->h_staging, ctx->d_staging, cnt * 16, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaMemcpyAsync(pinned ? (void*)(amps + 2 * j0) : ctx->h_staging, ctx->d_staging, cnt * 16,
+                       cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
-    memcpy(amps + 2 * j0, ctx->h_staging, cnt * 16);
+    if (!pinned) memcpy(amps + 2 * j0, ctx->h_staging, cnt * 16);
   }
   return OWQS_OK;
 }
@@ -311,6 +351,7 @@ void owqs_destroy(owqs_ctx* ctx) {
   cudaFree(ctx->d_forced);
   cudaFree(ctx->d_staging);
   if (ctx->h_staging) cudaFreeHost(ctx->h_staging);
+  for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -568,6 +609,27 @@ owqs_status owqs_set_proa_weights(owqs_ctx* ctx, double a, double b, double g, d
     owqs_status s = compile_modes(ctx);
     if (s != OWQS_OK) return s;
     ctx->has_input = ctx->has_output = false;
+  }
+  return OWQS_OK;
+}
+
+owqs_status owqs_launch_profile(owqs_ctx* ctx, int32_t* kclass, double* bytes, float* ms, int64_t n) {
+  if (!ctx) return OWQS_E_ARG;
+  if (!(ctx->cfg.flags & OWQS_FLAG_PROFILE) || ctx->prof_cm < 0 || !ctx->has_output)
+    return fail(ctx, OWQS_E_STATE, "no profiled run (create the context with OWQS_FLAG_PROFILE)");
+  const Program& pr = ctx->cm[ctx->prof_cm].prog;
+  if (n < (int64_t)pr.steps.size()) return fail(ctx, OWQS_E_ARG, "arrays smaller than the launch count");
+  for (size_t i = 0; i < pr.steps.size(); ++i) {
+    const StepDesc& s = pr.steps[i];
+    const double S = std::ldexp((double)ctx->elem, s.width);
+    int kc = step_kclass(s, ctx->prec);
+    if (kclass) kclass[i] = kc;
+    if (bytes) bytes[i] = s.kind == ST_GROW ? 3 * S : s.kind == ST_SHRINK ? 1.5 * S : (s.n_ops > 0 ? 2 * S : S);
+    if (ms) {
+      float t = 0;
+      CU(cudaEventElapsedTime(&t, ctx->prof_ev[i], ctx->prof_ev[i + 1]));
+      ms[i] = t;
+    }
   }
   return OWQS_OK;
 }

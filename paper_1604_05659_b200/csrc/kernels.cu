@@ -696,6 +696,16 @@ int max_partial_blocks() { return 16 * 148 * 2; }
 static inline int unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
 static inline int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; }
 
+// Kernel class of a step (OWQS_KCLASS_* of include/owqs.h).
+int step_kclass(const StepDesc& d, int prec) {
+  const int SB = prec == 0 ? 6 : 5;
+  if (d.kind == ST_GROW) return 2;
+  if (d.kind == ST_SHRINK) return 3;
+  const int slack = d.width - SB - d.nb_hi - log2i(unr_of(d.nb_hi));
+  if (slack < 0) return 1;
+  return d.n_ops == 0 ? 4 : 0;
+}
+
 // Launch one step. prec: 0 complex64, 1 complex128.
 cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s) {
   const int SB = prec == 0 ? 6 : 5;

@@ -122,8 +122,10 @@ class Simulator:
         self._check(st)
         return (out[:K], p0[:K]) if want else (None, None)
 
-    def get_output(self) -> np.ndarray:
-        out = np.empty(2 ** self.n_out, dtype=np.complex128)
+    def get_output(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        if out is None:
+            out = np.empty(2 ** self.n_out, dtype=np.complex128)
+        assert out.dtype == np.complex128 and out.flags.c_contiguous and out.size >= 2 ** self.n_out
         self._check(self._lib.owqs_get_output(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
         return out
 
@@ -155,6 +157,17 @@ class Simulator:
 
     def set_proa_weights(self, a: float, b: float, g: float, d: float, tune: bool = True):
         self._check(self._lib.owqs_set_proa_weights(self._h, a, b, g, d, int(tune)))
+
+    def launch_profile(self):
+        """(kclass[n], bytes[n], ms[n]) of the last run of a context created with FLAG_PROFILE."""
+        n = self.stats()["n_launches"]
+        kc = np.zeros(max(n, 1), dtype=np.int32)
+        by = np.zeros(max(n, 1), dtype=np.float64)
+        ms = np.zeros(max(n, 1), dtype=np.float32)
+        self._check(self._lib.owqs_launch_profile(self._h, kc.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                  by.ctypes.data_as(C.POINTER(C.c_double)),
+                                                  ms.ctypes.data_as(C.POINTER(C.c_float)), n))
+        return kc[:n], by[:n], ms[:n]
 
     def stats(self) -> dict:
         s = owqs_stats_t()
