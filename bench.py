@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py — headline benchmark of the OWQS/EOWQS array executor on B200.
+
+Metric (BASELINE.json): pattern commands/s and state-update HBM GB/s vs peak.
+Default workload (N=1): config 3 — 28-wire random brickwork, depth 40 (5020 commands, paper m 29,
+28 physical bits = 2 GiB complex64), sampled OWQS outcomes, complex64 amplitudes.
+A step = set the resident input (device copy) + one owqs_run over the whole pattern.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C3]
+For N > 1 launch with torch.distributed.run (one rank per GPU); every rank runs its own replica
+(the path's sharded multi-GPU mode is not in this build: DESIGN.md §7), scaling "weak".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    "C3": "config 3: brickwork 28 wires x 40 layers (J(alpha) + alternating CZ), sampled OWQS",
+    "C3W": "config 3 at width 30: brickwork 30 wires x 40 layers, sampled OWQS",
+    "C2": "config 2: QFT-20 (H = J(0), CP = 8 J + 2 CZ), sampled OWQS",
+    "C3E": "config 3 in EOWQS mode (positive branch, no probabilities)",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", type=int, default=64, choices=[64, 128])
+    ap.add_argument("--flags", type=int, default=0, help="OWQS_FLAG_* for the timed context")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ref-cmds", type=int, default=4, help="oracle sample: first k commands at full width")
+    return ap.parse_args()
+
+
+def pattern_for(workload):
+    from workloads import patterns as W
+    if workload in ("C3", "C3E"):
+        return W.config_pattern("C3", seed=1), ("eowqs" if workload == "C3E" else "sampled")
+    return W.config_pattern(workload, seed=1), "sampled"
+
+
+# --------------------------------------------------------------------------------------- clocks
+REASONS = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, uuid):
+        self.uuid = uuid
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        q = "clocks.sm,clocks.max.sm,power.draw," + ",".join(f"clocks_event_reasons.{r}" for r in REASONS)
+        cmd = ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "200"]
+        if self.uuid:
+            cmd += ["-i", self.uuid]
+        try:
+            self.proc = subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3 + len(REASONS):
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            for k, name in enumerate(REASONS):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------------------------------- oracle
+def oracle_prefix_sample(pattern, psi, k_cmds, seed):
+    """Run the oracle on the first k commands of `pattern` (full width). Returns (seconds, k)."""
+    import oracle
+    from workloads.patterns import KIND_M, KIND_N, Pattern
+    cmds = pattern.cmds[:k_cmds]
+    live = list(pattern.inputs)
+    for c in cmds:
+        if c.kind == KIND_N:
+            live.append(c.q0)
+        elif c.kind == KIND_M:
+            live.remove(c.q0)
+    pre = Pattern(list(pattern.inputs), live, list(cmds), pattern.name + f"[:{k_cmds}]")
+    t0 = time.perf_counter()
+    oracle.run(pre, psi, mode="sampled", seed=seed)
+    return time.perf_counter() - t0, len(cmds)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------------ reference
+def run_reference(args, rank, world):
+    if rank != 0:
+        return 0
+    import numpy as np  # noqa: F401
+    from workloads.inputs import haar_state
+    pattern, mode = pattern_for(args.workload)
+    n = len(pattern.inputs)
+    psi = haar_state(n, 1)
+    times = []
+    k = args.ref_cmds
+    for s in range(args.warmup + args.steps):
+        dt, k = oracle_prefix_sample(pattern, psi, args.ref_cmds, seed=s)
+        if s >= args.warmup:
+            times.append(dt)
+    t = sum(times)
+    value = k * len(times) / t
+    line = {
+        "impl": "reference", "metric": "pattern commands/s", "value": value, "unit": "commands/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload], "sample": f"first {k} commands at full width"},
+        "cpu_baseline": {"value": value, "unit": "commands/s", "cores": 1, "kind": "oracle",
+                         "sample": f"oracle (numpy complex128, given order) on the first {k} commands of "
+                                   f"{args.workload} at full width ({n}+1 qubits), per step"},
+        "e2e": {"value": value, "unit": "commands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------ ours
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_05659_b200 import FLAG_PROFILE, KCLASS_NAMES, Simulator
+    from workloads.patterns import Pattern
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream(dev)
+    pattern, mode = pattern_for(args.workload)
+    n_in = len(pattern.inputs)
+    N = 2 ** n_in
+    prec = args.precision
+    cdt = torch.complex64 if prec == 64 else torch.complex128
+
+    sim = Simulator(precision=prec, device=local_rank, flags=args.flags, stream=stream.cuda_stream)
+    t0 = time.perf_counter()
+    sim.load(pattern)
+    load_s = time.perf_counter() - t0
+    st = sim.stats()
+
+    # resident input: device Haar generator of the library, copied into a torch-owned buffer
+    x = torch.empty(N, dtype=cdt, device=dev)
+    gen = Simulator(precision=prec, device=local_rank, stream=stream.cuda_stream)
+    gen.load(Pattern(list(range(n_in)), list(range(n_in)), []))
+    gen.set_input_random(1 + rank)
+    gen.run("eowqs", want=False)
+    gen.get_output_device(x.data_ptr(), prec, N)
+    gen.close()
+    torch.cuda.synchronize()
+
+    def step(i):
+        sim.set_input_device(x.data_ptr(), prec, N)
+        sim.run(mode, seed=1000 + i + 100_000 * rank, want=False)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    uuid = None
+    try:
+        uuid = "GPU-" + str(torch.cuda.get_device_properties(local_rank).uuid)
+    except Exception:
+        pass
+    clk = ClockSampler(uuid)
+    clk.start()
+    time.sleep(0.3)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    ev0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_per_step = ms / args.steps
+    st = sim.stats()
+    n_cmd = st["n_commands"]
+    value = world * n_cmd * args.steps / (ms / 1e3)
+    hbm_gbs = st["bytes_per_run"] / (ms_per_step / 1e3) / 1e9
+
+    # ---- roofline of the dominant kernel: per-launch CUDA events over profiled runs ----
+    peak, peak_src = peaks()
+    prof = Simulator(precision=prec, device=local_rank, flags=args.flags | FLAG_PROFILE, stream=stream.cuda_stream)
+    prof.load(pattern)
+    agg = {}
+    for r in range(3):
+        prof.set_input_device(x.data_ptr(), prec, N)
+        prof.run(mode, seed=77 + r, want=False)
+        if r == 0:
+            continue  # first run captures the graph
+        kc, by, tm = prof.launch_profile()
+        for c in set(kc.tolist()):
+            m = kc == c
+            a = agg.setdefault(int(c), [0.0, 0.0, 0])
+            a[0] += float(by[m].sum())
+            a[1] += float(tm[m].sum())
+            a[2] += int(m.sum())
+    prof_step_ms = prof.stats()["last_run_ms"]
+    prof.close()
+    dom = max(agg, key=lambda c: agg[c][1])
+    by_sum, ms_sum, cnt = agg[dom]
+    achieved = by_sum / (ms_sum / 1e3) / 1e9
+    traffic = ncu_traffic()
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": (traffic or {}).get("dram_bytes_per_launch"),
+                "kernel": f"owqs::{KCLASS_NAMES[dom]}_kernel", "launches": cnt,
+                "bytes_per_launch": by_sum / cnt, "avg_launch_us": 1e3 * ms_sum / cnt,
+                "share_of_step": ms_sum / 2 / prof_step_ms if prof_step_ms else None,
+                "peak_source": peak_src, "algorithmic_bytes": "read + write of the 2^w-amplitude state per pass"}
+
+    # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H inside the timed region ----
+    e2e = None
+    if not args.no_e2e:
+        h_in = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+        h_in.copy_(x.to(torch.complex128))
+        h_out = torch.empty(N, dtype=torch.complex128, pin_memory=True)
+        a_in, a_out = h_in.numpy(), h_out.numpy()
+        sim_n_out = 2 ** len(pattern.outputs)
+        assert sim_n_out == N
+        k_e2e = max(2, args.steps // 2)
+
+        def e2e_step(i):
+            sim.set_input(a_in)
+            sim.run(mode, seed=5000 + i, want=False)
+            sim.get_output(a_out)
+
+        e2e_step(0)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for i in range(k_e2e):
+            e2e_step(1 + i)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        e2e = {"value": world * n_cmd * k_e2e / dt, "unit": "commands/s", "h2d_bytes_per_step": N * 16,
+               "d2h_bytes_per_step": N * 16, "steps": k_e2e, "ms_per_step": 1e3 * dt / k_e2e}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            psi_host = a_in
+    # ---- CPU baseline: the oracle, rank 0 at N=1 only, bounded sample ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        if args.no_e2e:
+            psi_host = x.to(torch.complex128).cpu().numpy()
+        psi_host = psi_host / np.linalg.norm(psi_host)
+        dt, k = oracle_prefix_sample(pattern, psi_host, args.ref_cmds, seed=1)
+        cpu = {"value": k / dt, "unit": "commands/s", "cores": 1, "kind": "oracle",
+               "sample": f"oracle (numpy complex128, given order, single thread) on the first {k} commands "
+                         f"of {args.workload} at full width ({n_in}->{n_in + 1} qubits): {dt:.1f} s",
+               "host_cores_available": os.cpu_count()}
+
+    line = {
+        "metric": "pattern commands/s (state-update HBM GB/s in hbm_gbs / roofline)",
+        "value": value, "unit": "commands/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32" if prec == 64 else "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS[args.workload], "mode": mode, "amplitudes": f"complex{prec}",
+                   "commands": n_cmd, "measurements": st["n_measure"], "paper_m": st["paper_m"],
+                   "phys_bits": st["phys_bits"], "passes_per_run": st["n_passes"],
+                   "launches_per_run": st["n_launches"], "state_bytes": N * (8 if prec == 64 else 16),
+                   "l2": "state (>= 2 GiB) larger than the 126 MB L2: no flush needed",
+                   "parallelism": "single" if world == 1 else f"replicas{world}",
+                   "load_pattern_s": load_s, "schedule_ms": st["schedule_ms"]},
+        "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / peak,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": st["n_launches"] * args.steps,
+        "clocks": clocks,
+    }
+    sim.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    rc = run_ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+    return rc
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -82,7 +82,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 # ---- include/owqs_host.h (host-only introspection; no CUDA calls) ------------------------------
 HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_error",
                  "owqs_host_free"]
-KMAX_HI, MAX_OPS = 4, 40
+KMAX_HI, MAX_OPS, MAX_BFLY = 4, 64, 24
 
 
 class Op(C.Structure):
@@ -94,7 +94,8 @@ class StepDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("width", C.c_int32), ("nb_hi", C.c_int32), ("bhi", C.c_int32 * KMAX_HI),
                 ("n_ops", C.c_int32), ("red_kind", C.c_int32), ("red_slot", C.c_int32), ("slot", C.c_int32),
                 ("shrink_m", C.c_int32), ("n_bfly", C.c_int32), ("first_uses_red", C.c_int32),
-                ("first_full_rho", C.c_int32), ("pad", C.c_int32), ("ops", Op * MAX_OPS)]
+                ("first_full_rho", C.c_int32), ("pad", C.c_int32), ("ops", Op * MAX_OPS),
+                ("absorb", C.c_uint64 * MAX_BFLY)]
 
 
 class MStatic(C.Structure):

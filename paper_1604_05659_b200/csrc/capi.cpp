@@ -122,8 +122,7 @@ owqs_status compile_modes(owqs_ctx* ctx) {
     free_mode(ctx->cm[i]);
     auto t0 = std::chrono::steady_clock::now();
     CompiledMode& m = ctx->cm[i];
-    m.plan = make_plan(ctx->hp, i == 1, given, w);
-    m.prog = compile_program(ctx->hp, m.plan, i == 1 ? 2 : 0, SB, fuse);
+    plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog);
     for (const auto& s : m.prog.steps)
       if (s.kind == ST_PASS && s.width > 12 && s.width - SB - s.nb_hi < 0)
         return fail(ctx, OWQS_E_PATTERN, "internal: pass grouping exceeds the register file");

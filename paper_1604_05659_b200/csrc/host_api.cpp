@@ -40,8 +40,8 @@ owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t
     w.d = weights[3];
   }
   if (flags & OWQS_FLAG_NO_TUNE) w.tune = false;
-  h->plan = make_plan(h->hp, mode == 2, (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w);
-  h->prog = compile_program(h->hp, h->plan, mode, precision == 64 ? 6 : 5, !(flags & OWQS_FLAG_NO_FUSE));
+  plan_and_compile(h->hp, mode, precision == 64 ? 6 : 5, !(flags & OWQS_FLAG_NO_FUSE),
+                   (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w, h->plan, h->prog);
   h->elem = precision == 64 ? 8 : 16;
   return OWQS_OK;
 }

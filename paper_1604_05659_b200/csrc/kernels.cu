@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "owqs_internal.h"
@@ -162,6 +164,8 @@ __device__ void decide(const DevPtrs& p, int m, bool use_red, bool full, bool re
 // Prologue shared by the pass kernels: decisions of the pass's butterflies and op conditions.
 struct PassShared {
   double coef[MAX_BFLY][8];
+  double ka[MAX_BFLY][2];  // structured butterfly U = k [[1, a], [1, -a]]: a (k folded into scale)
+  double scale;            // product of the pass's butterfly k's
   uint8_t cond[MAX_OPS];
   uint8_t bidx[MAX_OPS];
   double red[32][4];
@@ -173,17 +177,32 @@ __device__ void pass_prologue(const StepDesc& d, const DevPtrs& p, PassShared& s
     LocalOutcomes loc;
     loc.n = 0;
     int bi = 0;
+    double scale = 1.0;
     const bool record = blockIdx.x == 0;
     for (int i = 0; i < d.n_ops; ++i) {
       const Op& op = d.ops[i];
       if (op.type == OP_BFLY) {
-        decide(p, op.m, bi == 0 && d.first_uses_red, false, record, sh.coef[bi], loc);
+        double* cf = sh.coef[bi];
+        decide(p, op.m, bi == 0 && d.first_uses_red, false, record, cf, loc);
+        // folded X_a^s (cond/sig of a butterfly): swap the output rows when the signal is 1
+        if (op.cond && signal_parity(p, op.sig_off, op.sig_len, loc))
+          for (int j = 0; j < 4; ++j) {
+            double t = cf[j];
+            cf[j] = cf[4 + j];
+            cf[4 + j] = t;
+          }
+        // every slot-reuse butterfly has the form k [[1, a], [1, -a]] (rows swapped: a -> -a)
+        const double kk = cf[0];
+        sh.ka[bi][0] = kk != 0.0 ? cf[2] / kk : 0.0;
+        sh.ka[bi][1] = kk != 0.0 ? cf[3] / kk : 0.0;
+        scale *= kk;
         sh.bidx[i] = (uint8_t)bi++;
         sh.cond[i] = 1;
       } else {
         sh.cond[i] = op.cond ? (uint8_t)signal_parity(p, op.sig_off, op.sig_len, loc) : (uint8_t)1;
       }
     }
+    sh.scale = scale;
   }
   __syncthreads();
 }
@@ -243,77 +262,278 @@ __device__ __forceinline__ void cmul_add(T ar, T ai, T xr, T xi, T br, T bi, T y
   outi = ar * xi + ai * xr + br * yi + bi * yr;
 }
 
+// Bit mask over a thread's NV*EPV amplitudes (position v*EPV + e, v = u*G + c) of those whose
+// index has slot x set: element bit (complex64 slot 0), lane bit, group bit j of c, or a bit of
+// the group base gb[u].
+template <int NV, int EPV, int G>
+struct PosMasks {
+  __host__ __device__ static constexpr uint32_t full() { return NV * EPV >= 32 ? 0xffffffffu : ((1u << (NV * EPV)) - 1u); }
+  __host__ __device__ static constexpr uint32_t elem1() {
+    uint32_t m = 0;
+    for (int p = 0; p < NV * EPV; ++p)
+      if (p % EPV == 1) m |= 1u << p;
+    return m;
+  }
+  __host__ __device__ static constexpr uint32_t group(int j) {
+    uint32_t m = 0;
+    for (int p = 0; p < NV * EPV; ++p)
+      if ((((p / EPV) % G) >> j) & 1) m |= 1u << p;
+    return m;
+  }
+  __host__ __device__ static constexpr uint32_t block(int u) {
+    uint32_t m = 0;
+    for (int p = 0; p < NV * EPV; ++p)
+      if (p / EPV / G == u) m |= 1u << p;
+    return m;
+  }
+};
+
 template <typename T, int KHI, int UNR>
-__global__ void __launch_bounds__(256) pass_kernel(const StepDesc d, const DevPtrs p) {
+__device__ __forceinline__ uint32_t slot_mask(int x, int lane, const uint64_t (&gb)[UNR], const int (&q)[KHI > 0 ? KHI : 1]) {
+  constexpr int SB = VT<T>::SB, EPV = VT<T>::EPV, G = 1 << KHI, NV = UNR * G;
+  typedef PosMasks<NV, EPV, G> PM;
+  if (EPV == 2 && x == 0) return PM::elem1();
+  if (x < SB) return ((lane >> (x - (EPV == 2 ? 1 : 0))) & 1) ? PM::full() : 0u;
+#pragma unroll
+  for (int j = 0; j < KHI; ++j)
+    if (q[j] == x - SB) return PM::group(j);
+  uint32_t m = 0;
+#pragma unroll
+  for (int u = 0; u < UNR; ++u)
+    if ((gb[u] >> (x - SB)) & 1) m |= PM::block(u);
+  return m;
+}
+
+template <typename T, int KHI, int UNR>
+__device__ __forceinline__ uint32_t slot_mask_p(int x, int lane, const uint64_t (&gb)[UNR], const StepDesc& d) {
+  constexpr int SB = VT<T>::SB, EPV = VT<T>::EPV, G = 1 << KHI, NV = UNR * G;
+  typedef PosMasks<NV, EPV, G> PM;
+  if (EPV == 2 && x == 0) return PM::elem1();
+  if (x < SB) return ((lane >> (x - (EPV == 2 ? 1 : 0))) & 1) ? PM::full() : 0u;
+  uint32_t m = 0;
+  bool grp = false;
+#pragma unroll
+  for (int j = 0; j < KHI; ++j)
+    if (d.bhi[j] == x) {
+      m = PM::group(j);
+      grp = true;
+    }
+  if (grp) return m;
+#pragma unroll
+  for (int u = 0; u < UNR; ++u)
+    if ((gb[u] >> (x - SB)) & 1) m |= PM::block(u);
+  return m;
+}
+
+// Opaque dependency: makes `lm` depend on `x`, so later shuffles (which use lm) cannot be hoisted
+// above the work that produced x (bounds the registers a cross-lane op keeps in flight).
+template <typename T> __device__ __forceinline__ void chain(int& lm, T x);
+template <> __device__ __forceinline__ void chain<float>(int& lm, float x) {
+  asm volatile("{ .reg .f32 t; mov.f32 t, %1; }" : "+r"(lm) : "f"(x));
+}
+template <> __device__ __forceinline__ void chain<double>(int& lm, double x) {
+  asm volatile("{ .reg .f64 t; mov.f64 t, %1; }" : "+r"(lm) : "d"(x));
+}
+
+template <int KHI, int MINB> struct PassBounds {
+  static constexpr int min_blocks = MINB > 0 ? MINB : (KHI <= 2 ? 3 : 2);
+};
+
+// Sign flips accumulated in `neg` (bit v*EPV+e) applied branch-free through the sign bit.
+template <typename T> __device__ __forceinline__ T flip_sign(T x, uint32_t f);
+template <> __device__ __forceinline__ float flip_sign<float>(float x, uint32_t f) {
+  return __int_as_float(__float_as_int(x) ^ (f << 31));
+}
+template <> __device__ __forceinline__ double flip_sign<double>(double x, uint32_t f) {
+  return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)f << 63));
+}
+
+// ---- in-place register kernels of the pass (inline PTX pins each amplitude to one register,
+// so the runtime op dispatch does not force register shuffling at its merge points) ----
+// structured butterfly: x0 <- x0 + a x1, x1 <- x0 - a x1
+__device__ __forceinline__ void bfly_ip(float& x0r, float& x0i, float& x1r, float& x1i, float ar, float ai, float nai) {
+  asm("{\n\t.reg .f32 tr, ti;\n\t"
+      "mul.f32 tr, %4, %2;\n\t"
+      "fma.rn.f32 tr, %6, %3, tr;\n\t"
+      "mul.f32 ti, %4, %3;\n\t"
+      "fma.rn.f32 ti, %5, %2, ti;\n\t"
+      "sub.f32 %2, %0, tr;\n\t"
+      "sub.f32 %3, %1, ti;\n\t"
+      "add.f32 %0, %0, tr;\n\t"
+      "add.f32 %1, %1, ti;\n\t}"
+      : "+f"(x0r), "+f"(x0i), "+f"(x1r), "+f"(x1i)
+      : "f"(ar), "f"(ai), "f"(nai));
+}
+__device__ __forceinline__ void bfly_ip(double& x0r, double& x0i, double& x1r, double& x1i, double ar, double ai, double) {
+  const double tr = ar * x1r - ai * x1i, ti = ar * x1i + ai * x1r;
+  x1r = x0r - tr; x1i = x0i - ti;
+  x0r = x0r + tr; x0i = x0i + ti;
+}
+// butterfly with the sign of a x1 flipped by bit 31 of sb (absorbed CZ)
+__device__ __forceinline__ void bfly_ip_s(float& x0r, float& x0i, float& x1r, float& x1i, float ar, float ai, float nai,
+                                          uint32_t sb) {
+  asm("{\n\t.reg .f32 tr, ti;\n\t"
+      "mul.f32 tr, %4, %2;\n\t"
+      "fma.rn.f32 tr, %6, %3, tr;\n\t"
+      "mul.f32 ti, %4, %3;\n\t"
+      "fma.rn.f32 ti, %5, %2, ti;\n\t"
+      "xor.b32 tr, tr, %7;\n\t"
+      "xor.b32 ti, ti, %7;\n\t"
+      "sub.f32 %2, %0, tr;\n\t"
+      "sub.f32 %3, %1, ti;\n\t"
+      "add.f32 %0, %0, tr;\n\t"
+      "add.f32 %1, %1, ti;\n\t}"
+      : "+f"(x0r), "+f"(x0i), "+f"(x1r), "+f"(x1i)
+      : "f"(ar), "f"(ai), "f"(nai), "r"(sb));
+}
+__device__ __forceinline__ void bfly_ip_s(double& x0r, double& x0i, double& x1r, double& x1i, double ar, double ai,
+                                          double, uint32_t sb) {
+  double tr = ar * x1r - ai * x1i, ti = ar * x1i + ai * x1r;
+  if (sb) { tr = -tr; ti = -ti; }
+  x1r = x0r - tr; x1i = x0i - ti;
+  x0r = x0r + tr; x0i = x0i + ti;
+}
+__device__ __forceinline__ void lane_bfly_ip_s(float& xr, float& xi, float cr, float ci, float nci, float s, int lm,
+                                               uint32_t sb) {
+  asm("{\n\t.reg .f32 yr, yi, rr, ri;\n\t"
+      "mul.f32 yr, %2, %0;\n\t"
+      "fma.rn.f32 yr, %4, %1, yr;\n\t"
+      "mul.f32 yi, %2, %1;\n\t"
+      "fma.rn.f32 yi, %3, %0, yi;\n\t"
+      "xor.b32 yr, yr, %7;\n\t"
+      "xor.b32 yi, yi, %7;\n\t"
+      "shfl.sync.bfly.b32 rr, yr, %6, 0x1f, 0xffffffff;\n\t"
+      "shfl.sync.bfly.b32 ri, yi, %6, 0x1f, 0xffffffff;\n\t"
+      "fma.rn.f32 %0, %5, yr, rr;\n\t"
+      "fma.rn.f32 %1, %5, yi, ri;\n\t}"
+      : "+f"(xr), "+f"(xi)
+      : "f"(cr), "f"(ci), "f"(nci), "f"(s), "r"(lm), "r"(sb));
+}
+__device__ __forceinline__ void lane_bfly_ip_s(double& xr, double& xi, double cr, double ci, double, double s, int lm,
+                                               uint32_t sb) {
+  double yr = cr * xr - ci * xi, yi = cr * xi + ci * xr;
+  if (sb) { yr = -yr; yi = -yi; }
+  const double rr = __shfl_xor_sync(FULLMASK, yr, lm), ri = __shfl_xor_sync(FULLMASK, yi, lm);
+  xr = rr + s * yr;
+  xi = ri + s * yi;
+}
+// cross-lane butterfly: y = c x, r = y of the partner lane, x <- r + s y
+__device__ __forceinline__ void lane_bfly_ip(float& xr, float& xi, float cr, float ci, float nci, float s, int lm) {
+  asm("{\n\t.reg .f32 yr, yi, rr, ri;\n\t"
+      "mul.f32 yr, %2, %0;\n\t"
+      "fma.rn.f32 yr, %4, %1, yr;\n\t"
+      "mul.f32 yi, %2, %1;\n\t"
+      "fma.rn.f32 yi, %3, %0, yi;\n\t"
+      "shfl.sync.bfly.b32 rr, yr, %6, 0x1f, 0xffffffff;\n\t"
+      "shfl.sync.bfly.b32 ri, yi, %6, 0x1f, 0xffffffff;\n\t"
+      "fma.rn.f32 %0, %5, yr, rr;\n\t"
+      "fma.rn.f32 %1, %5, yi, ri;\n\t}"
+      : "+f"(xr), "+f"(xi)
+      : "f"(cr), "f"(ci), "f"(nci), "f"(s), "r"(lm));
+}
+__device__ __forceinline__ void lane_bfly_ip(double& xr, double& xi, double cr, double ci, double, double s, int lm) {
+  const double yr = cr * xr - ci * xi, yi = cr * xi + ci * xr;
+  const double rr = __shfl_xor_sync(FULLMASK, yr, lm), ri = __shfl_xor_sync(FULLMASK, yi, lm);
+  xr = rr + s * yr;
+  xi = ri + s * yi;
+}
+// sign flip of (re, im) by bit `pos` of neg
+template <int POS>
+__device__ __forceinline__ void flip_ip(float& re, float& im, uint32_t neg) {
+  asm("{\n\t.reg .b32 t;\n\t"
+      "shl.b32 t, %2, %3;\n\t"
+      "and.b32 t, t, 0x80000000;\n\t"
+      "xor.b32 %0, %0, t;\n\t"
+      "xor.b32 %1, %1, t;\n\t}"
+      : "+f"(re), "+f"(im)
+      : "r"(neg), "n"(31 - POS));
+}
+template <int POS>
+__device__ __forceinline__ void flip_ip(double& re, double& im, uint32_t neg) {
+  const uint32_t f = (neg >> POS) & 1u;
+  re = flip_sign<double>(re, f);
+  im = flip_sign<double>(im, f);
+}
+template <typename T, int NV, int EPV, int P = 0>
+__device__ __forceinline__ void flush_all(T (&re)[NV][2], T (&im)[NV][2], uint32_t neg) {
+  if constexpr (P < NV * EPV) {
+    flip_ip<P>(re[P / EPV][P % EPV], im[P / EPV][P % EPV], neg);
+    flush_all<T, NV, EPV, P + 1>(re, im, neg);
+  }
+}
+
+
+template <typename T, int KHI, int UNR, int MINB = 0>
+__global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass_kernel(const StepDesc d, const DevPtrs p) {
   typedef typename VT<T>::V V;
   constexpr int SB = VT<T>::SB, EPV = VT<T>::EPV;
   constexpr int G = 1 << KHI;
   constexpr int NV = UNR * G;
   __shared__ PassShared sh;
+  __shared__ T s_a[MAX_BFLY][2];
   pass_prologue(d, p, sh);
+  if (threadIdx.x < MAX_BFLY) {
+    s_a[threadIdx.x][0] = (T)sh.ka[threadIdx.x][0];
+    s_a[threadIdx.x][1] = (T)sh.ka[threadIdx.x][1];
+  }
+  __syncthreads();
 
   const int lane = threadIdx.x & 31;
-  const uint64_t warp_id = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t n_warps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const uint64_t n_units = (1ull << (d.width - SB - KHI)) / UNR;
-  int q[KHI > 0 ? KHI : 1];
-#pragma unroll
-  for (int j = 0; j < KHI; ++j) q[j] = d.bhi[j] - SB;
+  const int warp = threadIdx.x >> 5;
+  // the loop condition depends on blockIdx only, so the compiler sees converged warps at the
+  // shuffles (launch: 256 threads, n_units a multiple of 8)
+  const uint64_t n_blk_units = ((1ull << (d.width - SB - KHI)) / UNR) >> 3;
   V* st = reinterpret_cast<V*>(p.state);
   double acc[4] = {0, 0, 0, 0};
-  const bool do_store = d.n_ops > 0;
+  const T pass_scale = (T)sh.scale;
 
-  for (uint64_t unit = warp_id; unit < n_units; unit += n_warps) {
-    uint64_t seg[NV];
+  for (uint64_t ub = blockIdx.x; ub < n_blk_units; ub += gridDim.x) {
+    const uint64_t unit = ub * 8 + warp;
+    // group base: the unit's group index with zeros inserted at the group slots (ascending)
+    uint64_t gb[UNR];
 #pragma unroll
     for (int u = 0; u < UNR; ++u) {
       uint64_t g = unit * UNR + u;
 #pragma unroll
-      for (int j = 0; j < KHI; ++j) g = ((g >> q[j]) << (q[j] + 1)) | (g & ((1ull << q[j]) - 1));
-#pragma unroll
-      for (int c = 0; c < G; ++c) {
-        uint64_t s = g;
-#pragma unroll
-        for (int j = 0; j < KHI; ++j)
-          if ((c >> j) & 1) s |= 1ull << q[j];
-        seg[u * G + c] = s;
+      for (int j = 0; j < KHI; ++j) {
+        const int qj = d.bhi[j] - SB;
+        g = ((g >> qj) << (qj + 1)) | (g & ((1ull << qj) - 1));
       }
+      gb[u] = g;
     }
     T re[NV][2], im[NV][2];
 #pragma unroll
-    for (int v = 0; v < NV; ++v) vload<T>(st + seg[v] * 32 + lane, re[v], im[v]);
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int c = 0; c < G; ++c) {
+        uint64_t s = gb[u];
+#pragma unroll
+        for (int j = 0; j < KHI; ++j)
+          if ((c >> j) & 1) s |= 1ull << (d.bhi[j] - SB);
+        vload<T>(st + s * 32 + lane, re[u * G + c], im[u * G + c]);
+      }
 
+    uint32_t neg = 0;
     for (int i = 0; i < d.n_ops; ++i) {
-      const Op op = d.ops[i];
-      if (!sh.cond[i]) continue;
-      if (op.type == OP_DIAG_E || op.type == OP_DIAG_Z) {
-        const int a = op.a, b = op.type == OP_DIAG_E ? op.b : op.a;
-#pragma unroll
-        for (int v = 0; v < NV; ++v)
-#pragma unroll
-          for (int e = 0; e < EPV; ++e) {
-            uint64_t idx = (seg[v] << SB) | (uint64_t)(lane * EPV + e);
-            if ((idx >> a) & (idx >> b) & 1) {
-              re[v][e] = -re[v][e];
-              im[v][e] = -im[v][e];
-            }
-          }
-      } else {
-        // 2x2 on slot a: butterfly coefficients or X swap
-        const int a = op.a;
-        T c00r, c00i, c01r, c01i, c10r, c10i, c11r, c11i;
-        if (op.type == OP_BFLY) {
-          const double* cf = sh.coef[sh.bidx[i]];
-          c00r = (T)cf[0]; c00i = (T)cf[1]; c01r = (T)cf[2]; c01i = (T)cf[3];
-          c10r = (T)cf[4]; c10i = (T)cf[5]; c11r = (T)cf[6]; c11i = (T)cf[7];
-        } else {
-          c00r = 0; c00i = 0; c01r = 1; c01i = 0; c10r = 1; c10i = 0; c11r = 0; c11i = 0;
-        }
+      const int type = d.ops[i].type;
+      const int a = d.ops[i].a;
+      if (type == OP_DIAG_E || type == OP_DIAG_Z) {
+        uint32_t m = slot_mask_p<T, KHI, UNR>(a, lane, gb, d);
+        if (type == OP_DIAG_E) m &= slot_mask_p<T, KHI, UNR>(d.ops[i].b, lane, gb, d);
+        neg ^= sh.cond[i] ? m : 0u;
+        continue;
+      }
+      if (type == OP_FLUSH) {  // placed by the compiler where a pending diagonal must apply
+        flush_all<T, NV, EPV>(re, im, neg);
+        neg = 0;
+        continue;
+      }
+      if (type == OP_X) {
+        if (!__all_sync(FULLMASK, sh.cond[i] != 0)) continue;
         if (a >= SB) {
-          const int qa = a - SB;
 #pragma unroll
           for (int jj = 0; jj < KHI; ++jj) {
-            if (q[jj] != qa) continue;
+            if (d.bhi[jj] != a) continue;
 #pragma unroll
             for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -322,60 +542,89 @@ __global__ void __launch_bounds__(256) pass_kernel(const StepDesc d, const DevPt
                 const int v0 = u * G + c, v1 = v0 + (1 << jj);
 #pragma unroll
                 for (int e = 0; e < EPV; ++e) {
-                  T x0r = re[v0][e], x0i = im[v0][e], x1r = re[v1][e], x1i = im[v1][e];
-                  cmul_add(c00r, c00i, x0r, x0i, c01r, c01i, x1r, x1i, re[v0][e], im[v0][e]);
-                  cmul_add(c10r, c10i, x0r, x0i, c11r, c11i, x1r, x1i, re[v1][e], im[v1][e]);
+                  T tr = re[v0][e], ti = im[v0][e];
+                  re[v0][e] = re[v1][e]; im[v0][e] = im[v1][e];
+                  re[v1][e] = tr; im[v1][e] = ti;
                 }
               }
           }
         } else if (EPV == 2 && a == 0) {
 #pragma unroll
           for (int v = 0; v < NV; ++v) {
-            T x0r = re[v][0], x0i = im[v][0], x1r = re[v][1], x1i = im[v][1];
-            cmul_add(c00r, c00i, x0r, x0i, c01r, c01i, x1r, x1i, re[v][0], im[v][0]);
-            cmul_add(c10r, c10i, x0r, x0i, c11r, c11i, x1r, x1i, re[v][1], im[v][1]);
+            T tr = re[v][0], ti = im[v][0];
+            re[v][0] = re[v][1]; im[v][0] = im[v][1];
+            re[v][1] = tr; im[v][1] = ti;
           }
+        } else {
+          int lm = 1 << (a - (EPV == 2 ? 1 : 0));
+#pragma unroll
+          for (int v = 0; v < NV; ++v) {
+#pragma unroll
+            for (int e = 0; e < EPV; ++e) {
+              re[v][e] = __shfl_xor_sync(FULLMASK, re[v][e], lm);
+              im[v][e] = __shfl_xor_sync(FULLMASK, im[v][e], lm);
+            }
+            if ((v & 3) == 3) chain(lm, re[v][0]);
+          }
+        }
+        continue;
+      }
+      // structured butterfly: out0 = x0 + a x1, out1 = x0 - a x1 (k folded into the pass scale)
+      const int bi = sh.bidx[i];
+      T ar = s_a[bi][0], ai = s_a[bi][1];
+      const uint64_t am = d.absorb[bi];
+      constexpr uint64_t LANE_SLOTS = EPV == 2 ? 0x3Eull : 0x1Full;
+      if (am & ~LANE_SLOTS) {
+        // absorbed CZ signs depend on group / element / base bits: a sign bit per pair
+        uint32_t M = 0;
+        for (uint64_t r = am; r; r &= r - 1) M ^= slot_mask_p<T, KHI, UNR>(__ffsll((long long)r) - 1, lane, gb, d);
+        const T nai = -ai;
+        if (a >= SB) {
+#pragma unroll
+          for (int jj = 0; jj < KHI; ++jj) {
+            if (d.bhi[jj] != a) continue;
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+#pragma unroll
+              for (int c = 0; c < G; ++c) {
+                if ((c >> jj) & 1) continue;
+                const int v0 = u * G + c, v1 = v0 + (1 << jj);
+#pragma unroll
+                for (int e = 0; e < EPV; ++e)
+                  bfly_ip_s(re[v0][e], im[v0][e], re[v1][e], im[v1][e], ar, ai, nai, (M >> (v0 * EPV + e)) << 31);
+              }
+          }
+        } else if (EPV == 2 && a == 0) {
+#pragma unroll
+          for (int v = 0; v < NV; ++v)
+            bfly_ip_s(re[v][0], im[v][0], re[v][1], im[v][1], ar, ai, nai, (M >> (v * EPV)) << 31);
         } else {
           const int lb = a - (EPV == 2 ? 1 : 0);
           const bool hi = (lane >> lb) & 1;
-          // mine * cA + partner * cB
-          const T aR = hi ? c11r : c00r, aI = hi ? c11i : c00i;
-          const T bR = hi ? c10r : c01r, bI = hi ? c10i : c01i;
+          const T cr = hi ? ar : (T)1, ci = hi ? ai : (T)0, nci = -ci;
+          const T sg = hi ? (T)-1 : (T)1;
+          const uint32_t Mh = hi ? M : 0u;
+          const int lm = 1 << lb;
 #pragma unroll
           for (int v = 0; v < NV; ++v)
 #pragma unroll
-            for (int e = 0; e < EPV; ++e) {
-              T pr = __shfl_xor_sync(FULLMASK, re[v][e], 1 << lb);
-              T pi = __shfl_xor_sync(FULLMASK, im[v][e], 1 << lb);
-              T mr = re[v][e], mi = im[v][e];
-              cmul_add(aR, aI, mr, mi, bR, bI, pr, pi, re[v][e], im[v][e]);
-            }
+            for (int e = 0; e < EPV; ++e)
+              lane_bfly_ip_s(re[v][e], im[v][e], cr, ci, nci, sg, lm, (Mh >> (v * EPV + e)) << 31);
+        }
+        continue;
+      }
+      if (am) {  // signs from lane bits only: one sign per thread, folded into the coefficient
+        const uint32_t lbits = (uint32_t)(EPV == 2 ? (am >> 1) : am) & 31u;
+        if (__popc((uint32_t)lane & lbits) & 1) {
+          ar = -ar;
+          ai = -ai;
         }
       }
-    }
-
-    if (d.red_kind == RED_NORM) {
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int e = 0; e < EPV; ++e)
-          acc[0] += (double)re[v][e] * re[v][e] + (double)im[v][e] * im[v][e];
-    } else if (d.red_kind == RED_RHO) {
-      const int r = d.red_slot;
-#pragma unroll
-      for (int v = 0; v < NV; ++v)
-#pragma unroll
-        for (int e = 0; e < EPV; ++e) {
-          uint64_t idx = (seg[v] << SB) | (uint64_t)(lane * EPV + e);
-          double n = (double)re[v][e] * re[v][e] + (double)im[v][e] * im[v][e];
-          if ((idx >> r) & 1) acc[1] += n; else acc[0] += n;
-        }
-      // c = sum conj(x0) x1 over pairs split on slot r
-      if (r >= SB) {
-        const int qr = r - SB;
+      const T nai = -ai;
+      if (a >= SB) {
 #pragma unroll
         for (int jj = 0; jj < KHI; ++jj) {
-          if (q[jj] != qr) continue;
+          if (d.bhi[jj] != a) continue;
 #pragma unroll
           for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -383,41 +632,117 @@ __global__ void __launch_bounds__(256) pass_kernel(const StepDesc d, const DevPt
               if ((c >> jj) & 1) continue;
               const int v0 = u * G + c, v1 = v0 + (1 << jj);
 #pragma unroll
+              for (int e = 0; e < EPV; ++e) bfly_ip(re[v0][e], im[v0][e], re[v1][e], im[v1][e], ar, ai, nai);
+            }
+        }
+      } else if (EPV == 2 && a == 0) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) bfly_ip(re[v][0], im[v][0], re[v][1], im[v][1], ar, ai, nai);
+      } else {
+        // pair across lanes. Each lane sends y = c x (c = 1 on the lower lane, a on the upper);
+        // lower: out = x0 + (a x1 received); upper: out = (x0 received) - a x1 = r - y.
+        const int lb = a - (EPV == 2 ? 1 : 0);
+        const bool hi = (lane >> lb) & 1;
+        const T cr = hi ? ar : (T)1, ci = hi ? ai : (T)0, nci = -ci;
+        const T sg = hi ? (T)-1 : (T)1;
+        const int lm = 1 << lb;
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+          for (int e = 0; e < EPV; ++e) lane_bfly_ip(re[v][e], im[v][e], cr, ci, nci, sg, lm);
+      }
+    }
+
+    if (pass_scale != (T)1) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) {
+          re[v][e] *= pass_scale;
+          im[v][e] *= pass_scale;
+        }
+    }
+
+    // reductions of the pass output: per-vector partials in T, accumulated in fp64
+    if (d.red_kind == RED_NORM) {
+#pragma unroll
+      for (int v = 0; v < NV; ++v) {
+        T n = 0;
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) n += re[v][e] * re[v][e] + im[v][e] * im[v][e];
+        acc[0] += (double)n;
+      }
+    } else if (d.red_kind == RED_RHO) {
+      const int r = d.red_slot;
+      const uint32_t mr1 = slot_mask_p<T, KHI, UNR>(r, lane, gb, d);
+#pragma unroll
+      for (int v = 0; v < NV; ++v)
+#pragma unroll
+        for (int e = 0; e < EPV; ++e) {
+          T n = re[v][e] * re[v][e] + im[v][e] * im[v][e];
+          if ((mr1 >> (v * EPV + e)) & 1u) acc[1] += (double)n; else acc[0] += (double)n;
+        }
+      // c = sum conj(x0) x1 over pairs split on slot r
+      if (r >= SB) {
+#pragma unroll
+        for (int jj = 0; jj < KHI; ++jj) {
+          if (d.bhi[jj] != r) continue;
+#pragma unroll
+          for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int c = 0; c < G; ++c) {
+              if ((c >> jj) & 1) continue;
+              const int v0 = u * G + c, v1 = v0 + (1 << jj);
+              T cr = 0, ci = 0;
+#pragma unroll
               for (int e = 0; e < EPV; ++e) {
-                double x0r = re[v0][e], x0i = im[v0][e], x1r = re[v1][e], x1i = im[v1][e];
-                acc[2] += x0r * x1r + x0i * x1i;
-                acc[3] += x0r * x1i - x0i * x1r;
+                cr += re[v0][e] * re[v1][e] + im[v0][e] * im[v1][e];
+                ci += re[v0][e] * im[v1][e] - im[v0][e] * re[v1][e];
               }
+              acc[2] += (double)cr;
+              acc[3] += (double)ci;
             }
         }
       } else if (EPV == 2 && r == 0) {
 #pragma unroll
         for (int v = 0; v < NV; ++v) {
-          double x0r = re[v][0], x0i = im[v][0], x1r = re[v][1], x1i = im[v][1];
-          acc[2] += x0r * x1r + x0i * x1i;
-          acc[3] += x0r * x1i - x0i * x1r;
+          T cr = re[v][0] * re[v][1] + im[v][0] * im[v][1];
+          T ci = re[v][0] * im[v][1] - im[v][0] * re[v][1];
+          acc[2] += (double)cr;
+          acc[3] += (double)ci;
         }
       } else {
         const int lb = r - (EPV == 2 ? 1 : 0);
         const bool hi = (lane >> lb) & 1;
 #pragma unroll
-        for (int v = 0; v < NV; ++v)
+        for (int v = 0; v < NV; ++v) {
+          T cr = 0, ci = 0;
 #pragma unroll
           for (int e = 0; e < EPV; ++e) {
             T pr = __shfl_xor_sync(FULLMASK, re[v][e], 1 << lb);
             T pi = __shfl_xor_sync(FULLMASK, im[v][e], 1 << lb);
-            if (!hi) {
-              double x0r = re[v][e], x0i = im[v][e], x1r = pr, x1i = pi;
-              acc[2] += x0r * x1r + x0i * x1i;
-              acc[3] += x0r * x1i - x0i * x1r;
-            }
+            cr += re[v][e] * pr + im[v][e] * pi;
+            ci += re[v][e] * pi - im[v][e] * pr;
           }
+          if (!hi) {
+            acc[2] += (double)cr;
+            acc[3] += (double)ci;
+          }
+        }
       }
     }
 
-    if (do_store) {
+    if (d.n_ops > 0) {
 #pragma unroll
-      for (int v = 0; v < NV; ++v) vstore<T>(st + seg[v] * 32 + lane, re[v], im[v]);
+      for (int u = 0; u < UNR; ++u)
+#pragma unroll
+        for (int c = 0; c < G; ++c) {
+          uint64_t s = gb[u];
+#pragma unroll
+          for (int j = 0; j < KHI; ++j)
+            if ((c >> j) & 1) s |= 1ull << (d.bhi[j] - SB);
+          vstore<T>(st + s * 32 + lane, re[u * G + c], im[u * G + c]);
+        }
     }
   }
   if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
@@ -440,7 +765,7 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
   __syncthreads();
   for (int k = 0; k < d.n_ops; ++k) {
     const Op op = d.ops[k];
-    if (!sh.cond[k]) continue;
+    if (!sh.cond[k] || op.type == OP_FLUSH) continue;
     if (op.type == OP_DIAG_E || op.type == OP_DIAG_Z) {
       const int a = op.a, b = op.type == OP_DIAG_E ? op.b : op.a;
       for (int i = threadIdx.x; i < n; i += blockDim.x)
@@ -457,10 +782,15 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
         double x[8] = {0, 0, 1, 0, 1, 0, 0, 0};
         for (int j = 0; j < 8; ++j) cf[j] = x[j];
       }
+      const uint32_t am = op.type == OP_BFLY ? (uint32_t)d.absorb[sh.bidx[k]] : 0u;  // w <= 12
       for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
         int i0 = ((i >> a) << (a + 1)) | (i & ((1 << a) - 1));
         int i1 = i0 | (1 << a);
         T x0r = s[i0].x, x0i = s[i0].y, x1r = s[i1].x, x1i = s[i1].y;
+        if (__popc((uint32_t)i1 & am) & 1) {  // absorbed CZ: x1 sign by the other slots' bits
+          x1r = -x1r;
+          x1i = -x1i;
+        }
         T o0r, o0i, o1r, o1i;
         cmul_add<T>((T)cf[0], (T)cf[1], x0r, x0i, (T)cf[2], (T)cf[3], x1r, x1i, o0r, o0i);
         cmul_add<T>((T)cf[4], (T)cf[5], x0r, x0i, (T)cf[6], (T)cf[7], x1r, x1i, o1r, o1i);
@@ -657,6 +987,7 @@ __global__ void __launch_bounds__(256) dot_kernel(DevPtrs p, const double2* a, c
 // ------------------------------------------------------------------------------------------------
 struct KernelLimits {
   int max_blocks_pass[2][KMAX_HI + 1];
+  int one_cta[KMAX_HI + 1];  // use the 1-CTA/SM (uncapped registers) variant
   int max_blocks_elem;
   int sm_count;
 };
@@ -675,10 +1006,16 @@ cudaError_t init_kernel_limits(int device) {
   void* fns[2][KMAX_HI + 1] = {
       {pass_fn<float, 0, 4>(), pass_fn<float, 1, 2>(), pass_fn<float, 2, 1>(), pass_fn<float, 3, 1>(), pass_fn<float, 4, 1>()},
       {pass_fn<double, 0, 4>(), pass_fn<double, 1, 2>(), pass_fn<double, 2, 1>(), pass_fn<double, 3, 1>(), pass_fn<double, 4, 1>()}};
+  for (int k = 0; k <= KMAX_HI; ++k) g_lim.one_cta[k] = 0;
+  if (const char* env = getenv("OWQS_ONE_CTA"))  // bit k: KHI = k uses the 1-CTA/SM variant
+    for (int k = 3; k <= KMAX_HI; ++k) g_lim.one_cta[k] = (atoi(env) >> k) & 1;
+  void* one[2][2] = {{(void*)pass_kernel<float, 3, 1, 1>, (void*)pass_kernel<float, 4, 1, 1>},
+                     {(void*)pass_kernel<double, 3, 1, 1>, (void*)pass_kernel<double, 4, 1, 1>}};
   for (int pr = 0; pr < 2; ++pr)
     for (int k = 0; k <= KMAX_HI; ++k) {
       int nb = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[pr][k], 256, 0);
+      void* f = (k >= 3 && g_lim.one_cta[k]) ? one[pr][k - 3] : fns[pr][k];
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 256, 0);
       if (e != cudaSuccess) return e;
       g_lim.max_blocks_pass[pr][k] = std::max(1, nb) * g_lim.sm_count;
     }
@@ -701,7 +1038,7 @@ int step_kclass(const StepDesc& d, int prec) {
   const int SB = prec == 0 ? 6 : 5;
   if (d.kind == ST_GROW) return 2;
   if (d.kind == ST_SHRINK) return 3;
-  const int slack = d.width - SB - d.nb_hi - log2i(unr_of(d.nb_hi));
+  const int slack = d.width - SB - d.nb_hi - log2i(unr_of(d.nb_hi)) - 3;
   if (slack < 0) return 1;
   return d.n_ops == 0 ? 4 : 0;
 }
@@ -712,7 +1049,7 @@ cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStrea
   if (d.kind == ST_PASS) {
     const int khi = d.nb_hi;
     const int unr = unr_of(khi);
-    const int slack = d.width - SB - khi - log2i(unr);
+    const int slack = d.width - SB - khi - log2i(unr) - 3;  // units come in groups of 8 warps
     if (slack < 0) {
       if (d.width > 12) return cudaErrorInvalidValue;
       size_t sm = (size_t)(prec == 0 ? 8 : 16) << d.width;
@@ -720,26 +1057,26 @@ cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStrea
       else small_pass_kernel<double><<<1, 512, sm, s>>>(d, p);
       return cudaGetLastError();
     }
-    const uint64_t units = 1ull << slack;
-    uint64_t blocks = (units + 7) / 8;
+    uint64_t blocks = 1ull << slack;
     blocks = std::min<uint64_t>(blocks, (uint64_t)g_lim.max_blocks_pass[prec][khi]);
     dim3 grid((unsigned)blocks), blk(256);
 #define OWQS_PASS(T, K, U) pass_kernel<T, K, U><<<grid, blk, 0, s>>>(d, p)
+#define OWQS_PASS1(T, K, U) pass_kernel<T, K, U, 1><<<grid, blk, 0, s>>>(d, p)
     if (prec == 0) {
       switch (khi) {
         case 0: OWQS_PASS(float, 0, 4); break;
         case 1: OWQS_PASS(float, 1, 2); break;
         case 2: OWQS_PASS(float, 2, 1); break;
-        case 3: OWQS_PASS(float, 3, 1); break;
-        default: OWQS_PASS(float, 4, 1); break;
+        case 3: if (g_lim.one_cta[3]) OWQS_PASS1(float, 3, 1); else OWQS_PASS(float, 3, 1); break;
+        default: if (g_lim.one_cta[4]) OWQS_PASS1(float, 4, 1); else OWQS_PASS(float, 4, 1); break;
       }
     } else {
       switch (khi) {
         case 0: OWQS_PASS(double, 0, 4); break;
         case 1: OWQS_PASS(double, 1, 2); break;
         case 2: OWQS_PASS(double, 2, 1); break;
-        case 3: OWQS_PASS(double, 3, 1); break;
-        default: OWQS_PASS(double, 4, 1); break;
+        case 3: if (g_lim.one_cta[3]) OWQS_PASS1(double, 3, 1); else OWQS_PASS(double, 3, 1); break;
+        default: if (g_lim.one_cta[4]) OWQS_PASS1(double, 4, 1); else OWQS_PASS(double, 4, 1); break;
       }
     }
 #undef OWQS_PASS

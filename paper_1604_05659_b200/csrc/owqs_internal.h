@@ -13,6 +13,8 @@ enum OpType : uint8_t {
   OP_X = 3,       // X^s on slot a (swap pairs)
   OP_BFLY = 4,    // measurement butterfly on slot a, M record m (slot reuse: the new qubit takes
                   // slot a; Eqs. 11-12 with N_o E_io folded in)
+  OP_FLUSH = 5,   // apply the sign flips accumulated by the preceding diagonal ops (placed by the
+                  // compiler before the first 2x2 on a slot those diagonals touch)
 };
 
 struct Op {
@@ -26,7 +28,7 @@ struct Op {
 };
 static_assert(sizeof(Op) == 16, "Op layout");
 
-constexpr int MAX_OPS = 40;      // ops per pass
+constexpr int MAX_OPS = 64;      // ops per pass (incl. compiler-placed flushes)
 constexpr int KMAX_HI = 4;       // group slots above the warp segment per pass
 constexpr int MAX_BFLY = 24;     // butterflies per pass (fused mode)
 
@@ -49,6 +51,9 @@ struct StepDesc {
   int32_t first_full_rho;  // 1: red_result holds (n0, n1, Re c, Im c) of the measured slot
   int32_t pad;
   Op ops[MAX_OPS];
+  // absorb[bi]: slots whose bits flip the sign of butterfly bi's coefficient a — the CZ's
+  // E(o, a) absorbed into the first following butterfly on slot a (U Z^{x_o} = k[[1,-+a],[1,+-a]])
+  uint64_t absorb[MAX_BFLY];
 };
 
 // Static record of one measurement (plan order). Uploaded once per compiled plan.

@@ -8,10 +8,14 @@
 #include <sstream>
 #include <unordered_map>
 #include <unordered_set>
+#include <cstdio>
+#include <cstdlib>
 
 #include "owqs.h"
 
 namespace owqs {
+
+constexpr int MAX_OPS_HARD = MAX_OPS;
 
 namespace {
 std::string fmt_cmd(int64_t i) {
@@ -602,6 +606,327 @@ double Program::bytes_per_run(int eb) const {
   return b;
 }
 
+// Fusion-aware packing of the slot-level op stream into device steps.
+//  * dependencies: on each slot, butterflies / X serialize with everything; diagonals (E, Z)
+//    commute with each other; a decision waits for the ops that decide its signal domain;
+//    GROW / SHRINK are barriers (they change the width and the slot map);
+//  * X_a^s directly after the butterfly on slot a is folded into that butterfly (row swap);
+//  * list scheduling: a pass owns the warp-segment slots (< SB) plus <= KMAX_HI group slots;
+//    it greedily takes every ready op that fits, preferring ops on slots it already owns.
+namespace {
+
+struct Packer {
+  const std::vector<LOp>& ops;
+  std::vector<MStatic>& mst;
+  Program& pr;
+  const int SB;
+  const bool eowqs;
+  const int max_bfly;
+  int width;
+  int kmax_hi = KMAX_HI;
+
+  Packer(const std::vector<LOp>& o, Program& p, int sb, bool e, int mb)
+      : ops(o), mst(p.mst), pr(p), SB(sb), eowqs(e), max_bfly(mb), width(p.in_width) {
+    if (const char* env = getenv("OWQS_KMAX_HI")) kmax_hi = std::max(0, std::min(KMAX_HI, atoi(env)));
+  }
+
+  void emit(const StepDesc& s) {
+    pr.steps.push_back(s);
+    if (s.kind == ST_PASS) ++pr.n_passes;
+    if (s.kind == ST_GROW) ++pr.n_grow;
+    if (s.kind == ST_SHRINK) ++pr.n_shrink;
+  }
+  StepDesc blank(int kind) const {
+    StepDesc d{};
+    d.kind = kind;
+    d.width = width;
+    d.red_slot = -1;
+    d.slot = -1;
+    d.shrink_m = -1;
+    return d;
+  }
+  // the state produced by the last emitted step must carry its norm (first butterfly of a pass)
+  void need_norm_before() {
+    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NORM) return;
+    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE) {
+      pr.steps.back().red_kind = RED_NORM;
+      return;
+    }
+    StepDesc r = blank(ST_PASS);
+    r.red_kind = RED_NORM;
+    emit(r);
+  }
+  void push_sig(Op& o, const std::vector<int>& sig) {
+    o.cond = sig.empty() ? 0 : 1;
+    o.sig_off = (int32_t)pr.sig_pool.size();
+    o.sig_len = (int32_t)sig.size();
+    pr.sig_pool.insert(pr.sig_pool.end(), sig.begin(), sig.end());
+  }
+
+  // Diagonal ops only XOR a sign mask in the kernel; a FLUSH applies it. A diagonal commutes with
+  // a 2x2 on a slot it does not touch. An unconditional E(o, s) pending when the first butterfly
+  // on s (or o) arrives is absorbed into that butterfly: U_s Z_s^{x_o} = butterfly with
+  // coefficient (-1)^{x_o} a (absorb mask). Other pending diagonals touching the slot of a 2x2
+  // are applied by a FLUSH placed right before it; leftovers are flushed at the end of the pass.
+  void absorb_and_flush(StepDesc& cur) {
+    Op out[MAX_OPS + MAX_OPS];
+    uint64_t absorb[MAX_BFLY] = {0};
+    int n = 0, bi = 0;
+    struct Pend { int idx; int a, b; bool e; bool alive; };
+    std::vector<Pend> pend;
+    auto touches = [](const Pend& p, int s) { return p.a == s || p.b == s; };
+    auto flush = [&]() {
+      bool any = false;
+      for (auto& p : pend) any |= p.alive;
+      if (any) {
+        Op f{};
+        f.type = OP_FLUSH;
+        out[n++] = f;
+      }
+      pend.clear();
+    };
+    for (int i = 0; i < cur.n_ops; ++i) {
+      const Op& o = cur.ops[i];
+      if (o.type == OP_DIAG_E || o.type == OP_DIAG_Z) {
+        Pend p{n, o.a, o.type == OP_DIAG_E ? o.b : o.a, o.type == OP_DIAG_E && !o.cond, true};
+        pend.push_back(p);
+        out[n++] = o;
+        continue;
+      }
+      const int s = o.a;
+      bool conflict = false;  // a pending diagonal on s that cannot be absorbed
+      for (auto& p : pend)
+        if (p.alive && touches(p, s) && !(o.type == OP_BFLY && p.e)) conflict = true;
+      if (conflict) {
+        flush();
+      } else if (o.type == OP_BFLY) {
+        for (auto& p : pend)
+          if (p.alive && touches(p, s)) {
+            const int other = p.a == s ? p.b : p.a;
+            absorb[bi] ^= 1ull << other;
+            p.alive = false;
+            out[p.idx].type = OP_NONE;  // removed below
+          }
+      }
+      if (o.type == OP_BFLY) ++bi;
+      out[n++] = o;
+    }
+    flush();
+    int m = 0;
+    for (int i = 0; i < n; ++i)
+      if (out[i].type != OP_NONE) cur.ops[m++] = out[i];
+    if (m > MAX_OPS_HARD) {
+      fprintf(stderr, "owqs: internal op overflow\n");
+      abort();
+    }
+    cur.n_ops = m;
+    for (int k = 0; k < MAX_BFLY; ++k) cur.absorb[k] = absorb[k];
+  }
+
+  // schedule ops[lo, hi) (no barriers inside) into passes
+  void segment(int lo, int hi) {
+    // node list: X ops may be folded into a butterfly
+    struct Node {
+      int op;                   // index into ops
+      std::vector<int> xsig;    // folded X signal (BFLY only)
+      bool folded_x = false;
+      std::vector<int> preds;
+      int npred = 0;
+      std::vector<int> succ;
+      bool done = false;
+    };
+    std::vector<Node> nodes;
+    std::vector<int> last_write(64, -1);
+    std::vector<std::vector<int>> diags(64);
+    std::unordered_map<int, int> decider;  // given-order ordinal -> node deciding it
+    for (int i = lo; i < hi; ++i) {
+      const LOp& l = ops[i];
+      if (l.type == 3 && last_write[l.a] >= 0 && diags[l.a].empty()) {
+        Node& w = nodes[last_write[l.a]];
+        const LOp& wl = ops[w.op];
+        bool ok = wl.type == 4 && !w.folded_x;
+        if (ok)
+          for (int o : l.sig) {
+            auto it = decider.find(o);
+            if (it != decider.end() && it->second > last_write[l.a]) ok = false;
+          }
+        if (ok) {
+          w.folded_x = true;
+          w.xsig = l.sig;
+          for (int o : l.sig) {
+            auto it = decider.find(o);
+            if (it != decider.end() && it->second != last_write[l.a]) w.preds.push_back(it->second);
+          }
+          continue;
+        }
+      }
+      Node n;
+      n.op = i;
+      const int id = (int)nodes.size();
+      auto sigdeps = [&](const std::vector<int>& sig) {
+        for (int o : sig) {
+          auto it = decider.find(o);
+          if (it != decider.end()) n.preds.push_back(it->second);
+        }
+      };
+      if (l.type == 1 || l.type == 2) {
+        const int b = l.type == 1 ? l.b : l.a;
+        if (last_write[l.a] >= 0) n.preds.push_back(last_write[l.a]);
+        if (last_write[b] >= 0) n.preds.push_back(last_write[b]);
+        sigdeps(l.sig);
+        diags[l.a].push_back(id);
+        if (b != l.a) diags[b].push_back(id);
+      } else {  // X or BFLY on slot a
+        if (last_write[l.a] >= 0) n.preds.push_back(last_write[l.a]);
+        for (int d : diags[l.a]) n.preds.push_back(d);
+        diags[l.a].clear();
+        last_write[l.a] = id;
+        if (l.type == 3) sigdeps(l.sig);
+        if (l.type == 4) {
+          const MStatic& m = mst[l.m];
+          for (int k = 0; k < m.s_len; ++k) {
+            auto it = decider.find(pr.sig_pool[m.s_off + k]);
+            if (it != decider.end()) n.preds.push_back(it->second);
+          }
+          for (int k = 0; k < m.t_len; ++k) {
+            auto it = decider.find(pr.sig_pool[m.t_off + k]);
+            if (it != decider.end()) n.preds.push_back(it->second);
+          }
+          decider[m.ord] = id;
+        }
+      }
+      nodes.push_back(std::move(n));
+    }
+    const int N = (int)nodes.size();
+    for (int i = 0; i < N; ++i) {
+      auto& P = nodes[i].preds;
+      std::sort(P.begin(), P.end());
+      P.erase(std::unique(P.begin(), P.end()), P.end());
+      nodes[i].npred = (int)P.size();
+      for (int p : P) nodes[p].succ.push_back(i);
+    }
+    std::vector<int> ready;
+    for (int i = 0; i < N; ++i)
+      if (nodes[i].npred == 0) ready.push_back(i);
+    int remaining = N;
+    while (remaining > 0) {
+      StepDesc cur = blank(ST_PASS);
+      auto has_slot = [&](int a) {
+        if (a < SB) return true;
+        for (int j = 0; j < cur.nb_hi; ++j)
+          if (cur.bhi[j] == a) return true;
+        return false;
+      };
+      while (true) {
+        if (2 * cur.n_ops + 2 > MAX_OPS) break;  // room for the FLUSH ops inserted afterwards
+        // pick: (1) fits without a new slot, lowest stream index; (2) needs a new slot
+        int best = -1, best_new = -1;
+        for (int k = 0; k < (int)ready.size(); ++k) {
+          const Node& n = nodes[ready[k]];
+          const LOp& l = ops[n.op];
+          if (l.type == 4 && cur.n_bfly >= max_bfly) continue;
+          bool fits = (l.type == 1 || l.type == 2) || has_slot(l.a);
+          if (fits) {
+            if (best < 0 || n.op < nodes[ready[best]].op) best = k;
+          } else if (cur.nb_hi < kmax_hi) {
+            if (best_new < 0 || n.op < nodes[ready[best_new]].op) best_new = k;
+          }
+        }
+        int pick = best >= 0 ? best : best_new;
+        if (pick < 0) break;
+        const int id = ready[pick];
+        ready[pick] = ready.back();
+        ready.pop_back();
+        Node& n = nodes[id];
+        const LOp& l = ops[n.op];
+        if ((l.type == 3 || l.type == 4) && !has_slot(l.a)) {
+          cur.bhi[cur.nb_hi++] = l.a;
+          std::sort(cur.bhi, cur.bhi + cur.nb_hi);
+        }
+        Op o{};
+        o.type = (uint8_t)l.type;
+        o.a = (uint8_t)std::max(l.a, 0);
+        o.b = (uint8_t)std::max(l.b, 0);
+        o.m = l.m;
+        if (l.type == 4) {
+          push_sig(o, n.xsig);  // cond/sig of a butterfly = folded X_a^s
+          if (cur.n_bfly == 0 && !eowqs) cur.first_uses_red = 1;
+          ++cur.n_bfly;
+        } else {
+          push_sig(o, l.sig);
+        }
+        cur.ops[cur.n_ops++] = o;
+        n.done = true;
+        --remaining;
+        for (int s : n.succ)
+          if (--nodes[s].npred == 0) ready.push_back(s);
+      }
+      if (cur.n_ops == 0) break;  // cannot happen: some op is always ready
+      if (cur.first_uses_red) need_norm_before();
+      absorb_and_flush(cur);
+      emit(cur);
+    }
+  }
+
+  void run() {
+    int lo = 0;
+    const int n = (int)ops.size();
+    for (int i = 0; i <= n; ++i) {
+      if (i < n && ops[i].type != 10 && ops[i].type != 11) continue;
+      segment(lo, i);
+      lo = i + 1;
+      if (i == n) break;
+      const LOp& l = ops[i];
+      if (l.type == 10) {
+        StepDesc g = blank(ST_GROW);
+        g.slot = l.a;
+        emit(g);
+        ++width;
+      } else {
+        if (!eowqs) {  // rho of the measured slot from the last pass (or a read-only pass)
+          StepDesc* last = pr.steps.empty() ? nullptr : &pr.steps.back();
+          bool room = last && last->kind == ST_PASS && last->red_kind == RED_NONE && last->width == width &&
+                      (l.a < SB || last->nb_hi < kmax_hi ||
+                       std::find(last->bhi, last->bhi + last->nb_hi, l.a) != last->bhi + last->nb_hi);
+          if (room) {
+            if (l.a >= SB && std::find(last->bhi, last->bhi + last->nb_hi, l.a) == last->bhi + last->nb_hi) {
+              last->bhi[last->nb_hi++] = l.a;
+              std::sort(last->bhi, last->bhi + last->nb_hi);
+            }
+            last->red_kind = RED_RHO;
+            last->red_slot = l.a;
+          } else {
+            StepDesc r = blank(ST_PASS);
+            if (l.a >= SB) r.bhi[r.nb_hi++] = l.a;
+            r.red_kind = RED_RHO;
+            r.red_slot = l.a;
+            emit(r);
+          }
+        }
+        StepDesc s = blank(ST_SHRINK);
+        s.slot = l.a;
+        s.shrink_m = l.m;
+        s.first_uses_red = eowqs ? 0 : 1;
+        s.first_full_rho = eowqs ? 0 : 1;
+        emit(s);
+        --width;
+      }
+    }
+    // final norm of the output state (EOWQS determinism check / drift report)
+    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE)
+      pr.steps.back().red_kind = RED_NORM;
+    else if (pr.steps.empty() || pr.steps.back().red_kind != RED_NORM) {
+      StepDesc r = blank(ST_PASS);
+      r.red_kind = RED_NORM;
+      emit(r);
+    }
+    for (const auto& s : pr.steps)
+      if (s.red_kind != RED_NONE) ++pr.n_reduce;
+  }
+};
+
+}  // namespace
+
 Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse) {
   const bool eowqs = mode == 2;
   Emitter em(hp, eowqs);
@@ -612,160 +937,32 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
   pr.phys_bits = em.max_width;
   pr.in_width = (int)hp.inputs.size();
   for (int o : hp.outputs) pr.out_slot.push_back(em.slot_of[o]);
-
-  // ---- pack into steps ----
-  int width = pr.in_width;
-  StepDesc cur{};
-  bool cur_open = false;
-  auto open = [&]() {
-    cur = StepDesc{};
-    cur.kind = ST_PASS;
-    cur.width = width;
-    cur.red_slot = -1;
-    cur.shrink_m = -1;
-    cur.slot = -1;
-    cur_open = true;
-  };
-  auto emit = [&](const StepDesc& s) {
-    pr.steps.push_back(s);
-    if (s.kind == ST_PASS) ++pr.n_passes;
-    if (s.kind == ST_GROW) ++pr.n_grow;
-    if (s.kind == ST_SHRINK) ++pr.n_shrink;
-  };
-  auto flush = [&](int red_kind, int red_slot) {
-    if (!cur_open) open();
-    if (cur.n_ops > 0 || red_kind != RED_NONE) {
-      cur.red_kind = red_kind;
-      cur.red_slot = red_slot;
-      emit(cur);
-    }
-    cur_open = false;
-  };
-  auto has_slot = [&](int a) {
-    if (a < SB) return true;
-    for (int j = 0; j < cur.nb_hi; ++j)
-      if (cur.bhi[j] == a) return true;
-    return false;
-  };
-  auto add_slot = [&](int a) -> bool {  // false if no room
-    if (has_slot(a)) return true;
-    if (cur.nb_hi >= KMAX_HI) return false;
-    int j = cur.nb_hi++;
-    cur.bhi[j] = a;
-    std::sort(cur.bhi, cur.bhi + cur.nb_hi);
-    return true;
-  };
-  auto push = [&](const LOp& l) {
-    Op o{};
-    o.type = (uint8_t)l.type;
-    o.a = (uint8_t)std::max(l.a, 0);
-    o.b = (uint8_t)std::max(l.b, 0);
-    o.m = l.m;
-    o.cond = l.sig.empty() ? 0 : 1;
-    o.sig_off = (int32_t)pr.sig_pool.size();
-    o.sig_len = (int32_t)l.sig.size();
-    pr.sig_pool.insert(pr.sig_pool.end(), l.sig.begin(), l.sig.end());
-    cur.ops[cur.n_ops++] = o;
-    if (l.type == 4) ++cur.n_bfly;
-  };
-  // Request a reduction of the state produced by the last emitted step (NORM), creating a
-  // read-only pass if the program has not emitted anything yet.
-  auto need_norm_before = [&]() {
-    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE) {
-      pr.steps.back().red_kind = RED_NORM;
-      return;
-    }
-    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NORM) return;
-    StepDesc r{};
-    r.kind = ST_PASS;
-    r.width = width;
-    r.red_kind = RED_NORM;
-    r.red_slot = -1;
-    r.slot = -1;
-    r.shrink_m = -1;
-    emit(r);
-  };
-  open();
-  for (const LOp& l : em.ops) {
-    if (l.type == 1 || l.type == 2) {
-      if (cur.n_ops >= MAX_OPS) flush(RED_NONE, -1), open();
-      push(l);
-    } else if (l.type == 3) {
-      if (cur.n_ops >= MAX_OPS || !add_slot(l.a)) {
-        flush(RED_NONE, -1);
-        open();
-        add_slot(l.a);
-      }
-      push(l);
-    } else if (l.type == 4) {  // slot-reuse butterfly
-      const MStatic& ms = pr.mst[l.m];
-      bool join = fuse && cur_open && cur.n_bfly > 0 && cur.n_bfly < MAX_BFLY && cur.n_ops < MAX_OPS &&
-                  (eowqs || ms.structural) && add_slot(l.a);
-      if (!join) {
-        if (!cur_open) open();
-        // everything before this butterfly goes into the previous pass (SURVEY §8(a) a6 rule)
-        flush(RED_NONE, -1);
-        if (!eowqs) need_norm_before();
-        open();
-        cur.first_uses_red = eowqs ? 0 : 1;
-        add_slot(l.a);
-      }
-      push(l);
-    } else if (l.type == 10) {  // GROW
-      flush(RED_NONE, -1);
-      StepDesc g{};
-      g.kind = ST_GROW;
-      g.width = width;  // old width; writes slot `width`
-      g.slot = l.a;
-      g.red_slot = -1;
-      g.shrink_m = -1;
-      emit(g);
-      ++width;
-      open();
-    } else if (l.type == 11) {  // SHRINK: needs rho of the measured slot (OWQS)
-      if (!eowqs) {
-        if (!cur_open) open();
-        if (cur.n_ops < MAX_OPS && add_slot(l.a)) {
-          flush(RED_RHO, l.a);
-        } else {
-          flush(RED_NONE, -1);
-          open();
-          add_slot(l.a);
-          flush(RED_RHO, l.a);
-        }
-      } else {
-        flush(RED_NONE, -1);
-      }
-      StepDesc s{};
-      s.kind = ST_SHRINK;
-      s.width = width;
-      s.slot = l.a;
-      s.shrink_m = l.m;
-      s.red_slot = -1;
-      s.first_uses_red = eowqs ? 0 : 1;
-      s.first_full_rho = eowqs ? 0 : 1;
-      emit(s);
-      --width;
-      open();
-    }
-  }
-  flush(RED_NONE, -1);
-  // final norm of the output state (EOWQS determinism check / drift report), fused when possible
-  if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE)
-    pr.steps.back().red_kind = RED_NORM;
-  else if (pr.steps.empty() || pr.steps.back().red_kind != RED_NORM) {
-    StepDesc r{};
-    r.kind = ST_PASS;
-    r.width = width;
-    r.red_kind = RED_NORM;
-    r.red_slot = -1;
-    r.slot = -1;
-    r.shrink_m = -1;
-    emit(r);
-  }
-  for (const auto& s : pr.steps)
-    if (s.red_kind != RED_NONE) ++pr.n_reduce;
+  Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1);
+  pk.run();
   return pr;
+}
+
+void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool given, const ProaWeights& w,
+                      Plan& plan, Program& prog) {
+  if (mode != 2) {
+    plan = make_plan(hp, false, given, w);
+    prog = compile_program(hp, plan, mode, SB, fuse);
+    return;
+  }
+  plan = make_plan(hp, true, given, w);
+  prog = compile_program(hp, plan, 2, SB, fuse);
+  Plan alt = make_plan(hp, false, given, w);
+  Plan filt;
+  for (int c : alt.order)
+    if (hp.cmds[c].kind != H_X && hp.cmds[c].kind != H_Z) filt.order.push_back(c);
+  filt.m_cmds = alt.m_cmds;
+  filt.ms = alt.ms;
+  filt.paper_m = alt.paper_m;
+  Program ap = compile_program(hp, filt, 2, SB, fuse);
+  if (ap.phys_bits < prog.phys_bits || (ap.phys_bits == prog.phys_bits && ap.n_passes < prog.n_passes)) {
+    plan = std::move(filt);
+    prog = std::move(ap);
+  }
 }
 
 }  // namespace owqs

@@ -66,4 +66,10 @@ struct Program {
 // mode: 0 sampled / 1 forced (OWQS) or 2 EOWQS. seg_bits: 6 for complex64, 5 for complex128.
 Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int seg_bits, bool fuse);
 
+// Plan + compile for a mode. For EOWQS two candidates are compiled — PROA without dependencies
+// and the OWQS plan with its (identity) corrections dropped — and the one with the
+// smaller physical width, then fewer passes, is kept.
+void plan_and_compile(const HostPattern& hp, int mode, int seg_bits, bool fuse, bool given_order,
+                      const ProaWeights& w, Plan& plan, Program& prog);
+
 }  // namespace owqs

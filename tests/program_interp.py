@@ -88,19 +88,25 @@ class Interp:
             w = d.width
             n = 1 << w
             if d.kind == ST_PASS:
-                loc, coefs, conds = {}, {}, {}
+                loc, coefs, conds, bidx = {}, {}, {}, {}
                 bi = 0
                 for i in range(d.n_ops):
                     op = d.ops[i]
                     if op.type == OP_BFLY:
-                        coefs[i] = self.decide(op.m, bi == 0 and d.first_uses_red, False, loc)
+                        U = self.decide(op.m, bi == 0 and d.first_uses_red, False, loc)
+                        if op.cond and self.parity(op.sig_off, op.sig_len, loc):
+                            U = U[::-1].copy()  # folded X: swap output rows
+                        coefs[i] = U
+                        bidx[i] = bi
                         bi += 1
-                    else:
+                    elif op.type != 5:
                         conds[i] = self.parity(op.sig_off, op.sig_len, loc) if op.cond else 1
                 v = st[:n].copy()
                 idx = np.arange(n)
                 for i in range(d.n_ops):
                     op = d.ops[i]
+                    if op.type == 5:  # FLUSH: diagonals are applied directly here
+                        continue
                     if op.type in (OP_DIAG_E, OP_DIAG_Z):
                         if not conds[i]:
                             continue
@@ -115,6 +121,10 @@ class Interp:
                         i0 = idx[((idx >> a) & 1) == 0]
                         i1 = i0 | (1 << a)
                         x0, x1 = v[i0].copy(), v[i1].copy()
+                        if op.type == OP_BFLY:  # absorbed CZs: x1 sign by the parity of absorb bits
+                            am = d.absorb[bidx[i]]
+                            par = np.array([bin(int(j) & am).count("1") & 1 for j in i1]) if am else 0
+                            x1 = x1 * (1 - 2 * par)
                         v[i0] = U[0, 0] * x0 + U[0, 1] * x1
                         v[i1] = U[1, 0] * x0 + U[1, 1] * x1
                 if d.n_ops > 0:
