@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--flags", type=int, default=0, help="OWQS_FLAG_* for the timed context")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--ref-cmds", type=int, default=4, help="oracle sample: first k commands at full width")
+    ap.add_argument("--ref-cmds", type=int, default=None,
+                    help="oracle sample: first k commands at full width (default 4 for cpu_baseline, "
+                         "2 per step for --impl reference so K+W steps finish in minutes)")
     return ap.parse_args()
 
 
@@ -156,9 +158,9 @@ def run_reference(args, rank, world):
     n = len(pattern.inputs)
     psi = haar_state(n, 1)
     times = []
-    k = args.ref_cmds
+    k = args.ref_cmds or 2
     for s in range(args.warmup + args.steps):
-        dt, k = oracle_prefix_sample(pattern, psi, args.ref_cmds, seed=s)
+        dt, k = oracle_prefix_sample(pattern, psi, args.ref_cmds or 2, seed=s)
         if s >= args.warmup:
             times.append(dt)
     t = sum(times)
@@ -319,7 +321,7 @@ def run_ours(args, rank, world, local_rank):
         if args.no_e2e:
             psi_host = x.to(torch.complex128).cpu().numpy()
         psi_host = psi_host / np.linalg.norm(psi_host)
-        dt, k = oracle_prefix_sample(pattern, psi_host, args.ref_cmds, seed=1)
+        dt, k = oracle_prefix_sample(pattern, psi_host, args.ref_cmds or 4, seed=1)
         cpu = {"value": k / dt, "unit": "commands/s", "cores": 1, "kind": "oracle",
                "sample": f"oracle (numpy complex128, given order, single thread) on the first {k} commands "
                          f"of {args.workload} at full width ({n_in}->{n_in + 1} qubits): {dt:.1f} s",
