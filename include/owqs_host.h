@@ -32,15 +32,19 @@ typedef struct {
   int32_t step_bytes;   /* sizeof(StepDesc), for layout checks                              */
   int32_t mstatic_bytes;/* sizeof(MStatic)                                                  */
   int32_t n_passes, n_grow, n_shrink, n_reduce;
-  double bytes_per_run; /* analytic HBM bytes of one run at `precision`                     */
+  int32_t n_swaps;      /* global<->local qubit swaps (n_ranks > 1)                           */
+  int32_t n_global;     /* log2(n_ranks): top slot positions that are rank bits               */
+  double bytes_per_run; /* analytic HBM bytes of one run at `precision`, per rank             */
 } owqs_host_info;
 
 /* Validate + PROA + compile for `mode` (owqs_mode) at `precision` (64/128) with `flags`
- * (OWQS_FLAG_*). weights: NULL (paper defaults and tuning) or {alpha, beta, gamma, delta}. */
+ * (OWQS_FLAG_*). weights: NULL (paper defaults and tuning) or {alpha, beta, gamma, delta}.
+ * n_ranks: power of two; > 1 compiles the sharded program (the top log2(n_ranks)
+ * slot positions are rank bits; SWAP steps exchange a rank bit with a local bit). */
 owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t* outputs, int32_t n_out,
                               const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool, int64_t pool_len,
                               int32_t mode, int32_t precision, uint32_t flags, const double* weights,
-                              owqs_host_plan** out);
+                              int32_t n_ranks, owqs_host_plan** out);
 owqs_status owqs_host_info_get(const owqs_host_plan* h, owqs_host_info* info);
 /* Copy out the program. Any pointer may be NULL. steps: n_steps * step_bytes bytes; mst:
  * n_measure * mstatic_bytes bytes; sig: sig_len int32; out_slot: n_out int32 (slot of outputs[k]);

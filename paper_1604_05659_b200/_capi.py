@@ -95,7 +95,7 @@ class StepDesc(C.Structure):
                 ("n_ops", C.c_int32), ("red_kind", C.c_int32), ("red_slot", C.c_int32), ("slot", C.c_int32),
                 ("shrink_m", C.c_int32), ("n_bfly", C.c_int32), ("first_uses_red", C.c_int32),
                 ("first_full_rho", C.c_int32), ("pad", C.c_int32), ("ops", Op * MAX_OPS),
-                ("absorb", C.c_uint64 * MAX_BFLY)]
+                ("absorb", C.c_uint64 * MAX_BFLY), ("swap_local", C.c_int32), ("swap_global", C.c_int32)]
 
 
 class MStatic(C.Structure):
@@ -108,7 +108,7 @@ class owqs_host_info(C.Structure):
                 ("paper_m", C.c_int32), ("phys_bits", C.c_int32), ("in_width", C.c_int32), ("n_out", C.c_int32),
                 ("step_bytes", C.c_int32), ("mstatic_bytes", C.c_int32), ("n_passes", C.c_int32),
                 ("n_grow", C.c_int32), ("n_shrink", C.c_int32), ("n_reduce", C.c_int32),
-                ("bytes_per_run", C.c_double)]
+                ("n_swaps", C.c_int32), ("n_global", C.c_int32), ("bytes_per_run", C.c_double)]
 
 
 def declare_host(lib: C.CDLL) -> C.CDLL:
@@ -117,7 +117,7 @@ def declare_host(lib: C.CDLL) -> C.CDLL:
     sig = {
         "owqs_host_compile": (C.c_int, [P(C.c_int32), C.c_int32, P(C.c_int32), C.c_int32, P(owqs_cmd), C.c_int64,
                                         P(C.c_int32), C.c_int64, C.c_int32, C.c_int32, C.c_uint32,
-                                        P(C.c_double), P(h)]),
+                                        P(C.c_double), C.c_int32, P(h)]),
         "owqs_host_info_get": (C.c_int, [h, P(owqs_host_info)]),
         "owqs_host_program": (C.c_int, [h, C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32),
                                         P(C.c_int32)]),

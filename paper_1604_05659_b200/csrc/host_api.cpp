@@ -21,10 +21,13 @@ extern "C" {
 owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t* outputs, int32_t n_out,
                               const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool, int64_t pool_len,
                               int32_t mode, int32_t precision, uint32_t flags, const double* weights,
-                              owqs_host_plan** out) {
+                              int32_t n_ranks, owqs_host_plan** out) {
   if (!out) return OWQS_E_ARG;
   *out = nullptr;
   if ((precision != 64 && precision != 128) || mode < 0 || mode > 2) return OWQS_E_ARG;
+  if (n_ranks < 1 || (n_ranks & (n_ranks - 1))) return OWQS_E_ARG;
+  int n_global = 0;
+  while ((1 << n_global) < n_ranks) ++n_global;
   owqs_host_plan* h = new owqs_host_plan();
   *out = h;
   std::string e = validate_pattern(inputs, n_in, outputs, n_out, cmds, n_cmds, domain_pool, pool_len, h->hp);
@@ -41,8 +44,12 @@ owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t
   }
   if (flags & OWQS_FLAG_NO_TUNE) w.tune = false;
   plan_and_compile(h->hp, mode, precision == 64 ? 6 : 5, !(flags & OWQS_FLAG_NO_FUSE),
-                   (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w, h->plan, h->prog);
+                   (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w, h->plan, h->prog, n_global);
   h->elem = precision == 64 ? 8 : 16;
+  if (!h->prog.error.empty()) {
+    h->err = h->prog.error;
+    return OWQS_E_ARG;
+  }
   return OWQS_OK;
 }
 
@@ -62,6 +69,8 @@ owqs_status owqs_host_info_get(const owqs_host_plan* h, owqs_host_info* info) {
   info->n_grow = h->prog.n_grow;
   info->n_shrink = h->prog.n_shrink;
   info->n_reduce = h->prog.n_reduce;
+  info->n_swaps = h->prog.n_swaps;
+  info->n_global = h->prog.n_global;
   info->bytes_per_run = h->prog.bytes_per_run(h->elem);
   return OWQS_OK;
 }

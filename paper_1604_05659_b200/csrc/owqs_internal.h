@@ -32,7 +32,7 @@ constexpr int MAX_OPS = 64;      // ops per pass (incl. compiler-placed flushes)
 constexpr int KMAX_HI = 4;       // group slots above the warp segment per pass
 constexpr int MAX_BFLY = 24;     // butterflies per pass (fused mode)
 
-enum StepKind : int32_t { ST_PASS = 0, ST_GROW = 1, ST_SHRINK = 2 };
+enum StepKind : int32_t { ST_PASS = 0, ST_GROW = 1, ST_SHRINK = 2, ST_SWAP = 3 };
 enum RedKind : int32_t { RED_NONE = 0, RED_NORM = 1, RED_RHO = 2 };
 
 // One device step. Passed by value as a kernel parameter.
@@ -54,6 +54,9 @@ struct StepDesc {
   // absorb[bi]: slots whose bits flip the sign of butterfly bi's coefficient a — the CZ's
   // E(o, a) absorbed into the first following butterfly on slot a (U Z^{x_o} = k[[1,-+a],[1,+-a]])
   uint64_t absorb[MAX_BFLY];
+  // ST_SWAP (multi-rank): exchange the qubit at global position swap_global (a rank bit) with the
+  // one at local position swap_local; each rank trades half of its shard with rank ^ (1 << (g - wl))
+  int32_t swap_local, swap_global;
 };
 
 // Static record of one measurement (plan order). Uploaded once per compiled plan.
@@ -86,6 +89,8 @@ struct DevPtrs {
   unsigned int* counter;       // last-block-done counter
   double* red_result;          // [4]
   int32_t* err;                // device error flag (1 = forced branch with prob < 1e-12)
+  uint32_t rank;               // multi-rank: this shard's rank = the global (top) index bits
+  int32_t local_width;         // multi-rank: bits of the shard index (positions >= are rank bits)
 };
 
 }  // namespace owqs

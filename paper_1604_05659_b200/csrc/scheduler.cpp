@@ -600,6 +600,8 @@ double Program::bytes_per_run(int eb) const {
       b += s.n_ops > 0 ? 2 * S : S;
     else if (s.kind == ST_GROW)
       b += 3 * S;
+    else if (s.kind == ST_SWAP)
+      b += 2 * S;  // pack (read S/2, write S/2) + unpack (read S/2, write S/2)
     else
       b += 1.5 * S;
   }
@@ -624,10 +626,23 @@ struct Packer {
   const int max_bfly;
   int width;
   int kmax_hi = KMAX_HI;
+  const int n_global;         // log2(ranks); positions >= width - n_global are rank bits
+  std::vector<int> pos, at;   // virtual slot -> physical position, and back
 
-  Packer(const std::vector<LOp>& o, Program& p, int sb, bool e, int mb)
-      : ops(o), mst(p.mst), pr(p), SB(sb), eowqs(e), max_bfly(mb), width(p.in_width) {
+  Packer(const std::vector<LOp>& o, Program& p, int sb, bool e, int mb, int ng)
+      : ops(o), mst(p.mst), pr(p), SB(sb), eowqs(e), max_bfly(mb), width(p.in_width), n_global(ng) {
     if (const char* env = getenv("OWQS_KMAX_HI")) kmax_hi = std::max(0, std::min(KMAX_HI, atoi(env)));
+    for (int v = 0; v < 64; ++v) {
+      pos.push_back(v);
+      at.push_back(v);
+    }
+  }
+  int wl() const { return width - n_global; }
+  // last step that computes something (a SWAP only permutes: it preserves the norm)
+  StepDesc* last_compute() {
+    for (int i = (int)pr.steps.size() - 1; i >= 0; --i)
+      if (pr.steps[i].kind != ST_SWAP) return &pr.steps[i];
+    return nullptr;
   }
 
   void emit(const StepDesc& s) {
@@ -639,7 +654,7 @@ struct Packer {
   StepDesc blank(int kind) const {
     StepDesc d{};
     d.kind = kind;
-    d.width = width;
+    d.width = width - n_global;  // the shard's width
     d.red_slot = -1;
     d.slot = -1;
     d.shrink_m = -1;
@@ -647,9 +662,10 @@ struct Packer {
   }
   // the state produced by the last emitted step must carry its norm (first butterfly of a pass)
   void need_norm_before() {
-    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NORM) return;
-    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE) {
-      pr.steps.back().red_kind = RED_NORM;
+    StepDesc* last = last_compute();
+    if (last && last->red_kind == RED_NORM) return;
+    if (last && last->red_kind == RED_NONE) {
+      last->red_kind = RED_NORM;
       return;
     }
     StepDesc r = blank(ST_PASS);
@@ -811,6 +827,7 @@ struct Packer {
     int remaining = N;
     while (remaining > 0) {
       StepDesc cur = blank(ST_PASS);
+      const int WL = wl();
       auto has_slot = [&](int a) {
         if (a < SB) return true;
         for (int j = 0; j < cur.nb_hi; ++j)
@@ -825,7 +842,9 @@ struct Packer {
           const Node& n = nodes[ready[k]];
           const LOp& l = ops[n.op];
           if (l.type == 4 && cur.n_bfly >= max_bfly) continue;
-          bool fits = (l.type == 1 || l.type == 2) || has_slot(l.a);
+          const bool diag = l.type == 1 || l.type == 2;
+          if (!diag && pos[l.a] >= WL) continue;  // 2x2 on a rank bit: needs a SWAP first
+          bool fits = diag || has_slot(pos[l.a]);
           if (fits) {
             if (best < 0 || n.op < nodes[ready[best]].op) best = k;
           } else if (cur.nb_hi < kmax_hi) {
@@ -839,14 +858,14 @@ struct Packer {
         ready.pop_back();
         Node& n = nodes[id];
         const LOp& l = ops[n.op];
-        if ((l.type == 3 || l.type == 4) && !has_slot(l.a)) {
-          cur.bhi[cur.nb_hi++] = l.a;
+        if ((l.type == 3 || l.type == 4) && !has_slot(pos[l.a])) {
+          cur.bhi[cur.nb_hi++] = pos[l.a];
           std::sort(cur.bhi, cur.bhi + cur.nb_hi);
         }
         Op o{};
         o.type = (uint8_t)l.type;
-        o.a = (uint8_t)std::max(l.a, 0);
-        o.b = (uint8_t)std::max(l.b, 0);
+        o.a = (uint8_t)pos[std::max(l.a, 0)];
+        o.b = (uint8_t)pos[std::max(l.b, 0)];
         o.m = l.m;
         if (l.type == 4) {
           push_sig(o, n.xsig);  // cond/sig of a butterfly = folded X_a^s
@@ -861,7 +880,40 @@ struct Packer {
         for (int s : n.succ)
           if (--nodes[s].npred == 0) ready.push_back(s);
       }
-      if (cur.n_ops == 0) break;  // cannot happen: some op is always ready
+      if (cur.n_ops == 0) {
+        // every ready op is a 2x2 on a rank bit: bring its qubit into the shard, evicting the
+        // local qubit whose next 2x2 is farthest away (Belady); light-cone skew falls out of the
+        // list scheduler advancing everything local first
+        int g = -1, gop = 1 << 30;
+        for (int id : ready) {
+          const LOp& l = ops[nodes[id].op];
+          if ((l.type == 3 || l.type == 4) && pos[l.a] >= WL && nodes[id].op < gop) {
+            gop = nodes[id].op;
+            g = l.a;
+          }
+        }
+        if (g < 0) break;  // cannot happen
+        std::vector<int> next_use(64, 1 << 30);
+        for (const Node& nd : nodes)
+          if (!nd.done) {
+            const LOp& l = ops[nd.op];
+            if (l.type == 3 || l.type == 4) next_use[l.a] = std::min(next_use[l.a], nd.op);
+          }
+        int victim = -1;
+        for (int p = WL - 1; p >= 0; --p) {
+          const int v = at[p];
+          if (victim < 0 || next_use[v] > next_use[victim]) victim = v;
+        }
+        StepDesc sw = blank(ST_SWAP);
+        sw.swap_local = pos[victim];
+        sw.swap_global = pos[g];
+        emit(sw);
+        ++pr.n_swaps;
+        std::swap(pos[victim], pos[g]);
+        at[pos[victim]] = victim;
+        at[pos[g]] = g;
+        continue;
+      }
       if (cur.first_uses_red) need_norm_before();
       absorb_and_flush(cur);
       emit(cur);
@@ -913,9 +965,10 @@ struct Packer {
       }
     }
     // final norm of the output state (EOWQS determinism check / drift report)
-    if (!pr.steps.empty() && pr.steps.back().red_kind == RED_NONE)
-      pr.steps.back().red_kind = RED_NORM;
-    else if (pr.steps.empty() || pr.steps.back().red_kind != RED_NORM) {
+    StepDesc* lc = last_compute();
+    if (lc && lc->red_kind == RED_NONE)
+      lc->red_kind = RED_NORM;
+    else if (!lc || lc->red_kind != RED_NORM || pr.steps.back().kind == ST_SWAP) {
       StepDesc r = blank(ST_PASS);
       r.red_kind = RED_NORM;
       emit(r);
@@ -927,7 +980,7 @@ struct Packer {
 
 }  // namespace
 
-Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse) {
+Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse, int n_global) {
   const bool eowqs = mode == 2;
   Emitter em(hp, eowqs);
   em.run(plan);
@@ -936,21 +989,33 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
   pr.sig_pool = em.pool;
   pr.phys_bits = em.max_width;
   pr.in_width = (int)hp.inputs.size();
-  for (int o : hp.outputs) pr.out_slot.push_back(em.slot_of[o]);
-  Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1);
+  pr.n_global = n_global;
+  if (n_global > 0) {
+    for (const LOp& l : em.ops)
+      if (l.type == 10 || l.type == 11) {
+        pr.error = "multi-rank execution needs a constant-width program (no GROW / SHRINK)";
+        return pr;
+      }
+    if (pr.in_width - n_global < 2) {
+      pr.error = "state too narrow for " + std::to_string(1 << n_global) + " ranks";
+      return pr;
+    }
+  }
+  Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1, n_global);
   pk.run();
+  for (int o : hp.outputs) pr.out_slot.push_back(pk.pos[em.slot_of[o]]);
   return pr;
 }
 
 void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool given, const ProaWeights& w,
-                      Plan& plan, Program& prog) {
+                      Plan& plan, Program& prog, int n_global) {
   if (mode != 2) {
     plan = make_plan(hp, false, given, w);
-    prog = compile_program(hp, plan, mode, SB, fuse);
+    prog = compile_program(hp, plan, mode, SB, fuse, n_global);
     return;
   }
   plan = make_plan(hp, true, given, w);
-  prog = compile_program(hp, plan, 2, SB, fuse);
+  prog = compile_program(hp, plan, 2, SB, fuse, n_global);
   Plan alt = make_plan(hp, false, given, w);
   Plan filt;
   for (int c : alt.order)
@@ -958,8 +1023,10 @@ void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool g
   filt.m_cmds = alt.m_cmds;
   filt.ms = alt.ms;
   filt.paper_m = alt.paper_m;
-  Program ap = compile_program(hp, filt, 2, SB, fuse);
-  if (ap.phys_bits < prog.phys_bits || (ap.phys_bits == prog.phys_bits && ap.n_passes < prog.n_passes)) {
+  Program ap = compile_program(hp, filt, 2, SB, fuse, n_global);
+  if (!prog.error.empty() ||
+      (ap.error.empty() && (ap.phys_bits < prog.phys_bits ||
+                            (ap.phys_bits == prog.phys_bits && ap.n_passes + ap.n_swaps < prog.n_passes + prog.n_swaps)))) {
     plan = std::move(filt);
     prog = std::move(ap);
   }

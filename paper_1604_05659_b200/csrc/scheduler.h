@@ -59,17 +59,20 @@ struct Program {
   int phys_bits = 0;               // max width
   int in_width = 0;
   std::vector<int> out_slot;       // slot of outputs[k] at the end
-  int n_passes = 0, n_grow = 0, n_shrink = 0, n_reduce = 0;
-  double bytes_per_run(int elem_bytes) const;
+  int n_passes = 0, n_grow = 0, n_shrink = 0, n_reduce = 0, n_swaps = 0;
+  int n_global = 0;                // log2(ranks): top slot positions that are rank bits
+  std::string error;               // non-empty: the program cannot be built (e.g. sharding)
+  double bytes_per_run(int elem_bytes) const;  // per rank
 };
 
 // mode: 0 sampled / 1 forced (OWQS) or 2 EOWQS. seg_bits: 6 for complex64, 5 for complex128.
-Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int seg_bits, bool fuse);
+Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int seg_bits, bool fuse,
+                        int n_global = 0);
 
 // Plan + compile for a mode. For EOWQS two candidates are compiled — PROA without dependencies
 // and the OWQS plan with its (identity) corrections dropped — and the one with the
 // smaller physical width, then fewer passes, is kept.
 void plan_and_compile(const HostPattern& hp, int mode, int seg_bits, bool fuse, bool given_order,
-                      const ProaWeights& w, Plan& plan, Program& prog);
+                      const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0);
 
 }  // namespace owqs

@@ -24,13 +24,13 @@ class HostProgram:
 
 
 def compile_host(pattern, mode: str = "sampled", precision: int = 128, flags: int = 0,
-                 weights: Optional[Sequence[float]] = None) -> HostProgram:
+                 weights: Optional[Sequence[float]] = None, n_ranks: int = 1) -> HostProgram:
     L = lib()
     i, o, arr, pool, plen = marshal_pattern(pattern.inputs, pattern.outputs, pattern.cmds)
     w = (C.c_double * 4)(*weights) if weights is not None else None
     h = C.c_void_p()
     st = L.owqs_host_compile(i, len(pattern.inputs), o, len(pattern.outputs), arr, len(pattern.cmds), pool, plen,
-                             MODE_IDS[mode], precision, flags, w, C.byref(h))
+                             MODE_IDS[mode], precision, flags, w, n_ranks, C.byref(h))
     try:
         if st != 0:
             msg = L.owqs_host_error(h) if h else b""

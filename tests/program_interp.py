@@ -29,8 +29,13 @@ def _draw(seed, ord_):
 
 
 class Interp:
-    def __init__(self, prog, mode: str, seed: int = 0, forced=None):
+    """rank / world / comm: sharded execution (n_global = log2(world) top positions are rank bits);
+    comm provides all_reduce_sum(np.ndarray) and exchange(np.ndarray, partner) -> np.ndarray."""
+
+    def __init__(self, prog, mode: str, seed: int = 0, forced=None, rank: int = 0, world: int = 1, comm=None):
         self.p = prog
+        self.rank, self.world, self.comm = rank, world, comm
+        self.ng = prog.info.get("n_global", 0)
         self.mode = {"sampled": 0, "forced": 1, "eowqs": 2}[mode]
         self.seed = seed
         K = prog.info["n_measure"]
@@ -81,12 +86,30 @@ class Interp:
         loc[ms.ord] = outc
         return U
 
+    def _allreduce(self):
+        if self.world > 1:
+            self.red = self.comm.all_reduce_sum(self.red.copy())
+
     def run(self, psi):
-        st = np.zeros(2 ** self.p.info["phys_bits"], dtype=np.complex128)
-        st[: psi.size] = psi
+        """psi: the full input state (each rank takes its shard); returns the shard (world > 1)
+        or the permuted output (world == 1)."""
+        wl = self.p.info["phys_bits"] - self.ng
+        if self.world > 1:
+            st = psi[self.rank << wl:(self.rank + 1) << wl].astype(np.complex128).copy()
+        else:
+            st = np.zeros(2 ** self.p.info["phys_bits"], dtype=np.complex128)
+            st[: psi.size] = psi
         for d in self.p.steps:
             w = d.width
             n = 1 << w
+            if d.kind == 3:  # SWAP: trade the half with local bit = 1 - (rank bit) with the partner
+                gb = d.swap_global - w
+                b = (self.rank >> gb) & 1
+                partner = self.rank ^ (1 << gb)
+                idx = np.arange(n)
+                half = idx[((idx >> d.swap_local) & 1) == 1 - b]
+                st[half] = self.comm.exchange(st[half].copy(), partner)
+                continue
             if d.kind == ST_PASS:
                 loc, coefs, conds, bidx = {}, {}, {}, {}
                 bi = 0
@@ -102,7 +125,7 @@ class Interp:
                     elif op.type != 5:
                         conds[i] = self.parity(op.sig_off, op.sig_len, loc) if op.cond else 1
                 v = st[:n].copy()
-                idx = np.arange(n)
+                idx = np.arange(n) | (self.rank << w)  # global index (rank bits on top)
                 for i in range(d.n_ops):
                     op = d.ops[i]
                     if op.type == 5:  # FLUSH: diagonals are applied directly here
@@ -118,24 +141,29 @@ class Interp:
                             continue
                         U = coefs[i] if op.type == OP_BFLY else np.array([[0, 1], [1, 0]])
                         a = op.a
-                        i0 = idx[((idx >> a) & 1) == 0]
+                        loc = np.arange(n)
+                        i0 = loc[((loc >> a) & 1) == 0]
                         i1 = i0 | (1 << a)
                         x0, x1 = v[i0].copy(), v[i1].copy()
                         if op.type == OP_BFLY:  # absorbed CZs: x1 sign by the parity of absorb bits
                             am = d.absorb[bidx[i]]
-                            par = np.array([bin(int(j) & am).count("1") & 1 for j in i1]) if am else 0
+                            par = (np.array([bin(int(j) & am).count("1") & 1 for j in idx[i1]])
+                                   if am else 0)
                             x1 = x1 * (1 - 2 * par)
                         v[i0] = U[0, 0] * x0 + U[0, 1] * x1
                         v[i1] = U[1, 0] * x0 + U[1, 1] * x1
                 if d.n_ops > 0:
                     st[:n] = v
-                self._reduce(d, v, idx)
+                self._reduce(d, v, np.arange(n))
+                if d.red_kind != RED_NONE:
+                    self._allreduce()
             elif d.kind == ST_GROW:
                 x = st[:n] / math.sqrt(2)
                 st[:n] = x
                 st[n:2 * n] = x
                 if d.red_kind == RED_NORM:
                     self.red[:] = [np.vdot(st[:2 * n], st[:2 * n]).real, 0, 0, 0]
+                    self._allreduce()
             else:
                 U = self.decide(d.shrink_m, True, bool(d.first_full_rho), {})
                 b, top = d.slot, w - 1
@@ -152,6 +180,12 @@ class Interp:
                 if d.red_kind == RED_NORM:
                     h = n // 2
                     self.red[:] = [np.vdot(st[:h], st[:h]).real, 0, 0, 0]
+                    self._allreduce()
+        if self.world > 1:
+            return st[: 1 << wl]
+        return self.permute_out(st)
+
+    def permute_out(self, st):
         n_out = self.p.info["n_out"]
         j = np.arange(2 ** n_out)
         src = np.zeros_like(j)
