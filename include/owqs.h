@@ -88,6 +88,11 @@ typedef struct {
 #define OWQS_FLAG_NO_TUNE     0x8u /* PROA with the initial weights only (no L487 tuning loop)   */
 #define OWQS_FLAG_PROFILE     0x10u /* record a CUDA event after every kernel of owqs_run (event
                                        record nodes in the graph); see owqs_launch_profile       */
+#define OWQS_FLAG_LOOPBACK    0x20u /* n_ranks > 1 on ONE device: the context holds every rank's
+                                       shard and runs them one after the other (swaps and
+                                       all-reduces by device copies); for testing the sharded path
+                                       on one GPU. Without it, n_ranks > 1 means one process per GPU
+                                       over NCCL (nccl_id from owqs_nccl_unique_id)              */
 
 /* Kernel classes reported by owqs_launch_profile. */
 #define OWQS_KCLASS_PASS   0 /* fused warp-segment pass kernel (read + write the state)          */
@@ -95,6 +100,7 @@ typedef struct {
 #define OWQS_KCLASS_GROW   2 /* append |+> (N without a measurement to absorb it)                 */
 #define OWQS_KCLASS_SHRINK 3 /* measurement with elimination (no fresh neighbour)                 */
 #define OWQS_KCLASS_REDUCE 4 /* read-only pass: probability / norm reduction only                 */
+#define OWQS_KCLASS_SWAP   5 /* multi-rank global<->local qubit swap (pack, exchange, unpack)       */
 
 typedef enum { OWQS_SAMPLED = 0, OWQS_FORCED = 1, OWQS_EOWQS = 2 } owqs_mode;
 
@@ -114,8 +120,14 @@ typedef struct {
   double reserved[4];
 } owqs_stats_t;
 
-/* Create / destroy a context on cfg->device. */
+/* Create / destroy a context on cfg->device.
+ * Multi-rank: n_ranks = G (power of two) shards the state on its top log2(G) slot
+ * positions (rank bits); every rank makes the same call sequence (SPMD). With NCCL, nccl_id points
+ * to a 128-byte ncclUniqueId made by owqs_nccl_unique_id on one rank and broadcast by the caller;
+ * the library owns the communicator. Errors: OWQS_E_ARG, OWQS_E_CUDA, OWQS_E_NCCL. */
 owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out);
+/* Write a fresh 128-byte ncclUniqueId to out (call on one rank, broadcast to the others). */
+owqs_status owqs_nccl_unique_id(void* out);
 void owqs_destroy(owqs_ctx* ctx);
 
 /* Load a pattern in its GIVEN (execution) order (L67; right-to-left notation already reversed).
@@ -131,11 +143,13 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
 
 /* Input state of the input qubits (L153). amps: HOST array of n_amps = 2^n_in complex128 values,
  * interleaved (re, im). Copied to the device (converted to complex64 at precision 64).
+ * Multi-rank: every rank passes the full array; each copies its shard.
  * Errors: OWQS_E_ARG (size), OWQS_E_STATE (no pattern), OWQS_E_NOMEM, OWQS_E_CUDA. */
 owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps);
 
 /* Same from a DEVICE buffer on the context's device. precision 64: interleaved float pairs;
- * 128: interleaved double pairs. The buffer is read during the call only. */
+ * 128: interleaved double pairs. The buffer is read during the call only. NCCL multi-rank: the
+ * buffer holds this rank's shard (n_amps = 2^n_in / n_ranks); loopback: the full state. */
 owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t precision, int64_t n_amps);
 
 /* Device-generated Haar-random input (documented counter generator, workloads/inputs.py):
@@ -155,15 +169,20 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
                      uint8_t* outcomes_out, double* prob0_out);
 
 /* Output state over O (L153, L419): HOST array of n_amps >= 2^n_out complex128, interleaved,
- * bit k <-> outputs[k]. Multi-rank: filled on rank 0 only (amps may be NULL elsewhere). */
+ * bit k <-> outputs[k]. Multi-rank (collective): gathered to rank 0, filled on rank 0 only
+ * (amps may be NULL elsewhere); needs 2^n_out complex128 of free device memory on rank 0. */
 owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps);
 
 /* Output into a DEVICE buffer (precision 64: float pairs, 128: double pairs), n_amps >= 2^n_out
  * (single rank). */
 owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precision, int64_t n_amps);
 
-/* <a|b> of the output states of two contexts with the same output qubits, on the device. */
+/* <a|b> of the output states of two contexts with the same output qubits, on the device.
+ * Multi-rank: both contexts need the same sharding and final layout (collective call). */
 owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im);
+
+/* ||output||^2 on the device (all-reduced over ranks; collective call). */
+owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2);
 
 /* Recognition problem (L33): the unitary implemented by the loaded (deterministic) pattern.
  * Column k = EOWQS run on basis input |k> (all outcomes 0, sqrt2 per M: a linear map).

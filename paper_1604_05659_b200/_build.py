@@ -63,7 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                   "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(CUDA_HOME, "include"), "-c", s, "-o", o])
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread", "-ldl"])
+        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xlinker", "--no-undefined",
+              "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lpthread", "-ldl", "-lrt"])
         shutil.move(tmp, LIB)
     return LIB
 

@@ -12,13 +12,14 @@ STATUS_NAMES = {0: "OWQS_OK", 1: "OWQS_E_ARG", 2: "OWQS_E_PATTERN", 3: "OWQS_E_N
                 5: "OWQS_E_STATE", 6: "OWQS_E_NOMEM", 7: "OWQS_E_CUDA", 8: "OWQS_E_NCCL",
                 9: "OWQS_E_NOT_DETERMINISTIC"}
 MODES = {"sampled": 0, "forced": 1, "eowqs": 2}
-FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE = 1, 2, 4, 8, 16
-KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce"}
+FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE, FLAG_LOOPBACK = 1, 2, 4, 8, 16, 32
+KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = ["owqs_create", "owqs_destroy", "owqs_load_pattern", "owqs_set_input", "owqs_set_input_device",
             "owqs_set_input_random", "owqs_run", "owqs_get_output", "owqs_get_output_device",
-            "owqs_output_inner", "owqs_recognize", "owqs_pattern_info", "owqs_plan_order",
+            "owqs_output_inner", "owqs_output_norm", "owqs_nccl_unique_id", "owqs_recognize",
+            "owqs_pattern_info", "owqs_plan_order",
             "owqs_set_proa_weights", "owqs_stats", "owqs_launch_profile", "owqs_last_error", "owqs_version"]
 
 
@@ -63,6 +64,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "owqs_get_output": (C.c_int, [ctx, P(C.c_double), C.c_int64]),
         "owqs_get_output_device": (C.c_int, [ctx, C.c_void_p, C.c_int32, C.c_int64]),
         "owqs_output_inner": (C.c_int, [ctx, ctx, P(C.c_double), P(C.c_double)]),
+        "owqs_output_norm": (C.c_int, [ctx, P(C.c_double)]),
+        "owqs_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "owqs_recognize": (C.c_int, [ctx, P(C.c_double), C.c_int64, P(C.c_double)]),
         "owqs_pattern_info": (C.c_int, [ctx, P(C.c_int64), P(C.c_int32), P(C.c_int32), P(C.c_int32)]),
         "owqs_plan_order": (C.c_int, [ctx, C.c_int, P(C.c_int32), P(C.c_int32), C.c_int64]),

@@ -1,5 +1,6 @@
-// C-ABI implementation (include/owqs.h): context, device memory, CUDA-graph executor.
+// C-ABI implementation (include/owqs.h): context, device memory, CUDA-graph executor, sharding.
 #include <cuda_runtime.h>
+#include <nccl.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -18,11 +19,19 @@ int max_partial_blocks();
 cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s);
 cudaError_t launch_permute_out(const void* state, int prec, void* out, int out_prec, int nbits, const int* slots,
                                uint64_t j0, uint64_t count, cudaStream_t s);
+cudaError_t launch_scatter_out(const void* shard, int prec, void* out, int out_prec, int nbits, const int* slots,
+                               uint64_t rank, int wl, cudaStream_t s);
 cudaError_t launch_convert_in(const void* src, int src_prec, void* state, int prec, uint64_t j0, uint64_t count,
                               cudaStream_t s);
 cudaError_t launch_basis(void* state, int prec, uint64_t n, uint64_t k, cudaStream_t s);
-cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, cudaStream_t s);
+cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, uint64_t j0, cudaStream_t s);
+cudaError_t launch_scale(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
+cudaError_t launch_norm(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
 cudaError_t launch_dot(const DevPtrs& p, const void* a, const void* b, uint64_t n, cudaStream_t s);
+cudaError_t launch_dot_t(const DevPtrs& p, int prec, const void* a, const void* b, uint64_t n, cudaStream_t s);
+cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_width, int pl, int bit, bool unpack,
+                             cudaStream_t s);
+cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
 }  // namespace owqs
 
@@ -38,6 +47,14 @@ struct CompiledMode {
   cudaGraphExec_t gexec = nullptr;
   double schedule_ms = 0;
 };
+// one rank's part of the state and its reduction scratch
+struct Shard {
+  void* d_state = nullptr;
+  double* d_partials = nullptr;
+  unsigned* d_counter = nullptr;
+  int32_t* d_err = nullptr;
+  double* d_red = nullptr;  // -> ctx->d_red_all + 4 * index
+};
 constexpr size_t kStagingBytes = 64ull << 20;
 }  // namespace
 
@@ -52,12 +69,15 @@ struct owqs_ctx {
   bool loaded = false;
   CompiledMode cm[2];  // 0 OWQS (sampled / forced), 1 EOWQS
   ProaWeights weights;
-  void* d_state = nullptr;
-  size_t state_bytes = 0;
-  double* d_partials = nullptr;
-  unsigned* d_counter = nullptr;
-  double* d_red = nullptr;
-  int32_t* d_err = nullptr;
+  // sharding
+  int n_ranks = 1, rank = 0, n_global = 0;
+  bool loopback = false;
+  ncclComm_t comm = nullptr;
+  std::vector<Shard> shards;  // 1, or n_ranks in loopback mode
+  double* d_red_all = nullptr;
+  size_t shard_bytes = 0;
+  void* d_swap = nullptr;  // two half-shard buffers (send, receive)
+  // run state
   RunParams* d_run = nullptr;
   uint8_t* d_outcome = nullptr;
   double* d_prob0 = nullptr;
@@ -72,6 +92,8 @@ struct owqs_ctx {
   int last_cm = 0;
   std::vector<cudaEvent_t> prof_ev;  // OWQS_FLAG_PROFILE: event after every launch (+1 start)
   int prof_cm = -1;
+
+  uint32_t shard_rank(int i) const { return loopback ? (uint32_t)i : (uint32_t)rank; }
 };
 
 namespace {
@@ -89,19 +111,28 @@ owqs_status fail(owqs_ctx* c, owqs_status s, const std::string& m) {
                   std::string(#call) + ": " + cudaGetErrorString(e_));                    \
   } while (0)
 
-DevPtrs dev_ptrs(owqs_ctx* ctx, const CompiledMode& m) {
+#define NC(call)                                                                              \
+  do {                                                                                        \
+    ncclResult_t r_ = (call);                                                                 \
+    if (r_ != ncclSuccess) return fail(ctx, OWQS_E_NCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+DevPtrs dev_ptrs(owqs_ctx* ctx, const CompiledMode& m, int i) {
   DevPtrs p{};
-  p.state = ctx->d_state;
+  const Shard& s = ctx->shards[i];
+  p.state = s.d_state;
   p.mst = m.d_mst;
   p.outcome = ctx->d_outcome;
   p.prob0 = ctx->d_prob0;
   p.forced = ctx->d_forced;
   p.sig_pool = m.d_sig;
   p.run = ctx->d_run;
-  p.partials = ctx->d_partials;
-  p.counter = ctx->d_counter;
-  p.red_result = ctx->d_red;
-  p.err = ctx->d_err;
+  p.partials = s.d_partials;
+  p.counter = s.d_counter;
+  p.red_result = s.d_red;
+  p.err = s.d_err;
+  p.rank = ctx->shard_rank(i);
+  p.local_width = m.prog.phys_bits - ctx->n_global;
   return p;
 }
 
@@ -110,6 +141,14 @@ void free_mode(CompiledMode& m) {
   if (m.d_mst) cudaFree(m.d_mst);
   if (m.d_sig) cudaFree(m.d_sig);
   m = CompiledMode();
+}
+
+void drop_graphs(owqs_ctx* ctx) {
+  for (int i = 0; i < 2; ++i)
+    if (ctx->cm[i].gexec) {
+      cudaGraphExecDestroy(ctx->cm[i].gexec);
+      ctx->cm[i].gexec = nullptr;
+    }
 }
 
 owqs_status compile_modes(owqs_ctx* ctx) {
@@ -122,13 +161,13 @@ owqs_status compile_modes(owqs_ctx* ctx) {
     free_mode(ctx->cm[i]);
     auto t0 = std::chrono::steady_clock::now();
     CompiledMode& m = ctx->cm[i];
-    plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog);
-    for (const auto& s : m.prog.steps)
-      if (s.kind == ST_PASS && s.width > 12 && s.width - SB - s.nb_hi < 0)
-        return fail(ctx, OWQS_E_PATTERN, "internal: pass grouping exceeds the register file");
+    plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog, ctx->n_global);
+    if (!m.prog.error.empty()) return fail(ctx, OWQS_E_ARG, m.prog.error);
     m.schedule_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     m.valid = true;
   }
+  if (ctx->n_global > 0 && ctx->cm[0].prog.phys_bits != ctx->cm[1].prog.phys_bits)
+    return fail(ctx, OWQS_E_ARG, "multi-rank: OWQS and EOWQS programs differ in width");
   return OWQS_OK;
 }
 
@@ -136,24 +175,26 @@ owqs_status ensure_device(owqs_ctx* ctx) {
   CU(cudaSetDevice(ctx->cfg.device));
   int phys = 0;
   for (int i = 0; i < 2; ++i) phys = std::max(phys, ctx->cm[i].prog.phys_bits);
-  size_t need = (size_t)ctx->elem << phys;
-  need = std::max<size_t>(need, 64);
-  if (ctx->state_bytes < need) {
-    if (ctx->d_state) cudaFree(ctx->d_state);
-    ctx->d_state = nullptr;
-    ctx->state_bytes = 0;
-    for (int i = 0; i < 2; ++i)
-      if (ctx->cm[i].gexec) {
-        cudaGraphExecDestroy(ctx->cm[i].gexec);
-        ctx->cm[i].gexec = nullptr;
-      }
+  const int wl = phys - ctx->n_global;
+  size_t need = std::max<size_t>((size_t)ctx->elem << wl, 64);
+  if (ctx->shard_bytes < need) {
+    drop_graphs(ctx);
+    for (auto& s : ctx->shards) {
+      cudaFree(s.d_state);
+      s.d_state = nullptr;
+    }
+    cudaFree(ctx->d_swap);
+    ctx->d_swap = nullptr;
+    ctx->shard_bytes = 0;
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
-    if (need > free_b)
-      return fail(ctx, OWQS_E_NOMEM, "state of 2^" + std::to_string(phys) + " amplitudes (" +
-                                         std::to_string(need >> 20) + " MiB) exceeds free device memory");
-    CU(cudaMalloc(&ctx->d_state, need));
-    ctx->state_bytes = need;
+    const size_t total_need = need * ctx->shards.size() + (ctx->n_global > 0 ? need : 0);
+    if (total_need > free_b)
+      return fail(ctx, OWQS_E_NOMEM, "state shard(s) of 2^" + std::to_string(wl) + " amplitudes (" +
+                                         std::to_string(total_need >> 20) + " MiB) exceed free device memory");
+    for (auto& s : ctx->shards) CU(cudaMalloc(&s.d_state, need));
+    if (ctx->n_global > 0) CU(cudaMalloc(&ctx->d_swap, need));  // two halves: send | receive
+    ctx->shard_bytes = need;
   }
   size_t K = std::max<size_t>(1, (size_t)ctx->hp.n_measure);
   if (ctx->k_cap < K) {
@@ -165,11 +206,7 @@ owqs_status ensure_device(owqs_ctx* ctx) {
     CU(cudaMalloc(&ctx->d_forced, K));
     CU(cudaMemset(ctx->d_outcome, 0, K));
     ctx->k_cap = K;
-    for (int i = 0; i < 2; ++i)
-      if (ctx->cm[i].gexec) {
-        cudaGraphExecDestroy(ctx->cm[i].gexec);
-        ctx->cm[i].gexec = nullptr;
-      }
+    drop_graphs(ctx);
   }
   for (int i = 0; i < 2; ++i) {
     CompiledMode& m = ctx->cm[i];
@@ -185,6 +222,44 @@ owqs_status ensure_device(owqs_ctx* ctx) {
   return OWQS_OK;
 }
 
+// all-reduce of every shard's red_result (sum over ranks)
+owqs_status allreduce_red(owqs_ctx* ctx) {
+  if (ctx->n_ranks == 1) return OWQS_OK;
+  if (ctx->loopback) {
+    CU(launch_loopback_allreduce(ctx->d_red_all, ctx->n_ranks, ctx->stream));
+  } else {
+    NC(ncclAllReduce(ctx->d_red_all, ctx->d_red_all, 4, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  }
+  return OWQS_OK;
+}
+
+// ST_SWAP: every rank trades the half of its shard whose bit `pl` = 1 - (its rank bit) with rank ^ m
+owqs_status do_swap(owqs_ctx* ctx, const StepDesc& d) {
+  const int wl = d.width, pl = d.swap_local, gbit = d.swap_global - wl;
+  const size_t half = ((size_t)ctx->elem << wl) / 2;
+  char* sendb = (char*)ctx->d_swap;
+  char* recvb = sendb + half;
+  if (ctx->loopback) {
+    for (int r = 0; r < ctx->n_ranks; ++r) {
+      const int p = r ^ (1 << gbit);
+      if (p < r) continue;  // r has rank bit 0 (trades its bit-pl = 1 half), p has 1 (bit-pl = 0 half)
+      CU(launch_swap_pack(ctx->shards[r].d_state, sendb, ctx->prec, wl, pl, 1, false, ctx->stream));
+      CU(launch_swap_pack(ctx->shards[p].d_state, recvb, ctx->prec, wl, pl, 0, false, ctx->stream));
+      CU(launch_swap_pack(ctx->shards[r].d_state, recvb, ctx->prec, wl, pl, 1, true, ctx->stream));
+      CU(launch_swap_pack(ctx->shards[p].d_state, sendb, ctx->prec, wl, pl, 0, true, ctx->stream));
+    }
+    return OWQS_OK;
+  }
+  const int b = (ctx->rank >> gbit) & 1, partner = ctx->rank ^ (1 << gbit);
+  CU(launch_swap_pack(ctx->shards[0].d_state, sendb, ctx->prec, wl, pl, 1 - b, false, ctx->stream));
+  NC(ncclGroupStart());
+  NC(ncclSend(sendb, half, ncclChar, partner, ctx->comm, ctx->stream));
+  NC(ncclRecv(recvb, half, ncclChar, partner, ctx->comm, ctx->stream));
+  NC(ncclGroupEnd());
+  CU(launch_swap_pack(ctx->shards[0].d_state, recvb, ctx->prec, wl, pl, 1 - b, true, ctx->stream));
+  return OWQS_OK;
+}
+
 owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const uint8_t* forced) {
   CompiledMode& m = ctx->cm[cmi];
   RunParams rp{};
@@ -193,17 +268,13 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
   CU(cudaMemcpyAsync(ctx->d_run, &rp, sizeof(rp), cudaMemcpyHostToDevice, ctx->stream));
   if (mode == OWQS_FORCED && ctx->hp.n_measure > 0)
     CU(cudaMemcpyAsync(ctx->d_forced, forced, ctx->hp.n_measure, cudaMemcpyHostToDevice, ctx->stream));
-  CU(cudaMemsetAsync(ctx->d_err, 0, sizeof(int32_t), ctx->stream));
-  DevPtrs p = dev_ptrs(ctx, m);
+  for (auto& s : ctx->shards) CU(cudaMemsetAsync(s.d_err, 0, sizeof(int32_t), ctx->stream));
   const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH);
   const bool prof = (ctx->cfg.flags & OWQS_FLAG_PROFILE) != 0;
   if (prof) {
-    if (ctx->prof_cm != cmi) {
-      // event lists are per compiled mode: rebuild (and drop this mode's graph) on a mode switch
-      if (m.gexec) {
-        cudaGraphExecDestroy(m.gexec);
-        m.gexec = nullptr;
-      }
+    if (ctx->prof_cm != cmi && m.gexec) {  // event lists follow the compiled mode
+      cudaGraphExecDestroy(m.gexec);
+      m.gexec = nullptr;
     }
     while (ctx->prof_ev.size() < m.prog.steps.size() + 1) {
       cudaEvent_t e;
@@ -212,26 +283,37 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
     }
     ctx->prof_cm = cmi;
   }
-  auto launch_all = [&](bool capturing) -> cudaError_t {
-    cudaError_t e = cudaSuccess;
-    if (prof) e = capturing ? cudaEventRecordWithFlags(ctx->prof_ev[0], ctx->stream, cudaEventRecordExternal)
-                            : cudaEventRecord(ctx->prof_ev[0], ctx->stream);
-    for (size_t i = 0; i < m.prog.steps.size() && e == cudaSuccess; ++i) {
-      e = launch_step(m.prog.steps[i], p, ctx->prec, ctx->stream);
-      if (e == cudaSuccess && prof)
-        e = capturing ? cudaEventRecordWithFlags(ctx->prof_ev[i + 1], ctx->stream, cudaEventRecordExternal)
-                      : cudaEventRecord(ctx->prof_ev[i + 1], ctx->stream);
+  auto record = [&](int i, bool capturing) -> cudaError_t {
+    return capturing ? cudaEventRecordWithFlags(ctx->prof_ev[i], ctx->stream, cudaEventRecordExternal)
+                     : cudaEventRecord(ctx->prof_ev[i], ctx->stream);
+  };
+  auto launch_all = [&](bool capturing) -> owqs_status {
+    if (prof) CU(record(0, capturing));
+    for (size_t i = 0; i < m.prog.steps.size(); ++i) {
+      const StepDesc& s = m.prog.steps[i];
+      if (s.kind == ST_SWAP) {
+        owqs_status st = do_swap(ctx, s);
+        if (st != OWQS_OK) return st;
+      } else {
+        for (size_t r = 0; r < ctx->shards.size(); ++r)
+          CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
+        if (s.red_kind != RED_NONE) {
+          owqs_status st = allreduce_red(ctx);
+          if (st != OWQS_OK) return st;
+        }
+      }
+      if (prof) CU(record((int)i + 1, capturing));
     }
-    return e;
+    return OWQS_OK;
   };
   if (use_graph && !m.gexec) {
     cudaGraph_t g = nullptr;
     CU(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-    cudaError_t e = launch_all(true);
-    if (e != cudaSuccess) {
+    owqs_status st = launch_all(true);
+    if (st != OWQS_OK) {
       cudaStreamEndCapture(ctx->stream, &g);
       if (g) cudaGraphDestroy(g);
-      return fail(ctx, OWQS_E_CUDA, std::string("launch during capture: ") + cudaGetErrorString(e));
+      return st;
     }
     CU(cudaStreamEndCapture(ctx->stream, &g));
     CU(cudaGraphInstantiate(&m.gexec, g, 0));
@@ -241,7 +323,8 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
   if (use_graph) {
     CU(cudaGraphLaunch(m.gexec, ctx->stream));
   } else {
-    CU(launch_all(false));
+    owqs_status st = launch_all(false);
+    if (st != OWQS_OK) return st;
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
@@ -250,18 +333,15 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
   ctx->stats.last_run_ms = ms;
   ctx->last_cm = cmi;
   int32_t herr = 0;
-  CU(cudaMemcpy(&herr, ctx->d_err, sizeof(herr), cudaMemcpyDeviceToHost));
+  for (auto& s : ctx->shards) {
+    int32_t e = 0;
+    CU(cudaMemcpy(&e, s.d_err, sizeof(e), cudaMemcpyDeviceToHost));
+    herr |= e;
+  }
   ctx->has_input = false;
   ctx->has_output = true;
   ctx->out_cm = cmi;
   if (herr) return fail(ctx, OWQS_E_BRANCH, "forced outcome on a branch with probability < 1e-12");
-  return OWQS_OK;
-}
-
-owqs_status output_to_device(owqs_ctx* ctx, void* dst, int dst_prec, uint64_t j0, uint64_t count) {
-  const Program& pr = ctx->cm[ctx->out_cm].prog;
-  CU(launch_permute_out(ctx->d_state, ctx->prec, dst, dst_prec, (int)pr.out_slot.size(), pr.out_slot.data(), j0,
-                        count, ctx->stream));
   return OWQS_OK;
 }
 
@@ -274,14 +354,60 @@ bool is_pinned_host(const void* p) {
   return a.type == cudaMemoryTypeHost;
 }
 
+// output (complex128 when dst_prec = 1) in the caller's order into a device buffer of 2^n_out
+owqs_status output_to_device_full(owqs_ctx* ctx, void* dst, int dst_prec) {
+  const Program& pr = ctx->cm[ctx->out_cm].prog;
+  const int nb = (int)pr.out_slot.size();
+  const int wl = pr.phys_bits - ctx->n_global;
+  if (ctx->n_ranks == 1) {
+    CU(launch_permute_out(ctx->shards[0].d_state, ctx->prec, dst, dst_prec, nb, pr.out_slot.data(), 0, 1ull << nb,
+                          ctx->stream));
+    return OWQS_OK;
+  }
+  if (ctx->loopback) {
+    for (int r = 0; r < ctx->n_ranks; ++r)
+      CU(launch_scatter_out(ctx->shards[r].d_state, ctx->prec, dst, dst_prec, nb, pr.out_slot.data(), r, wl,
+                            ctx->stream));
+    return OWQS_OK;
+  }
+  // NCCL: shards travel to rank 0 (through the swap buffer), which scatters them into dst
+  if (ctx->rank == 0) {
+    CU(launch_scatter_out(ctx->shards[0].d_state, ctx->prec, dst, dst_prec, nb, pr.out_slot.data(), 0, wl,
+                          ctx->stream));
+    for (int r = 1; r < ctx->n_ranks; ++r) {
+      NC(ncclRecv(ctx->d_swap, (size_t)ctx->elem << wl, ncclChar, r, ctx->comm, ctx->stream));
+      CU(launch_scatter_out(ctx->d_swap, ctx->prec, dst, dst_prec, nb, pr.out_slot.data(), r, wl, ctx->stream));
+    }
+  } else {
+    NC(ncclSend(ctx->shards[0].d_state, (size_t)ctx->elem << wl, ncclChar, 0, ctx->comm, ctx->stream));
+  }
+  return OWQS_OK;
+}
+
 owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
   const uint64_t n = 1ull << ctx->hp.outputs.size();
+  if (ctx->n_ranks > 1) {
+    void* d = nullptr;
+    if (ctx->rank == 0 || ctx->loopback) CU(cudaMalloc(&d, n * 16));
+    owqs_status s = output_to_device_full(ctx, d, 1);
+    if (s == OWQS_OK && d) {
+      cudaError_t e = cudaMemcpyAsync(amps, d, n * 16, cudaMemcpyDeviceToHost, ctx->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) s = fail(ctx, OWQS_E_CUDA, cudaGetErrorString(e));
+    } else if (s == OWQS_OK) {
+      cudaError_t e = cudaStreamSynchronize(ctx->stream);
+      if (e != cudaSuccess) s = fail(ctx, OWQS_E_CUDA, cudaGetErrorString(e));
+    }
+    cudaFree(d);
+    return s;
+  }
+  const Program& pr = ctx->cm[ctx->out_cm].prog;
   const uint64_t chunk = kStagingBytes / 16;
   const bool pinned = is_pinned_host(amps);  // page-locked caller buffer: DMA straight into it
   for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
     uint64_t cnt = std::min(chunk, n - j0);
-    owqs_status s = output_to_device(ctx, ctx->d_staging, 1, j0, cnt);
-    if (s != OWQS_OK) return s;
+    CU(launch_permute_out(ctx->shards[0].d_state, ctx->prec, ctx->d_staging, 1, (int)pr.out_slot.size(),
+                          pr.out_slot.data(), j0, cnt, ctx->stream));
     CU(cudaMemcpyAsync(pinned ? (void*)(amps + 2 * j0) : ctx->h_staging, ctx->d_staging, cnt * 16,
                        cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
@@ -290,22 +416,50 @@ owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
   return OWQS_OK;
 }
 
+owqs_status norm_all(owqs_ctx* ctx, double* out) {
+  const Program& pr = ctx->cm[ctx->out_cm >= 0 ? ctx->out_cm : 0].prog;
+  const int nb = ctx->n_ranks > 1 ? pr.phys_bits - ctx->n_global : (int)ctx->hp.outputs.size();
+  for (size_t r = 0; r < ctx->shards.size(); ++r)
+    CU(launch_norm(dev_ptrs(ctx, ctx->cm[0], (int)r), ctx->prec, 1ull << nb, ctx->stream));
+  owqs_status s = allreduce_red(ctx);
+  if (s != OWQS_OK) return s;
+  double red[4];
+  CU(cudaMemcpyAsync(red, ctx->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(cudaStreamSynchronize(ctx->stream));
+  *out = red[0];
+  return OWQS_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
-const char* owqs_version(void) { return "owqs-b200 0.1 (sm_100a)"; }
+const char* owqs_version(void) { return "owqs-b200 0.2 (sm_100a)"; }
 
 const char* owqs_last_error(const owqs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+
+owqs_status owqs_nccl_unique_id(void* out) {
+  if (!out) return OWQS_E_ARG;
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return OWQS_E_NCCL;
+  memcpy(out, &id, sizeof(id));
+  return OWQS_OK;
+}
 
 owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
   if (!cfg || !out) return OWQS_E_ARG;
   *out = nullptr;
   if (cfg->precision != 64 && cfg->precision != 128) return OWQS_E_ARG;
-  if (cfg->n_ranks != 1 && cfg->n_ranks != 0) return OWQS_E_ARG;  // multi-rank: DESIGN.md §7
+  const int nr = cfg->n_ranks <= 0 ? 1 : cfg->n_ranks;
+  if (nr & (nr - 1)) return OWQS_E_ARG;
+  const bool loopback = nr > 1 && (cfg->flags & OWQS_FLAG_LOOPBACK);
+  if (nr > 1 && !loopback && (!cfg->nccl_id || cfg->rank < 0 || cfg->rank >= nr)) return OWQS_E_ARG;
   owqs_ctx* ctx = new owqs_ctx();
   ctx->cfg = *cfg;
-  ctx->cfg.n_ranks = 1;
+  ctx->n_ranks = nr;
+  ctx->rank = loopback ? 0 : (nr > 1 ? cfg->rank : 0);
+  ctx->loopback = loopback;
+  while ((1 << ctx->n_global) < nr) ++ctx->n_global;
   ctx->prec = cfg->precision == 64 ? 0 : 1;
   ctx->elem = cfg->precision == 64 ? 8 : 16;
   auto bail = [&](owqs_status s) {
@@ -321,15 +475,26 @@ owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
     ctx->own_stream = true;
   }
   if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return bail(OWQS_E_CUDA);
+  const int n_sh = loopback ? nr : 1;
+  ctx->shards.resize(n_sh);
+  if (cudaMalloc(&ctx->d_red_all, (size_t)n_sh * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM);
   const int nb = max_partial_blocks();
-  if (cudaMalloc(&ctx->d_partials, (size_t)nb * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM);
-  if (cudaMalloc(&ctx->d_counter, sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_NOMEM);
-  if (cudaMemset(ctx->d_counter, 0, sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_CUDA);
-  if (cudaMalloc(&ctx->d_red, 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM);
-  if (cudaMalloc(&ctx->d_err, sizeof(int32_t)) != cudaSuccess) return bail(OWQS_E_NOMEM);
+  for (int i = 0; i < n_sh; ++i) {
+    Shard& s = ctx->shards[i];
+    s.d_red = ctx->d_red_all + 4 * i;
+    if (cudaMalloc(&s.d_partials, (size_t)nb * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM);
+    if (cudaMalloc(&s.d_counter, sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_NOMEM);
+    if (cudaMemset(s.d_counter, 0, sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_CUDA);
+    if (cudaMalloc(&s.d_err, sizeof(int32_t)) != cudaSuccess) return bail(OWQS_E_NOMEM);
+  }
   if (cudaMalloc(&ctx->d_run, sizeof(RunParams)) != cudaSuccess) return bail(OWQS_E_NOMEM);
   if (cudaMalloc(&ctx->d_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM);
   if (cudaMallocHost(&ctx->h_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM);
+  if (nr > 1 && !loopback) {
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_id, sizeof(id));
+    if (ncclCommInitRank(&ctx->comm, nr, id, cfg->rank) != ncclSuccess) return bail(OWQS_E_NCCL);
+  }
   *out = ctx;
   return OWQS_OK;
 }
@@ -339,11 +504,14 @@ void owqs_destroy(owqs_ctx* ctx) {
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (int i = 0; i < 2; ++i) free_mode(ctx->cm[i]);
-  cudaFree(ctx->d_state);
-  cudaFree(ctx->d_partials);
-  cudaFree(ctx->d_counter);
-  cudaFree(ctx->d_red);
-  cudaFree(ctx->d_err);
+  for (auto& s : ctx->shards) {
+    cudaFree(s.d_state);
+    cudaFree(s.d_partials);
+    cudaFree(s.d_counter);
+    cudaFree(s.d_err);
+  }
+  cudaFree(ctx->d_red_all);
+  cudaFree(ctx->d_swap);
   cudaFree(ctx->d_run);
   cudaFree(ctx->d_outcome);
   cudaFree(ctx->d_prob0);
@@ -353,6 +521,7 @@ void owqs_destroy(owqs_ctx* ctx) {
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
@@ -378,10 +547,11 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
   ctx->stats.n_grow = pr.n_grow;
   ctx->stats.n_shrink = pr.n_shrink;
   ctx->stats.n_reduce = pr.n_reduce;
+  ctx->stats.n_swaps = pr.n_swaps;
   ctx->stats.n_launches = (int32_t)pr.steps.size();
   ctx->stats.bytes_per_run = pr.bytes_per_run(ctx->elem);
   ctx->stats.schedule_ms = ctx->cm[0].schedule_ms;
-  if (pr.phys_bits > 40) return fail(ctx, OWQS_E_NOMEM, "physical width above 40 bits");
+  if (pr.phys_bits - ctx->n_global > 40) return fail(ctx, OWQS_E_NOMEM, "shard width above 40 bits");
   ctx->loaded = true;
   return OWQS_OK;
 }
@@ -393,14 +563,20 @@ owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps) {
   if (!amps || n_amps != (int64_t)n) return fail(ctx, OWQS_E_ARG, "input must hold 2^n_in amplitudes");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
+  const uint64_t per = n >> ctx->n_global;  // amplitudes per shard
   const uint64_t chunk = kStagingBytes / 16;
-  for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
-    uint64_t cnt = std::min(chunk, n - j0);
-    if (ctx->prec == 1) {
-      CU(cudaMemcpyAsync((char*)ctx->d_state + j0 * 16, amps + 2 * j0, cnt * 16, cudaMemcpyHostToDevice, ctx->stream));
-    } else {
-      CU(cudaMemcpyAsync(ctx->d_staging, amps + 2 * j0, cnt * 16, cudaMemcpyHostToDevice, ctx->stream));
-      CU(launch_convert_in(ctx->d_staging, 1, ctx->d_state, 0, j0, cnt, ctx->stream));
+  for (size_t r = 0; r < ctx->shards.size(); ++r) {
+    const uint64_t base = (uint64_t)ctx->shard_rank((int)r) * per;
+    for (uint64_t j0 = 0; j0 < per; j0 += chunk) {
+      uint64_t cnt = std::min(chunk, per - j0);
+      const double* src = amps + 2 * (base + j0);
+      if (ctx->prec == 1) {
+        CU(cudaMemcpyAsync((char*)ctx->shards[r].d_state + j0 * 16, src, cnt * 16, cudaMemcpyHostToDevice,
+                           ctx->stream));
+      } else {
+        CU(cudaMemcpyAsync(ctx->d_staging, src, cnt * 16, cudaMemcpyHostToDevice, ctx->stream));
+        CU(launch_convert_in(ctx->d_staging, 1, ctx->shards[r].d_state, 0, j0, cnt, ctx->stream));
+      }
     }
   }
   CU(cudaStreamSynchronize(ctx->stream));
@@ -413,15 +589,21 @@ owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t p
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   const uint64_t n = 1ull << ctx->hp.inputs.size();
-  if (!dev_amps || n_amps != (int64_t)n || (precision != 64 && precision != 128))
-    return fail(ctx, OWQS_E_ARG, "input must hold 2^n_in amplitudes of precision 64 or 128");
+  const uint64_t per = n >> ctx->n_global;
+  const uint64_t expect = (ctx->n_ranks > 1 && !ctx->loopback) ? per : n;
+  if (!dev_amps || n_amps != (int64_t)expect || (precision != 64 && precision != 128))
+    return fail(ctx, OWQS_E_ARG, "input must hold the (shard's) amplitudes at precision 64 or 128");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
   const int sp = precision == 64 ? 0 : 1;
-  if (sp == ctx->prec) {
-    CU(cudaMemcpyAsync(ctx->d_state, dev_amps, n * ctx->elem, cudaMemcpyDeviceToDevice, ctx->stream));
-  } else {
-    CU(launch_convert_in(dev_amps, sp, ctx->d_state, ctx->prec, 0, n, ctx->stream));
+  const size_t se = precision == 64 ? 8 : 16;
+  for (size_t r = 0; r < ctx->shards.size(); ++r) {
+    const char* src = (const char*)dev_amps + (ctx->loopback ? r * per * se : 0);
+    if (sp == ctx->prec) {
+      CU(cudaMemcpyAsync(ctx->shards[r].d_state, src, per * ctx->elem, cudaMemcpyDeviceToDevice, ctx->stream));
+    } else {
+      CU(launch_convert_in(src, sp, ctx->shards[r].d_state, ctx->prec, 0, per, ctx->stream));
+    }
   }
   ctx->has_input = true;
   ctx->has_output = false;
@@ -433,8 +615,14 @@ owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed) {
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
-  DevPtrs p = dev_ptrs(ctx, ctx->cm[0]);
-  CU(launch_haar(p, ctx->prec, 1ull << ctx->hp.inputs.size(), seed, ctx->stream));
+  const uint64_t per = (1ull << ctx->hp.inputs.size()) >> ctx->n_global;
+  for (size_t r = 0; r < ctx->shards.size(); ++r)
+    CU(launch_haar(dev_ptrs(ctx, ctx->cm[0], (int)r), ctx->prec, per, seed, (uint64_t)ctx->shard_rank((int)r) * per,
+                   ctx->stream));
+  s = allreduce_red(ctx);
+  if (s != OWQS_OK) return s;
+  for (size_t r = 0; r < ctx->shards.size(); ++r)
+    CU(launch_scale(dev_ptrs(ctx, ctx->cm[0], (int)r), ctx->prec, per, ctx->stream));
   CU(cudaStreamSynchronize(ctx->stream));
   ctx->has_input = true;
   ctx->has_output = false;
@@ -471,13 +659,14 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   ctx->stats.n_grow = pr.n_grow;
   ctx->stats.n_shrink = pr.n_shrink;
   ctx->stats.n_reduce = pr.n_reduce;
+  ctx->stats.n_swaps = pr.n_swaps;
   ctx->stats.n_launches = (int32_t)pr.steps.size();
   ctx->stats.bytes_per_run = pr.bytes_per_run(ctx->elem);
   ctx->stats.schedule_ms = ctx->cm[cmi].schedule_ms;
   ctx->stats.phys_bits = pr.phys_bits;
   if (mode == OWQS_EOWQS) {
     double red[4];
-    CU(cudaMemcpy(red, ctx->d_red, sizeof(red), cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(red, ctx->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost));
     const double tol = ctx->prec == 1 ? 1e-8 : 1e-3;
     if (!(std::fabs(red[0] - 1.0) <= tol))
       return fail(ctx, OWQS_E_NOT_DETERMINISTIC,
@@ -490,7 +679,8 @@ owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
   const uint64_t n = 1ull << ctx->hp.outputs.size();
-  if (!amps || n_amps < (int64_t)n) return fail(ctx, OWQS_E_ARG, "output buffer smaller than 2^n_out");
+  const bool root = ctx->n_ranks == 1 || ctx->loopback || ctx->rank == 0;
+  if (root && (!amps || n_amps < (int64_t)n)) return fail(ctx, OWQS_E_ARG, "output buffer smaller than 2^n_out");
   return output_to_host(ctx, amps);
 }
 
@@ -498,12 +688,19 @@ owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precis
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
   const uint64_t n = 1ull << ctx->hp.outputs.size();
-  if (!dev_amps || n_amps < (int64_t)n || (precision != 64 && precision != 128))
+  const bool root = ctx->n_ranks == 1 || ctx->loopback || ctx->rank == 0;
+  if ((root && (!dev_amps || n_amps < (int64_t)n)) || (precision != 64 && precision != 128))
     return fail(ctx, OWQS_E_ARG, "bad output buffer");
-  owqs_status s = output_to_device(ctx, dev_amps, precision == 64 ? 0 : 1, 0, n);
+  owqs_status s = output_to_device_full(ctx, dev_amps, precision == 64 ? 0 : 1);
   if (s != OWQS_OK) return s;
   CU(cudaStreamSynchronize(ctx->stream));
   return OWQS_OK;
+}
+
+owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2) {
+  if (!ctx || !norm2) return OWQS_E_ARG;
+  if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
+  return norm_all(ctx, norm2);
 }
 
 owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) {
@@ -511,6 +708,25 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) 
   if (!a || !b || !re || !im) return OWQS_E_ARG;
   if (!a->has_output || !b->has_output) return fail(a, OWQS_E_STATE, "no output: run first");
   if (a->hp.outputs.size() != b->hp.outputs.size()) return fail(a, OWQS_E_ARG, "output widths differ");
+  if (a->n_ranks > 1 || b->n_ranks > 1) {
+    const Program& pa = a->cm[a->out_cm].prog;
+    const Program& pb = b->cm[b->out_cm].prog;
+    if (a->n_ranks != b->n_ranks || a->loopback != b->loopback || a->prec != b->prec || pa.out_slot != pb.out_slot ||
+        pa.phys_bits != pb.phys_bits)
+      return fail(a, OWQS_E_ARG, "multi-rank inner product needs equal sharding, precision and final layout");
+    const uint64_t per = 1ull << (pa.phys_bits - a->n_global);
+    for (size_t r = 0; r < a->shards.size(); ++r)
+      CU(launch_dot_t(dev_ptrs(a, a->cm[0], (int)r), a->prec, a->shards[r].d_state, b->shards[r].d_state, per,
+                      a->stream));
+    owqs_status s = allreduce_red(a);
+    if (s != OWQS_OK) return s;
+    double red[4];
+    CU(cudaMemcpyAsync(red, a->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost, a->stream));
+    CU(cudaStreamSynchronize(a->stream));
+    *re = red[0];
+    *im = red[1];
+    return OWQS_OK;
+  }
   const uint64_t n = 1ull << a->hp.outputs.size();
   void *ta = nullptr, *tb = nullptr;
   CU(cudaMalloc(&ta, n * 16));
@@ -519,14 +735,14 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) 
     cudaFree(ta);
     return fail(a, OWQS_E_NOMEM, "inner product scratch");
   }
-  owqs_status s = output_to_device(a, ta, 1, 0, n);
+  owqs_status s = output_to_device_full(a, ta, 1);
   if (s == OWQS_OK) {
     const Program& pb = b->cm[b->out_cm].prog;
-    cudaError_t e = launch_permute_out(b->d_state, b->prec, tb, 1, (int)pb.out_slot.size(), pb.out_slot.data(), 0, n,
-                                       a->stream);
-    if (e == cudaSuccess) e = launch_dot(dev_ptrs(a, a->cm[0]), ta, tb, n, a->stream);
+    cudaError_t e = launch_permute_out(b->shards[0].d_state, b->prec, tb, 1, (int)pb.out_slot.size(),
+                                       pb.out_slot.data(), 0, n, a->stream);
+    if (e == cudaSuccess) e = launch_dot(dev_ptrs(a, a->cm[0], 0), ta, tb, n, a->stream);
     double red[4] = {0, 0, 0, 0};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(red, a->d_red, sizeof(red), cudaMemcpyDeviceToHost, a->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(red, a->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost, a->stream);
     if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
     if (e != cudaSuccess) s = fail(a, OWQS_E_CUDA, cudaGetErrorString(e));
     *re = red[0];
@@ -540,6 +756,7 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) 
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "recognize before load_pattern");
+  if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "recognize runs on a single rank");
   const int ni = (int)ctx->hp.inputs.size(), no = (int)ctx->hp.outputs.size();
   if (ni > 14 || no > 14) return fail(ctx, OWQS_E_ARG, "recognize is limited to 14 input/output qubits");
   const uint64_t rows = 1ull << no, cols = 1ull << ni;
@@ -547,7 +764,7 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
   for (uint64_t k = 0; k < cols; ++k) {
-    CU(launch_basis(ctx->d_state, ctx->prec, cols, k, ctx->stream));
+    CU(launch_basis(ctx->shards[0].d_state, ctx->prec, cols, k, ctx->stream));
     ctx->has_input = true;
     s = run_internal(ctx, 1, OWQS_EOWQS, 0, nullptr);
     if (s != OWQS_OK) return s;
@@ -620,10 +837,14 @@ owqs_status owqs_launch_profile(owqs_ctx* ctx, int32_t* kclass, double* bytes, f
   if (n < (int64_t)pr.steps.size()) return fail(ctx, OWQS_E_ARG, "arrays smaller than the launch count");
   for (size_t i = 0; i < pr.steps.size(); ++i) {
     const StepDesc& s = pr.steps[i];
-    const double S = std::ldexp((double)ctx->elem, s.width);
+    const double S = std::ldexp((double)ctx->elem, s.width) * (double)ctx->shards.size();
     int kc = step_kclass(s, ctx->prec);
     if (kclass) kclass[i] = kc;
-    if (bytes) bytes[i] = s.kind == ST_GROW ? 3 * S : s.kind == ST_SHRINK ? 1.5 * S : (s.n_ops > 0 ? 2 * S : S);
+    if (bytes)
+      bytes[i] = s.kind == ST_GROW     ? 3 * S
+                 : s.kind == ST_SHRINK ? 1.5 * S
+                 : s.kind == ST_SWAP   ? 2 * S
+                                       : (s.n_ops > 0 ? 2 * S : S);
     if (ms) {
       float t = 0;
       CU(cudaEventElapsedTime(&t, ctx->prof_ev[i], ctx->prof_ev[i + 1]));

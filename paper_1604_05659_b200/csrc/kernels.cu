@@ -305,9 +305,11 @@ __device__ __forceinline__ uint32_t slot_mask(int x, int lane, const uint64_t (&
 }
 
 template <typename T, int KHI, int UNR>
-__device__ __forceinline__ uint32_t slot_mask_p(int x, int lane, const uint64_t (&gb)[UNR], const StepDesc& d) {
+__device__ __forceinline__ uint32_t slot_mask_p(int x, int lane, const uint64_t (&gb)[UNR], const StepDesc& d,
+                                                uint32_t rank) {
   constexpr int SB = VT<T>::SB, EPV = VT<T>::EPV, G = 1 << KHI, NV = UNR * G;
   typedef PosMasks<NV, EPV, G> PM;
+  if (x >= d.width) return ((rank >> (x - d.width)) & 1) ? PM::full() : 0u;  // rank bit (sharded)
   if (EPV == 2 && x == 0) return PM::elem1();
   if (x < SB) return ((lane >> (x - (EPV == 2 ? 1 : 0))) & 1) ? PM::full() : 0u;
   uint32_t m = 0;
@@ -518,8 +520,8 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
       const int type = d.ops[i].type;
       const int a = d.ops[i].a;
       if (type == OP_DIAG_E || type == OP_DIAG_Z) {
-        uint32_t m = slot_mask_p<T, KHI, UNR>(a, lane, gb, d);
-        if (type == OP_DIAG_E) m &= slot_mask_p<T, KHI, UNR>(d.ops[i].b, lane, gb, d);
+        uint32_t m = slot_mask_p<T, KHI, UNR>(a, lane, gb, d, p.rank);
+        if (type == OP_DIAG_E) m &= slot_mask_p<T, KHI, UNR>(d.ops[i].b, lane, gb, d, p.rank);
         neg ^= sh.cond[i] ? m : 0u;
         continue;
       }
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
       if (am & ~LANE_SLOTS) {
         // absorbed CZ signs depend on group / element / base bits: a sign bit per pair
         uint32_t M = 0;
-        for (uint64_t r = am; r; r &= r - 1) M ^= slot_mask_p<T, KHI, UNR>(__ffsll((long long)r) - 1, lane, gb, d);
+        for (uint64_t r = am; r; r &= r - 1) M ^= slot_mask_p<T, KHI, UNR>(__ffsll((long long)r) - 1, lane, gb, d, p.rank);
         const T nai = -ai;
         if (a >= SB) {
 #pragma unroll
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
       }
     } else if (d.red_kind == RED_RHO) {
       const int r = d.red_slot;
-      const uint32_t mr1 = slot_mask_p<T, KHI, UNR>(r, lane, gb, d);
+      const uint32_t mr1 = slot_mask_p<T, KHI, UNR>(r, lane, gb, d, p.rank);
 #pragma unroll
       for (int v = 0; v < NV; ++v)
 #pragma unroll
@@ -768,8 +770,9 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
     if (!sh.cond[k] || op.type == OP_FLUSH) continue;
     if (op.type == OP_DIAG_E || op.type == OP_DIAG_Z) {
       const int a = op.a, b = op.type == OP_DIAG_E ? op.b : op.a;
+      const uint64_t rk = (uint64_t)p.rank << d.width;  // rank bits above the shard (sharded runs)
       for (int i = threadIdx.x; i < n; i += blockDim.x)
-        if ((i >> a) & (i >> b) & 1) {
+        if ((((uint64_t)i | rk) >> a) & (((uint64_t)i | rk) >> b) & 1) {
           s[i].x = -s[i].x;
           s[i].y = -s[i].y;
         }
@@ -782,12 +785,13 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
         double x[8] = {0, 0, 1, 0, 1, 0, 0, 0};
         for (int j = 0; j < 8; ++j) cf[j] = x[j];
       }
-      const uint32_t am = op.type == OP_BFLY ? (uint32_t)d.absorb[sh.bidx[k]] : 0u;  // w <= 12
+      const uint64_t am = op.type == OP_BFLY ? d.absorb[sh.bidx[k]] : 0ull;
+      const uint64_t rk = (uint64_t)p.rank << d.width;
       for (int i = threadIdx.x; i < n / 2; i += blockDim.x) {
         int i0 = ((i >> a) << (a + 1)) | (i & ((1 << a) - 1));
         int i1 = i0 | (1 << a);
         T x0r = s[i0].x, x0i = s[i0].y, x1r = s[i1].x, x1i = s[i1].y;
-        if (__popc((uint32_t)i1 & am) & 1) {  // absorbed CZ: x1 sign by the other slots' bits
+        if (__popcll(((uint64_t)i1 | rk) & am) & 1) {  // absorbed CZ: x1 sign by the other slots' bits
           x1r = -x1r;
           x1i = -x1i;
         }
@@ -900,6 +904,23 @@ struct PermTab {
   int8_t slot[64];
 };
 
+// shard scatter: out[perm(G)] = shard[L] with G = (rank << wl) | L (output bit k <- position slot[k])
+template <typename T, typename TO>
+__global__ void scatter_out_kernel(const void* shard, void* out, int nbits, PermTab tab, uint64_t rank, int wl) {
+  typedef typename VT<T>::C C;
+  typedef typename VT<TO>::C CO;
+  const C* st = reinterpret_cast<const C*>(shard);
+  CO* o = reinterpret_cast<CO*>(out);
+  const uint64_t n = 1ull << wl;
+  for (uint64_t L = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; L < n; L += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t G = (rank << wl) | L;
+    uint64_t j = 0;
+    for (int k = 0; k < nbits; ++k) j |= ((G >> tab.slot[k]) & 1ull) << k;
+    C v = st[L];
+    o[j] = make_c<TO>((TO)v.x, (TO)v.y);
+  }
+}
+
 // out[j] = state[src(j)], bit k of j <-> slot tab.slot[k]  (output order outputs[0] = LSB)
 template <typename T, typename TO>
 __global__ void permute_out_kernel(const void* state, void* out, int nbits, PermTab tab, uint64_t j0, uint64_t count) {
@@ -938,15 +959,15 @@ __global__ void basis_kernel(void* state, uint64_t n, uint64_t k) {
 // Counter-based Haar input (workloads/inputs.py documents the same generator), unnormalised,
 // with the norm reduced into red_result[0].
 template <typename T>
-__global__ void __launch_bounds__(256) haar_kernel(DevPtrs p, uint64_t n, uint64_t seed) {
+__global__ void __launch_bounds__(256) haar_kernel(DevPtrs p, uint64_t n, uint64_t seed, uint64_t j0) {
   typedef typename VT<T>::C C;
   __shared__ PassShared sh;
   C* st = reinterpret_cast<C*>(p.state);
   const uint64_t key = splitmix64(seed);
   double acc[4] = {0, 0, 0, 0};
   for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t a = splitmix64(key ^ splitmix64(2 * j));
-    uint64_t b = splitmix64(key ^ splitmix64(2 * j + 1));
+    uint64_t a = splitmix64(key ^ splitmix64(2 * (j + j0)));
+    uint64_t b = splitmix64(key ^ splitmix64(2 * (j + j0) + 1));
     double u1 = ((double)(a >> 11) + 1.0) * 0x1.0p-53;
     double u2 = (double)(b >> 11) * 0x1.0p-53;
     double r = sqrt(-2.0 * log(u1));
@@ -1033,11 +1054,51 @@ int max_partial_blocks() { return 16 * 148 * 2; }
 static inline int unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
 static inline int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; }
 
+// ---- multi-rank: SWAP halves and reduction all-reduce ------------------------------------------
+// half of a shard whose bit `pl` equals `bit`, packed in index order (runs of 2^pl contiguous)
+template <typename T>
+__global__ void swap_pack_kernel(const void* state, void* buf, int local_width, int pl, int bit, int unpack) {
+  typedef typename VT<T>::C C;
+  const C* st = reinterpret_cast<const C*>(state);
+  C* sm = reinterpret_cast<C*>(const_cast<void*>(state));
+  C* b = reinterpret_cast<C*>(buf);
+  const uint64_t n = 1ull << (local_width - 1);
+  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t L = ((j >> pl) << (pl + 1)) | ((uint64_t)bit << pl) | (j & ((1ull << pl) - 1));
+    if (unpack) sm[L] = b[j];
+    else b[j] = st[L];
+  }
+}
+
+// loopback all-reduce: red[r*4 + k] <- sum_r red[r*4 + k] (fixed order: deterministic)
+__global__ void loopback_allreduce_kernel(double* red, int n_ranks) {
+  if (threadIdx.x < 4) {
+    double s = 0;
+    for (int r = 0; r < n_ranks; ++r) s += red[r * 4 + threadIdx.x];
+    for (int r = 0; r < n_ranks; ++r) red[r * 4 + threadIdx.x] = s;
+  }
+}
+
+cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_width, int pl, int bit, bool unpack,
+                             cudaStream_t s) {
+  const uint64_t n = 1ull << (local_width - 1);
+  unsigned b = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)(g_lim_ready ? g_lim.max_blocks_elem : 1184)));
+  if (prec == 0) swap_pack_kernel<float><<<b, 256, 0, s>>>(state, buf, local_width, pl, bit, unpack ? 1 : 0);
+  else swap_pack_kernel<double><<<b, 256, 0, s>>>(state, buf, local_width, pl, bit, unpack ? 1 : 0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s) {
+  loopback_allreduce_kernel<<<1, 32, 0, s>>>(red, n_ranks);
+  return cudaGetLastError();
+}
+
 // Kernel class of a step (OWQS_KCLASS_* of include/owqs.h).
 int step_kclass(const StepDesc& d, int prec) {
   const int SB = prec == 0 ? 6 : 5;
   if (d.kind == ST_GROW) return 2;
   if (d.kind == ST_SHRINK) return 3;
+  if (d.kind == ST_SWAP) return 5;
   const int slack = d.width - SB - d.nb_hi - log2i(unr_of(d.nb_hi)) - 3;
   if (slack < 0) return 1;
   return d.n_ops == 0 ? 4 : 0;
@@ -1098,6 +1159,18 @@ static inline unsigned elem_blocks(uint64_t n) {
   return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)(g_lim_ready ? g_lim.max_blocks_elem : 1184)));
 }
 
+cudaError_t launch_scatter_out(const void* shard, int prec, void* out, int out_prec, int nbits, const int* slots,
+                               uint64_t rank, int wl, cudaStream_t s) {
+  PermTab t;
+  for (int k = 0; k < 64; ++k) t.slot[k] = (int8_t)(k < nbits ? slots[k] : 0);
+  unsigned b = elem_blocks(1ull << wl);
+  if (prec == 0 && out_prec == 1) scatter_out_kernel<float, double><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
+  else if (prec == 0) scatter_out_kernel<float, float><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
+  else if (out_prec == 1) scatter_out_kernel<double, double><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
+  else scatter_out_kernel<double, float><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_permute_out(const void* state, int prec, void* out, int out_prec, int nbits, const int* slots,
                                uint64_t j0, uint64_t count, cudaStream_t s) {
   PermTab t;
@@ -1126,15 +1199,60 @@ cudaError_t launch_basis(void* state, int prec, uint64_t n, uint64_t k, cudaStre
   return cudaGetLastError();
 }
 
-cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, cudaStream_t s) {
+// Haar input (unnormalised, norm^2 into red_result) for amplitudes [j0, j0 + n) of the global state
+cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, uint64_t j0, cudaStream_t s) {
   unsigned b = elem_blocks(n);
-  if (prec == 0) {
-    haar_kernel<float><<<b, 256, 0, s>>>(p, n, seed);
-    scale_kernel<float><<<b, 256, 0, s>>>(p.state, n, p.red_result);
-  } else {
-    haar_kernel<double><<<b, 256, 0, s>>>(p, n, seed);
-    scale_kernel<double><<<b, 256, 0, s>>>(p.state, n, p.red_result);
+  if (prec == 0) haar_kernel<float><<<b, 256, 0, s>>>(p, n, seed, j0);
+  else haar_kernel<double><<<b, 256, 0, s>>>(p, n, seed, j0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scale(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s) {
+  unsigned b = elem_blocks(n);
+  if (prec == 0) scale_kernel<float><<<b, 256, 0, s>>>(p.state, n, p.red_result);
+  else scale_kernel<double><<<b, 256, 0, s>>>(p.state, n, p.red_result);
+  return cudaGetLastError();
+}
+
+// norm^2 of a shard into red_result[0] (read-only pass through the pass kernel machinery)
+template <typename T>
+__global__ void __launch_bounds__(256) norm_kernel(DevPtrs p, uint64_t n) {
+  typedef typename VT<T>::C C;
+  __shared__ PassShared sh;
+  const C* st = reinterpret_cast<const C*>(p.state);
+  double acc[4] = {0, 0, 0, 0};
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    C v = st[i];
+    acc[0] += (double)v.x * v.x + (double)v.y * v.y;
   }
+  reduce_finish<1>(acc, p, sh);
+}
+
+cudaError_t launch_norm(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s) {
+  if (prec == 0) norm_kernel<float><<<elem_blocks(n), 256, 0, s>>>(p, n);
+  else norm_kernel<double><<<elem_blocks(n), 256, 0, s>>>(p, n);
+  return cudaGetLastError();
+}
+
+// <a|b> of two same-precision shards into red_result[0..1]
+template <typename T>
+__global__ void __launch_bounds__(256) dot_t_kernel(DevPtrs p, const void* a, const void* b, uint64_t n) {
+  typedef typename VT<T>::C C;
+  __shared__ PassShared sh;
+  const C* x = reinterpret_cast<const C*>(a);
+  const C* y = reinterpret_cast<const C*>(b);
+  double acc[4] = {0, 0, 0, 0};
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    C u = x[i], v = y[i];
+    acc[0] += (double)u.x * v.x + (double)u.y * v.y;
+    acc[1] += (double)u.x * v.y - (double)u.y * v.x;
+  }
+  reduce_finish<2>(acc, p, sh);
+}
+
+cudaError_t launch_dot_t(const DevPtrs& p, int prec, const void* a, const void* b, uint64_t n, cudaStream_t s) {
+  if (prec == 0) dot_t_kernel<float><<<elem_blocks(n), 256, 0, s>>>(p, a, b, n);
+  else dot_t_kernel<double><<<elem_blocks(n), 256, 0, s>>>(p, a, b, n);
   return cudaGetLastError();
 }
 

@@ -48,20 +48,37 @@ def marshal_pattern(inputs, outputs, cmds):
     return _i32(inputs), _i32(outputs), arr, _i32(pool), len(pool)
 
 
-class Simulator:
-    """One owqs context (one GPU, one pattern at a time)."""
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    st = lib().owqs_nccl_unique_id(buf)
+    if st != 0:
+        raise OwqsError(st, "ncclGetUniqueId failed")
+    return buf.raw
 
-    def __init__(self, precision: int = 128, device: int = 0, flags: int = 0, stream: Optional[int] = None):
+
+class Simulator:
+    """One owqs context (one GPU or one rank's shard, one pattern at a time)."""
+
+    def __init__(self, precision: int = 128, device: int = 0, flags: int = 0, stream: Optional[int] = None,
+                 n_ranks: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None):
+        """n_ranks > 1: sharded state; with flags & FLAG_LOOPBACK all shards live on
+        `device` (single-GPU testing), otherwise one process per GPU over NCCL with `nccl_id`
+        (128 bytes from nccl_unique_id() on one rank, broadcast by the caller)."""
         self._lib = lib()
         cfg = owqs_config()
         cfg.precision = precision
-        cfg.n_ranks, cfg.rank, cfg.device = 1, 0, device
+        cfg.n_ranks, cfg.rank, cfg.device = n_ranks, rank, device
         cfg.flags = flags
         cfg.stream = stream
+        self._id_buf = None
+        if nccl_id is not None:
+            self._id_buf = C.create_string_buffer(bytes(nccl_id), 128)
+            cfg.nccl_id = C.cast(self._id_buf, C.c_void_p)
         h = C.c_void_p()
         st = self._lib.owqs_create(C.byref(cfg), C.byref(h))
         if st != 0:
-            raise OwqsError(st, "owqs_create failed (is a CUDA device visible?)")
+            raise OwqsError(st, "owqs_create failed (CUDA device visible? NCCL id / rank valid?)")
+        self.n_ranks, self.rank = n_ranks, rank
         self._h = h
         self.precision = precision
         self.n_in = self.n_out = 0
@@ -122,15 +139,25 @@ class Simulator:
         self._check(st)
         return (out[:K], p0[:K]) if want else (None, None)
 
-    def get_output(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        if out is None:
+    def get_output(self, out: Optional[np.ndarray] = None) -> Optional[np.ndarray]:
+        """Full output (rank 0 / single rank / loopback); None on the other ranks (collective)."""
+        root = self.n_ranks == 1 or self.rank == 0
+        if out is None and root:
             out = np.empty(2 ** self.n_out, dtype=np.complex128)
-        assert out.dtype == np.complex128 and out.flags.c_contiguous and out.size >= 2 ** self.n_out
-        self._check(self._lib.owqs_get_output(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
-        return out
+        if root:
+            assert out.dtype == np.complex128 and out.flags.c_contiguous and out.size >= 2 ** self.n_out
+            self._check(self._lib.owqs_get_output(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+            return out
+        self._check(self._lib.owqs_get_output(self._h, None, 0))
+        return None
 
     def get_output_device(self, ptr: int, precision: int, n: int):
         self._check(self._lib.owqs_get_output_device(self._h, C.c_void_p(ptr), precision, n))
+
+    def norm2(self) -> float:
+        v = C.c_double()
+        self._check(self._lib.owqs_output_norm(self._h, C.byref(v)))
+        return v.value
 
     def inner(self, other: "Simulator") -> complex:
         re, im = C.c_double(), C.c_double()
