@@ -7,8 +7,10 @@ Default workload (N=1): config 3 — 28-wire random brickwork, depth 40 (5020 co
 A step = set the resident input (device copy) + one owqs_run over the whole pattern.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C3]
-For N > 1 launch with torch.distributed.run (one rank per GPU); every rank runs its own replica
-(the path's sharded multi-GPU mode is not in this build: DESIGN.md §7), scaling "weak".
+For N > 1 launch with torch.distributed.run (one rank per GPU): by default every rank runs its own
+replica (scaling "weak"); --shard shards one problem over the ranks on its top log2(N) slot bits
+(NCCL swaps and all-reduces, scaling "strong"); --loopback G shards it over G virtual ranks on one
+GPU.
 """
 from __future__ import annotations
 
@@ -26,6 +28,8 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     "C3": "config 3: brickwork 28 wires x 40 layers (J(alpha) + alternating CZ), sampled OWQS",
+    "C4": "config 4: brickwork 33 wires x 24 layers, sampled OWQS",
+    "C5E": "config 5: 35 x 8 flow cluster, EOWQS (positive branch, no probabilities)",
     "C3W": "config 3 at width 30: brickwork 30 wires x 40 layers, sampled OWQS",
     "C2": "config 2: QFT-20 (H = J(0), CP = 8 J + 2 CZ), sampled OWQS",
     "C3E": "config 3 in EOWQS mode (positive branch, no probabilities)",
@@ -42,6 +46,11 @@ def parse():
     ap.add_argument("--precision", type=int, default=64, choices=[64, 128])
     ap.add_argument("--flags", type=int, default=0, help="OWQS_FLAG_* for the timed context")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="with torchrun N > 1: shard ONE problem over the N ranks (NCCL swaps / all-reduce, "
+                         "strong scaling) instead of running N replicas")
+    ap.add_argument("--loopback", type=int, default=1,
+                    help="N = 1: shard the problem over this many virtual ranks on the one GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-cmds", type=int, default=None,
                     help="oracle sample: first k commands at full width (default 4 for cpu_baseline, "
@@ -53,6 +62,8 @@ def pattern_for(workload):
     from workloads import patterns as W
     if workload in ("C3", "C3E"):
         return W.config_pattern("C3", seed=1), ("eowqs" if workload == "C3E" else "sampled")
+    if workload == "C5E":
+        return W.config_pattern("C5", seed=1), "eowqs"
     return W.config_pattern(workload, seed=1), "sampled"
 
 
@@ -186,7 +197,7 @@ def run_ours(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
-    from paper_1604_05659_b200 import FLAG_PROFILE, KCLASS_NAMES, Simulator
+    from paper_1604_05659_b200 import FLAG_LOOPBACK, FLAG_PROFILE, KCLASS_NAMES, Simulator, nccl_unique_id
     from workloads.patterns import Pattern
 
     torch.cuda.set_device(local_rank)
@@ -197,26 +208,49 @@ def run_ours(args, rank, world, local_rank):
     N = 2 ** n_in
     prec = args.precision
     cdt = torch.complex64 if prec == 64 else torch.complex128
+    shard = args.shard and world > 1          # one problem sharded over the ranks (NCCL)
+    loop = args.loopback if world == 1 else 1  # one problem sharded over virtual ranks on one GPU
+    n_shards = world if shard else loop
 
-    sim = Simulator(precision=prec, device=local_rank, flags=args.flags, stream=stream.cuda_stream)
+    def make_sim(extra_flags=0):
+        kw = dict(precision=prec, device=local_rank, flags=args.flags | extra_flags, stream=stream.cuda_stream)
+        if shard:
+            ids = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(ids, src=0)
+            return Simulator(n_ranks=world, rank=rank, nccl_id=ids[0], **kw)
+        if loop > 1:
+            kw["flags"] |= FLAG_LOOPBACK
+            return Simulator(n_ranks=loop, **kw)
+        return Simulator(**kw)
+
+    sim = make_sim()
     t0 = time.perf_counter()
     sim.load(pattern)
     load_s = time.perf_counter() - t0
     st = sim.stats()
 
-    # resident input: device Haar generator of the library, copied into a torch-owned buffer
-    x = torch.empty(N, dtype=cdt, device=dev)
-    gen = Simulator(precision=prec, device=local_rank, stream=stream.cuda_stream)
-    gen.load(Pattern(list(range(n_in)), list(range(n_in)), []))
-    gen.set_input_random(1 + rank)
-    gen.run("eowqs", want=False)
-    gen.get_output_device(x.data_ptr(), prec, N)
-    gen.close()
-    torch.cuda.synchronize()
+    big = (N * (8 if prec == 64 else 16)) > (32 << 30)  # > 32 GiB: no second full-size buffer
+    x = None
+    if not shard and not big:
+        # resident input: device Haar generator of the library, copied into a torch-owned buffer
+        x = torch.empty(N, dtype=cdt, device=dev)
+        gen = Simulator(precision=prec, device=local_rank, stream=stream.cuda_stream)
+        gen.load(Pattern(list(range(n_in)), list(range(n_in)), []))
+        gen.set_input_random(1 + rank)
+        gen.run("eowqs", want=False)
+        gen.get_output_device(x.data_ptr(), prec, N)
+        gen.close()
+        torch.cuda.synchronize()
+
+    def set_input(s, i):
+        if shard or big:  # device counter-Haar input (a second 2^33+ state is not materialised)
+            s.set_input_random(1 + i)
+        else:
+            s.set_input_device(x.data_ptr(), prec, N)
 
     def step(i):
-        sim.set_input_device(x.data_ptr(), prec, N)
-        sim.run(mode, seed=1000 + i + 100_000 * rank, want=False)
+        set_input(sim, i)
+        sim.run(mode, seed=1000 + i + (0 if shard else 100_000 * rank), want=False)
 
     for i in range(args.warmup):
         step(i)
@@ -249,16 +283,17 @@ def run_ours(args, rank, world, local_rank):
     ms_per_step = ms / args.steps
     st = sim.stats()
     n_cmd = st["n_commands"]
-    value = world * n_cmd * args.steps / (ms / 1e3)
-    hbm_gbs = st["bytes_per_run"] / (ms_per_step / 1e3) / 1e9
+    problems = 1 if shard else world  # replicas each run the whole pattern
+    value = problems * n_cmd * args.steps / (ms / 1e3)
+    hbm_gbs = st["bytes_per_run"] * (1 if shard else 1) / (ms_per_step / 1e3) / 1e9  # per GPU
 
     # ---- roofline of the dominant kernel: per-launch CUDA events over profiled runs ----
     peak, peak_src = peaks()
-    prof = Simulator(precision=prec, device=local_rank, flags=args.flags | FLAG_PROFILE, stream=stream.cuda_stream)
+    prof = make_sim(FLAG_PROFILE)
     prof.load(pattern)
     agg = {}
     for r in range(3):
-        prof.set_input_device(x.data_ptr(), prec, N)
+        set_input(prof, r)
         prof.run(mode, seed=77 + r, want=False)
         if r == 0:
             continue  # first run captures the graph
@@ -273,24 +308,25 @@ def run_ours(args, rank, world, local_rank):
     prof.close()
     dom = max(agg, key=lambda c: agg[c][1])
     by_sum, ms_sum, cnt = agg[dom]
-    achieved = by_sum / (ms_sum / 1e3) / 1e9
+    achieved = by_sum / (ms_sum / 1e3) / 1e9  # bytes of all shards on this GPU / their time
     traffic = ncu_traffic()
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                 "kernel": f"owqs::{KCLASS_NAMES[dom]}_kernel", "launches": cnt,
                 "bytes_per_launch": by_sum / cnt, "avg_launch_us": 1e3 * ms_sum / cnt,
                 "share_of_step": ms_sum / 2 / prof_step_ms if prof_step_ms else None,
+                "per_class_ms": {KCLASS_NAMES[c]: v[1] / 2 for c, v in agg.items()},
                 "peak_source": peak_src, "algorithmic_bytes": "read + write of the 2^w-amplitude state per pass"}
 
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H inside the timed region ----
     e2e = None
-    if not args.no_e2e:
+    psi_host = None
+    if not args.no_e2e and not shard and not big:
         h_in = torch.empty(N, dtype=torch.complex128, pin_memory=True)
         h_in.copy_(x.to(torch.complex128))
         h_out = torch.empty(N, dtype=torch.complex128, pin_memory=True)
         a_in, a_out = h_in.numpy(), h_out.numpy()
-        sim_n_out = 2 ** len(pattern.outputs)
-        assert sim_n_out == N
+        assert 2 ** len(pattern.outputs) == N
         k_e2e = max(2, args.steps // 2)
 
         def e2e_step(i):
@@ -311,14 +347,16 @@ def run_ours(args, rank, world, local_rank):
             t = torch.tensor([dt], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             dt = float(t.item())
-        e2e = {"value": world * n_cmd * k_e2e / dt, "unit": "commands/s", "h2d_bytes_per_step": N * 16,
+        e2e = {"value": problems * n_cmd * k_e2e / dt, "unit": "commands/s", "h2d_bytes_per_step": N * 16,
                "d2h_bytes_per_step": N * 16, "steps": k_e2e, "ms_per_step": 1e3 * dt / k_e2e}
-        if rank == 0 and world == 1 and not args.no_cpu_baseline:
-            psi_host = a_in
+        psi_host = a_in
+    elif shard or big:
+        e2e = {"value": None, "unit": "commands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "the 2^n host state (>= 128 GiB complex128) is not materialised; input generated on device"}
     # ---- CPU baseline: the oracle, rank 0 at N=1 only, bounded sample ----
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.no_e2e:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
+        if psi_host is None:
             psi_host = x.to(torch.complex128).cpu().numpy()
         psi_host = psi_host / np.linalg.norm(psi_host)
         dt, k = oracle_prefix_sample(pattern, psi_host, args.ref_cmds or 4, seed=1)
@@ -327,17 +365,24 @@ def run_ours(args, rank, world, local_rank):
                          f"of {args.workload} at full width ({n_in}->{n_in + 1} qubits): {dt:.1f} s",
                "host_cores_available": os.cpu_count()}
 
+    if shard:
+        par = f"shard{world}"
+    elif loop > 1:
+        par = f"loopback-shard{loop} (one GPU)"
+    else:
+        par = "single" if world == 1 else f"replicas{world}"
     line = {
         "metric": "pattern commands/s (state-update HBM GB/s in hbm_gbs / roofline)",
         "value": value, "unit": "commands/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if prec == 64 else "f64", "data": "synthetic",
+        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if shard else "weak",
+        "vs_baseline": None, "dtype": "f32" if prec == 64 else "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "mode": mode, "amplitudes": f"complex{prec}",
                    "commands": n_cmd, "measurements": st["n_measure"], "paper_m": st["paper_m"],
-                   "phys_bits": st["phys_bits"], "passes_per_run": st["n_passes"],
+                   "phys_bits": st["phys_bits"], "passes_per_run": st["n_passes"], "swaps_per_run": st["n_swaps"],
                    "launches_per_run": st["n_launches"], "state_bytes": N * (8 if prec == 64 else 16),
                    "l2": "state (>= 2 GiB) larger than the 126 MB L2: no flush needed",
-                   "parallelism": "single" if world == 1 else f"replicas{world}",
+                   "parallelism": par,
+                   "input": "device counter-Haar per step" if (shard or big) else "resident copy per step",
                    "load_pattern_s": load_s, "schedule_ms": st["schedule_ms"]},
         "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / peak,
         "roofline": roofline,
