@@ -465,8 +465,10 @@ __device__ __forceinline__ void flush_all(T (&re)[NV][2], T (&im)[NV][2], uint32
 }
 
 
-template <typename T, int KHI, int UNR, int MINB = 0>
+template <typename T, int KHI, int UNR, int MINB = 0, int RED = -1>
 __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass_kernel(const StepDesc d, const DevPtrs p) {
+  // RED >= 0: the step's reduction kind fixed at compile time (fewer live fp64 accumulators)
+  const int red_kind = RED >= 0 ? RED : d.red_kind;
   typedef typename VT<T>::V V;
   constexpr int SB = VT<T>::SB, EPV = VT<T>::EPV;
   constexpr int G = 1 << KHI;
@@ -666,7 +668,7 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
     }
 
     // reductions of the pass output: per-vector partials in T, accumulated in fp64
-    if (d.red_kind == RED_NORM) {
+    if (red_kind == RED_NORM) {
 #pragma unroll
       for (int v = 0; v < NV; ++v) {
         T n = 0;
@@ -674,7 +676,7 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
         for (int e = 0; e < EPV; ++e) n += re[v][e] * re[v][e] + im[v][e] * im[v][e];
         acc[0] += (double)n;
       }
-    } else if (d.red_kind == RED_RHO) {
+    } else if (red_kind == RED_RHO) {
       const int r = d.red_slot;
       const uint32_t mr1 = slot_mask_p<T, KHI, UNR>(r, lane, gb, d, p.rank);
 #pragma unroll
@@ -747,8 +749,8 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
         }
     }
   }
-  if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
-  else if (d.red_kind == RED_RHO) reduce_finish<4>(acc, p, sh);
+  if (red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
+  else if (red_kind == RED_RHO) reduce_finish<4>(acc, p, sh);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1121,7 +1123,12 @@ cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStrea
     uint64_t blocks = 1ull << slack;
     blocks = std::min<uint64_t>(blocks, (uint64_t)g_lim.max_blocks_pass[prec][khi]);
     dim3 grid((unsigned)blocks), blk(256);
-#define OWQS_PASS(T, K, U) pass_kernel<T, K, U><<<grid, blk, 0, s>>>(d, p)
+#define OWQS_PASS(T, K, U)                                                                      \
+  do {                                                                                          \
+    if (d.red_kind == RED_NONE) pass_kernel<T, K, U, 0, RED_NONE><<<grid, blk, 0, s>>>(d, p);   \
+    else if (d.red_kind == RED_NORM) pass_kernel<T, K, U, 0, RED_NORM><<<grid, blk, 0, s>>>(d, p); \
+    else pass_kernel<T, K, U, 0, RED_RHO><<<grid, blk, 0, s>>>(d, p);                            \
+  } while (0)
 #define OWQS_PASS1(T, K, U) pass_kernel<T, K, U, 1><<<grid, blk, 0, s>>>(d, p)
     if (prec == 0) {
       switch (khi) {
