@@ -41,7 +41,7 @@ typedef enum {
   OWQS_OK = 0,
   OWQS_E_ARG = 1,               /* bad argument (NULL, size mismatch, unknown enum)          */
   OWQS_E_PATTERN = 2,           /* rules D0-D3 (L83-91), duplicate E, E(u,u), second N, ...  */
-  OWQS_E_NO_GFLOW = 3,          /* reserved: EOWQS gflow pre-check (L372)                     */
+  OWQS_E_NO_GFLOW = 3,          /* EOWQS on a pattern whose open graph has no gflow (L372)     */
   OWQS_E_BRANCH = 4,            /* forced outcome whose probability is < 1e-12               */
   OWQS_E_STATE = 5,             /* call order (run before set_input, output before run, ...)  */
   OWQS_E_NOMEM = 6,             /* state width exceeds device memory                          */
@@ -88,6 +88,8 @@ typedef struct {
 #define OWQS_FLAG_NO_TUNE     0x8u /* PROA with the initial weights only (no L487 tuning loop)   */
 #define OWQS_FLAG_PROFILE     0x10u /* record a CUDA event after every kernel of owqs_run (event
                                        record nodes in the graph); see owqs_launch_profile       */
+#define OWQS_FLAG_NO_GFLOW    0x40u /* EOWQS without the gflow pre-check of L372 (the final-norm
+                                       check still reports OWQS_E_NOT_DETERMINISTIC)             */
 #define OWQS_FLAG_LOOPBACK    0x20u /* n_ranks > 1 on ONE device: the context holds every rank's
                                        shard and runs them one after the other (swaps and
                                        all-reduces by device copies); for testing the sharded path
@@ -158,6 +160,7 @@ owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed);
 
 /* Execute the loaded pattern on the current input (consumes it: the state becomes the output).
  * mode OWQS_SAMPLED : outcomes drawn as in the conventions above from `seed`;
+ *      (OWQS_EOWQS first checks the gflow: OWQS_E_NO_GFLOW, see owqs_gflow)
  *      OWQS_FORCED  : forced[n_measure] gives each outcome (given-order ordinal);
  *                     OWQS_E_BRANCH if a forced branch has probability < 1e-12;
  *      OWQS_EOWQS   : every outcome 0, no probability computation, sqrt2 per M (L372);
@@ -189,6 +192,13 @@ owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2);
  * U: HOST array of n = 2^n_out * 2^n_in complex128 (interleaved), column-major.
  * max_unitarity_err (may be NULL): max |(U^dag U - I)_ij|. Overwrites the current input. */
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err);
+
+/* gflow of the pattern's open graph (L372, Mhalla-Perdrix [25]; all measurements in the XY plane):
+ * OWQS_OK if one exists, else OWQS_E_NO_GFLOW ("the pattern is reported as an incorrect one").
+ * layers[n_measure] (may be NULL): backward layer of each measured qubit (given-order ordinal;
+ * outputs are layer 0); depth (may be NULL): number of layers. owqs_run(OWQS_EOWQS) and
+ * owqs_recognize apply this check first (unless OWQS_FLAG_NO_GFLOW). Host only. */
+owqs_status owqs_gflow(owqs_ctx* ctx, int32_t* layers, int32_t* depth);
 
 /* Sizes after owqs_load_pattern (any pointer may be NULL). n_passes is for the sampled plan. */
 owqs_status owqs_pattern_info(owqs_ctx* ctx, int64_t* n_measure, int32_t* paper_m, int32_t* phys_bits,

@@ -51,6 +51,9 @@ owqs_status owqs_host_info_get(const owqs_host_plan* h, owqs_host_info* info);
  * plan_qubits / plan_ms: n_measure int32 (measured qubit ids in plan order and their MS). */
 owqs_status owqs_host_program(const owqs_host_plan* h, void* steps, void* mst, int32_t* sig, int32_t* out_slot,
                               int32_t* plan_qubits, int32_t* plan_ms);
+/* gflow of the loaded pattern's open graph (see owqs_gflow in owqs.h): OWQS_OK or OWQS_E_NO_GFLOW;
+ * layers[n_measure] by given-order ordinal (may be NULL), depth (may be NULL). */
+owqs_status owqs_host_gflow(const owqs_host_plan* h, int32_t* layers, int32_t* depth);
 const char* owqs_host_error(const owqs_host_plan* h);
 void owqs_host_free(owqs_host_plan* h);
 

@@ -20,7 +20,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernels.cu"]
-CPP_SOURCES = ["scheduler.cpp", "capi.cpp", "host_api.cpp"]
+CPP_SOURCES = ["scheduler.cpp", "gflow.cpp", "capi.cpp", "host_api.cpp"]
 HEADERS = ["owqs_internal.h", "scheduler.h"]
 
 

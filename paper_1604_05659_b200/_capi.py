@@ -13,13 +13,14 @@ STATUS_NAMES = {0: "OWQS_OK", 1: "OWQS_E_ARG", 2: "OWQS_E_PATTERN", 3: "OWQS_E_N
                 9: "OWQS_E_NOT_DETERMINISTIC"}
 MODES = {"sampled": 0, "forced": 1, "eowqs": 2}
 FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE, FLAG_LOOPBACK = 1, 2, 4, 8, 16, 32
+FLAG_NO_GFLOW = 64
 KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = ["owqs_create", "owqs_destroy", "owqs_load_pattern", "owqs_set_input", "owqs_set_input_device",
             "owqs_set_input_random", "owqs_run", "owqs_get_output", "owqs_get_output_device",
             "owqs_output_inner", "owqs_output_norm", "owqs_nccl_unique_id", "owqs_recognize",
-            "owqs_pattern_info", "owqs_plan_order",
+            "owqs_pattern_info", "owqs_plan_order", "owqs_gflow",
             "owqs_set_proa_weights", "owqs_stats", "owqs_launch_profile", "owqs_last_error", "owqs_version"]
 
 
@@ -68,6 +69,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "owqs_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "owqs_recognize": (C.c_int, [ctx, P(C.c_double), C.c_int64, P(C.c_double)]),
         "owqs_pattern_info": (C.c_int, [ctx, P(C.c_int64), P(C.c_int32), P(C.c_int32), P(C.c_int32)]),
+        "owqs_gflow": (C.c_int, [ctx, P(C.c_int32), P(C.c_int32)]),
         "owqs_plan_order": (C.c_int, [ctx, C.c_int, P(C.c_int32), P(C.c_int32), C.c_int64]),
         "owqs_set_proa_weights": (C.c_int, [ctx, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int32]),
         "owqs_stats": (C.c_int, [ctx, P(owqs_stats_t)]),
@@ -83,8 +85,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 
 # ---- include/owqs_host.h (host-only introspection; no CUDA calls) ------------------------------
-HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_error",
-                 "owqs_host_free"]
+HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_gflow",
+                 "owqs_host_error", "owqs_host_free"]
 KMAX_HI, MAX_OPS, MAX_BFLY = 4, 64, 24
 
 
@@ -124,6 +126,7 @@ def declare_host(lib: C.CDLL) -> C.CDLL:
         "owqs_host_info_get": (C.c_int, [h, P(owqs_host_info)]),
         "owqs_host_program": (C.c_int, [h, C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32),
                                         P(C.c_int32)]),
+        "owqs_host_gflow": (C.c_int, [h, P(C.c_int32), P(C.c_int32)]),
         "owqs_host_error": (C.c_char_p, [h]),
         "owqs_host_free": (None, [h]),
     }

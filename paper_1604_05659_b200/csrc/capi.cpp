@@ -92,6 +92,8 @@ struct owqs_ctx {
   int last_cm = 0;
   std::vector<cudaEvent_t> prof_ev;  // OWQS_FLAG_PROFILE: event after every launch (+1 start)
   int prof_cm = -1;
+  int gflow_state = 0;  // 0 unknown, 1 has a gflow, -1 none (L372 pre-check, cached per pattern)
+  std::string gflow_msg;
 
   uint32_t shard_rank(int i) const { return loopback ? (uint32_t)i : (uint32_t)rank; }
 };
@@ -416,6 +418,19 @@ owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
   return OWQS_OK;
 }
 
+// L372: EOWQS only for patterns with a gflow ("otherwise ... reported as an incorrect one")
+owqs_status gflow_gate(owqs_ctx* ctx) {
+  if (ctx->cfg.flags & OWQS_FLAG_NO_GFLOW) return OWQS_OK;
+  if (ctx->gflow_state == 0) {
+    std::vector<int> layer;
+    std::vector<std::vector<int>> g;
+    ctx->gflow_msg = find_gflow(ctx->hp, layer, g);
+    ctx->gflow_state = ctx->gflow_msg.empty() ? 1 : -1;
+  }
+  if (ctx->gflow_state < 0) return fail(ctx, OWQS_E_NO_GFLOW, "EOWQS: " + ctx->gflow_msg);
+  return OWQS_OK;
+}
+
 owqs_status norm_all(owqs_ctx* ctx, double* out) {
   const Program& pr = ctx->cm[ctx->out_cm >= 0 ? ctx->out_cm : 0].prog;
   const int nb = ctx->n_ranks > 1 ? pr.phys_bits - ctx->n_global : (int)ctx->hp.outputs.size();
@@ -532,6 +547,7 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
   if (!ctx) return OWQS_E_ARG;
   ctx->loaded = false;
   ctx->has_input = ctx->has_output = false;
+  ctx->gflow_state = 0;
   std::string e = validate_pattern(inputs, n_in, outputs, n_out, cmds, n_cmds, domain_pool, pool_len, ctx->hp);
   if (!e.empty()) return fail(ctx, OWQS_E_PATTERN, e);
   if (n_in > 40 || n_out > 40) return fail(ctx, OWQS_E_ARG, "more than 40 input/output qubits");
@@ -636,6 +652,10 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   if (!ctx->has_input) return fail(ctx, OWQS_E_STATE, "run without a fresh input (set_input consumes per run)");
   if (mode != OWQS_SAMPLED && mode != OWQS_FORCED && mode != OWQS_EOWQS) return fail(ctx, OWQS_E_ARG, "bad mode");
   if (mode == OWQS_FORCED && ctx->hp.n_measure > 0 && !forced) return fail(ctx, OWQS_E_ARG, "forced outcomes missing");
+  if (mode == OWQS_EOWQS) {
+    owqs_status g = gflow_gate(ctx);
+    if (g != OWQS_OK) return g;
+  }
   const int cmi = mode == OWQS_EOWQS ? 1 : 0;
   owqs_status s = run_internal(ctx, cmi, mode, seed, forced);
   const int64_t K = ctx->hp.n_measure;
@@ -761,7 +781,9 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
   if (ni > 14 || no > 14) return fail(ctx, OWQS_E_ARG, "recognize is limited to 14 input/output qubits");
   const uint64_t rows = 1ull << no, cols = 1ull << ni;
   if (!U || n < (int64_t)(rows * cols)) return fail(ctx, OWQS_E_ARG, "U must hold 2^n_out * 2^n_in entries");
-  owqs_status s = ensure_device(ctx);
+  owqs_status s = gflow_gate(ctx);
+  if (s != OWQS_OK) return s;
+  s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
   for (uint64_t k = 0; k < cols; ++k) {
     CU(launch_basis(ctx->shards[0].d_state, ctx->prec, cols, k, ctx->stream));
@@ -788,6 +810,23 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
     *max_unitarity_err = worst;
   }
   return OWQS_OK;
+}
+
+owqs_status owqs_gflow(owqs_ctx* ctx, int32_t* layers, int32_t* depth) {
+  if (!ctx) return OWQS_E_ARG;
+  if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "no pattern loaded");
+  std::vector<int> layer;
+  std::vector<std::vector<int>> g;
+  std::string e = find_gflow(ctx->hp, layer, g);
+  ctx->gflow_state = e.empty() ? 1 : -1;
+  ctx->gflow_msg = e;
+  int d = 0;
+  for (int q = 0; q < ctx->hp.nq; ++q) {
+    d = std::max(d, layer[q]);
+    if (layers && ctx->hp.m_ord_of_qubit[q] >= 0) layers[ctx->hp.m_ord_of_qubit[q]] = layer[q];
+  }
+  if (depth) *depth = d;
+  return e.empty() ? OWQS_OK : fail(ctx, OWQS_E_NO_GFLOW, e);
 }
 
 owqs_status owqs_pattern_info(owqs_ctx* ctx, int64_t* n_measure, int32_t* paper_m, int32_t* phys_bits,

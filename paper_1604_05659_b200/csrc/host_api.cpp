@@ -1,6 +1,7 @@
 // Host-only introspection API (include/owqs_host.h): validation + PROA + compile, no CUDA calls.
 #include <string.h>
 
+#include <algorithm>
 #include <string>
 
 #include "owqs_host.h"
@@ -88,6 +89,20 @@ owqs_status owqs_host_program(const owqs_host_plan* h, void* steps, void* mst, i
     if (plan_ms) plan_ms[i] = h->plan.ms[i];
   }
   return OWQS_OK;
+}
+
+owqs_status owqs_host_gflow(const owqs_host_plan* h, int32_t* layers, int32_t* depth) {
+  if (!h) return OWQS_E_ARG;
+  std::vector<int> layer;
+  std::vector<std::vector<int>> g;
+  std::string e = find_gflow(h->hp, layer, g);
+  int d = 0;
+  for (int q = 0; q < h->hp.nq; ++q) {
+    d = std::max(d, layer[q]);
+    if (layers && h->hp.m_ord_of_qubit[q] >= 0) layers[h->hp.m_ord_of_qubit[q]] = layer[q];
+  }
+  if (depth) *depth = d;
+  return e.empty() ? OWQS_OK : OWQS_E_NO_GFLOW;
 }
 
 const char* owqs_host_error(const owqs_host_plan* h) { return h ? h->err.c_str() : "NULL handle"; }

@@ -75,4 +75,8 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int s
 void plan_and_compile(const HostPattern& hp, int mode, int seg_bits, bool fuse, bool given_order,
                       const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0);
 
+// gflow of the pattern's open graph ([25]): "" if found, else the reason. layer[q] = 0
+// for outputs, k >= 1 for the k-th backward layer; g[q] = correction set of measured q.
+std::string find_gflow(const HostPattern& hp, std::vector<int>& layer, std::vector<std::vector<int>>& g);
+
 }  // namespace owqs

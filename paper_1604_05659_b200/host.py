@@ -23,6 +23,27 @@ class HostProgram:
     plan_ms: List[int]
 
 
+def host_gflow(pattern):
+    """(has_gflow, layers per M in given order, depth) of the pattern's open graph (no GPU)."""
+    L = lib()
+    i, o, arr, pool, plen = marshal_pattern(pattern.inputs, pattern.outputs, pattern.cmds)
+    h = C.c_void_p()
+    st = L.owqs_host_compile(i, len(pattern.inputs), o, len(pattern.outputs), arr, len(pattern.cmds), pool, plen,
+                             2, 128, 0, None, 1, C.byref(h))
+    try:
+        if st != 0:
+            msg = L.owqs_host_error(h) if h else b""
+            raise OwqsError(st, msg.decode() if msg else "")
+        K = pattern.n_measure
+        layers = (C.c_int32 * max(1, K))()
+        depth = C.c_int32()
+        st = L.owqs_host_gflow(h, layers, C.byref(depth))
+        return st == 0, list(layers)[:K], depth.value
+    finally:
+        if h:
+            L.owqs_host_free(h)
+
+
 def compile_host(pattern, mode: str = "sampled", precision: int = 128, flags: int = 0,
                  weights: Optional[Sequence[float]] = None, n_ranks: int = 1) -> HostProgram:
     L = lib()

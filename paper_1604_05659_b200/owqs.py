@@ -170,6 +170,16 @@ class Simulator:
         self._check(self._lib.owqs_recognize(self._h, U.ctypes.data_as(C.POINTER(C.c_double)), U.size, C.byref(err)))
         return U.T.copy(), err.value
 
+    def gflow(self):
+        """(has_gflow, layers per M in given order, depth) — L372's EOWQS pre-check."""
+        K = self.n_measure
+        layers = (C.c_int32 * max(1, K))()
+        depth = C.c_int32()
+        st = self._lib.owqs_gflow(self._h, layers, C.byref(depth))
+        if st not in (0, 3):
+            self._check(st)
+        return st == 0, list(layers)[:K], depth.value
+
     def pattern_info(self) -> dict:
         nm, pm, pb, npass = C.c_int64(), C.c_int32(), C.c_int32(), C.c_int32()
         self._check(self._lib.owqs_pattern_info(self._h, C.byref(nm), C.byref(pm), C.byref(pb), C.byref(npass)))

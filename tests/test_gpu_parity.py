@@ -91,25 +91,57 @@ def test_random_patterns_vs_oracle(sim, seed):
     check(sim, p, psi, "sampled", seed=seed, same_order=False)
     ref = oracle.run(p, psi, mode="sampled", seed=seed)
     check(sim, p, psi, "forced", forced=ref.outcomes, same_order=False)
-    check(sim, p, psi, "eowqs") if _eowqs_ok(sim, p, psi) else None
+    _eowqs_check(sim, p, psi)
 
 
-def _eowqs_ok(sim, p, psi):
-    """EOWQS on a non-deterministic pattern must report OWQS_E_NOT_DETERMINISTIC unless the
-    sqrt2 rescale happens to conserve the norm; both cases are checked."""
-    ref = oracle.run(p, psi, mode="eowqs")
-    nrm = np.vdot(ref.output, ref.output).real
-    tol = 1e-8 if sim.precision == 128 else 1e-3
-    if abs(nrm - 1) <= tol:
-        return True
-    sim.load(p)
-    sim.set_input(psi)
+def _eowqs_check(sim, p, psi):
+    """EOWQS on an open graph without gflow is refused (OWQS_E_NO_GFLOW, L372). With the pre-check
+    off (or with a gflow), a non-deterministic command list reports OWQS_E_NOT_DETERMINISTIC unless
+    the sqrt2 rescale happens to conserve the norm; the positive branch matches the oracle."""
+    from paper_1604_05659_b200 import FLAG_NO_GFLOW
+    from paper_1604_05659_b200.host import host_gflow
+    run_sim, own = sim, False
+    if not host_gflow(p)[0]:
+        sim.load(p)
+        sim.set_input(psi)
+        with pytest.raises(OwqsError) as e:
+            sim.run("eowqs")
+        assert e.value.status_name == "OWQS_E_NO_GFLOW"
+        run_sim, own = Simulator(precision=sim.precision, flags=FLAG_NO_GFLOW), True
+    try:
+        ref = oracle.run(p, psi, mode="eowqs")
+        nrm = np.vdot(ref.output, ref.output).real
+        tol = 1e-8 if sim.precision == 128 else 1e-3
+        if abs(nrm - 1) <= tol:
+            check(run_sim, p, psi, "eowqs")
+            return
+        run_sim.load(p)
+        run_sim.set_input(psi)
+        with pytest.raises(OwqsError) as e:
+            run_sim.run("eowqs")
+        assert e.value.status_name == "OWQS_E_NOT_DETERMINISTIC"
+        out = run_sim.get_output()  # the output is still the sqrt2-scaled positive branch
+        assert np.max(np.abs(out - ref.output)) <= TOL[sim.precision]["amp"] * max(1.0, np.max(np.abs(ref.output)))
+    finally:
+        if own:
+            run_sim.close()
+
+
+def test_gflow_gate_and_layers(sim):
+    """owqs_gflow on the paper's patterns (L372): CNOT and config families have one, a funnel
+    graph does not (EOWQS refused)."""
+    sim.load(W.cnot_pattern_eq22())
+    ok, layers, depth = sim.gflow()
+    assert ok and depth == 2
+    sim.load(W.config_pattern("CL:6x5", seed=2))
+    assert sim.gflow()[0]
+    bad = W.Pattern([1, 2], [3], [W.E(1, 3), W.E(2, 3), W.M(1, 0.), W.M(2, 0.)])
+    sim.load(bad)
+    assert not sim.gflow()[0]
+    sim.set_input(haar_state(2, 1))
     with pytest.raises(OwqsError) as e:
         sim.run("eowqs")
-    assert e.value.status_name == "OWQS_E_NOT_DETERMINISTIC"
-    out = sim.get_output()  # the output is still the sqrt2-scaled positive branch
-    assert np.max(np.abs(out - ref.output)) <= TOL[sim.precision]["amp"] * max(1.0, np.max(np.abs(ref.output)))
-    return False
+    assert e.value.status_name == "OWQS_E_NO_GFLOW"
 
 
 def test_forced_impossible_branch(sim):
