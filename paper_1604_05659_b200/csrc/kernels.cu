@@ -338,7 +338,7 @@ template <> __device__ __forceinline__ void chain<double>(int& lm, double x) {
 }
 
 template <int KHI, int MINB> struct PassBounds {
-  static constexpr int min_blocks = MINB > 0 ? MINB : (KHI <= 2 ? 3 : 2);
+  static constexpr int min_blocks = MINB > 0 ? MINB : (KHI <= 3 ? 3 : 2);
 };
 
 // Sign flips accumulated in `neg` (bit v*EPV+e) applied branch-free through the sign bit.
