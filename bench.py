@@ -27,6 +27,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
+    "C1": "config 1: 3-wire random J/CZ circuit (12 J, 4 CZ), 64 Haar inputs per step in one batched launch",
     "C3": "config 3: brickwork 28 wires x 40 layers (J(alpha) + alternating CZ), sampled OWQS",
     "C4": "config 4: brickwork 33 wires x 24 layers, sampled OWQS",
     "C5E": "config 5: 35 x 8 flow cluster, EOWQS (positive branch, no probabilities)",
@@ -188,6 +189,68 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": "commands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------------------- config 1 (batched)
+def run_batched_c1(args, rank, world, local_rank):
+    """Config 1: each step runs 64 Haar inputs through one batched launch (owqs_run_batch) on a
+    host buffer (so value and e2e coincide: the 64 x 8 x 16 B host round trip is inside)."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1604_05659_b200 import Simulator
+    from workloads import patterns as W
+    from workloads.inputs import haar_state
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    p = W.config_pattern("C1", seed=1)
+    sim = Simulator(precision=args.precision, device=local_rank)
+    sim.load(p)
+    B = 64
+    psis = np.stack([haar_state(3, 1000 * rank + k) for k in range(B)])
+    for i in range(args.warmup):
+        sim.run_batch(psis, "sampled", seeds=np.arange(B) + i * B)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        sim.run_batch(psis, "sampled", seeds=np.arange(B) + (args.warmup + i) * B)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    st = sim.stats()
+    n_cmd = st["n_commands"]
+    value = world * B * n_cmd * args.steps / dt
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        t1 = time.perf_counter()
+        for k in range(B):
+            oracle.run(p, psis[k], mode="sampled", seed=k)
+        cdt = time.perf_counter() - t1
+        cpu = {"value": B * n_cmd / cdt, "unit": "commands/s", "cores": 1, "kind": "oracle",
+               "sample": f"the same 64 inputs of config 1 through the oracle: {cdt:.2f} s"}
+    line = {"metric": "pattern commands/s", "value": value, "unit": "commands/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == 64 else "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS["C1"], "batch": B, "commands": n_cmd, "paper_m": st["paper_m"],
+                       "phys_bits": st["phys_bits"], "parallelism": "single" if world == 1 else f"replicas{world}",
+                       "timing": "wall clock around synchronous batched calls (host buffers)"},
+            "roofline": None, "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "commands/s", "h2d_bytes_per_step": B * 8 * 16,
+                    "d2h_bytes_per_step": B * 4 * 16},
+            "gpu_launches": args.steps}
+    sim.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     return 0
 
 
@@ -409,7 +472,7 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    rc = run_ours(args, rank, world, local_rank)
+    rc = run_batched_c1(args, rank, world, local_rank) if args.workload == "C1" else run_ours(args, rank, world, local_rank)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

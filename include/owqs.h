@@ -171,6 +171,19 @@ owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed);
 owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced,
                      uint8_t* outcomes_out, double* prob0_out);
 
+/* Batched replicas: run the loaded pattern on n_batch independent inputs in
+ * one launch (one CTA per state, the state in shared memory; single rank, physical width <= 12).
+ * inputs  : HOST [n_batch][2^n_in] complex128 interleaved (input k of state b at b*2^n_in + k)
+ * seeds   : [n_batch] sampled-mode seeds (NULL: all 0); forced: [n_batch][n_measure] (OWQS_FORCED)
+ * outputs : HOST [n_batch][2^n_out] complex128; outcomes / prob0 (may be NULL): [n_batch][n_measure]
+ * Semantics per state are those of owqs_set_input + owqs_run + owqs_get_output; EOWQS applies the
+ * gflow gate, OWQS_E_BRANCH if any forced branch is impossible, OWQS_E_NOT_DETERMINISTIC if any
+ * EOWQS output norm^2 is off by more than the owqs_run tolerance. Does not touch the context's
+ * current input/output. */
+owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const double* inputs,
+                           const uint64_t* seeds, const uint8_t* forced, double* outputs,
+                           uint8_t* outcomes, double* prob0);
+
 /* Output state over O (L153, L419): HOST array of n_amps >= 2^n_out complex128, interleaved,
  * bit k <-> outputs[k]. Multi-rank (collective): gathered to rank 0, filled on rank 0 only
  * (amps may be NULL elsewhere); needs 2^n_out complex128 of free device memory on rank 0. */
@@ -188,7 +201,8 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im);
 owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2);
 
 /* Recognition problem (L33): the unitary implemented by the loaded (deterministic) pattern.
- * Column k = EOWQS run on basis input |k> (all outcomes 0, sqrt2 per M: a linear map).
+ * Column k = EOWQS run on basis input |k> (all outcomes 0, sqrt2 per M: a linear map); the
+ * 2^n_in columns run as one owqs_run_batch launch when the width allows.
  * U: HOST array of n = 2^n_out * 2^n_in complex128 (interleaved), column-major.
  * max_unitarity_err (may be NULL): max |(U^dag U - I)_ij|. Overwrites the current input. */
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err);

@@ -33,6 +33,8 @@ cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_w
                              cudaStream_t s);
 cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
+cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base, int K, int n_batch, const void* in,
+                         void* out, int n_in, int n_out, const int* out_slot, int phys, int prec, cudaStream_t s);
 }  // namespace owqs
 
 using namespace owqs;
@@ -44,6 +46,7 @@ struct CompiledMode {
   Program prog;
   MStatic* d_mst = nullptr;
   int32_t* d_sig = nullptr;
+  StepDesc* d_steps = nullptr;  // device copy of the program (batched replicas)
   cudaGraphExec_t gexec = nullptr;
   double schedule_ms = 0;
 };
@@ -142,6 +145,7 @@ void free_mode(CompiledMode& m) {
   if (m.gexec) cudaGraphExecDestroy(m.gexec);
   if (m.d_mst) cudaFree(m.d_mst);
   if (m.d_sig) cudaFree(m.d_sig);
+  if (m.d_steps) cudaFree(m.d_steps);
   m = CompiledMode();
 }
 
@@ -414,6 +418,92 @@ owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
                        cudaMemcpyDeviceToHost, ctx->stream));
     CU(cudaStreamSynchronize(ctx->stream));
     if (!pinned) memcpy(amps + 2 * j0, ctx->h_staging, cnt * 16);
+  }
+  return OWQS_OK;
+}
+
+constexpr int kBatchMaxBytes = 64 << 10;  // shared-memory state of one replica
+
+owqs_status run_batch_internal(owqs_ctx* ctx, int mode, int64_t nb, const double* inputs, const uint64_t* seeds,
+                               const uint8_t* forced, double* outputs, uint8_t* outcomes, double* prob0) {
+  const int cmi = mode == OWQS_EOWQS ? 1 : 0;
+  CompiledMode& m = ctx->cm[cmi];
+  const Program& pr = m.prog;
+  const int K = ctx->hp.n_measure, ni = (int)ctx->hp.inputs.size(), no = (int)ctx->hp.outputs.size();
+  if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "batched replicas run on a single rank");
+  if (((size_t)ctx->elem << pr.phys_bits) > (size_t)kBatchMaxBytes)
+    return fail(ctx, OWQS_E_ARG, "batched replicas need a physical width <= 12 (complex128: 12, complex64: 13)");
+  owqs_status s = ensure_device(ctx);
+  if (s != OWQS_OK) return s;
+  if (!m.d_steps) {
+    CU(cudaMalloc(&m.d_steps, std::max<size_t>(1, pr.steps.size()) * sizeof(StepDesc)));
+    CU(cudaMemcpy(m.d_steps, pr.steps.data(), pr.steps.size() * sizeof(StepDesc), cudaMemcpyHostToDevice));
+  }
+  const size_t in_b = (size_t)nb * (16ull << ni), out_b = (size_t)nb * (16ull << no);
+  const size_t Kb = std::max<size_t>(1, (size_t)K) * nb;
+  char *d_in = nullptr, *d_out = nullptr, *d_runs = nullptr, *d_oc = nullptr, *d_p0 = nullptr, *d_f = nullptr,
+       *d_err = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(d_in); cudaFree(d_out); cudaFree(d_runs); cudaFree(d_oc); cudaFree(d_p0); cudaFree(d_f); cudaFree(d_err);
+  };
+  cudaError_t e = cudaMalloc(&d_in, in_b);
+  if (e == cudaSuccess) e = cudaMalloc(&d_out, out_b);
+  if (e == cudaSuccess) e = cudaMalloc(&d_runs, nb * sizeof(RunParams));
+  if (e == cudaSuccess) e = cudaMalloc(&d_oc, Kb);
+  if (e == cudaSuccess) e = cudaMalloc(&d_p0, Kb * sizeof(double));
+  if (e == cudaSuccess) e = cudaMalloc(&d_f, Kb);
+  if (e == cudaSuccess) e = cudaMalloc(&d_err, nb * sizeof(int32_t));
+  if (e != cudaSuccess) {
+    cleanup();
+    return fail(ctx, OWQS_E_NOMEM, "batch buffers");
+  }
+  std::vector<RunParams> rp(nb);
+  for (int64_t b = 0; b < nb; ++b) {
+    rp[b].mode = mode;
+    rp[b].seed = seeds ? seeds[b] : 0;
+  }
+  e = cudaMemcpyAsync(d_in, inputs, in_b, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(d_runs, rp.data(), nb * sizeof(RunParams), cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess && mode == OWQS_FORCED && K > 0)
+    e = cudaMemcpyAsync(d_f, forced, (size_t)K * nb, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_err, 0, nb * sizeof(int32_t), ctx->stream);
+  DevPtrs base = dev_ptrs(ctx, m, 0);
+  base.outcome = (uint8_t*)d_oc;
+  base.prob0 = (double*)d_p0;
+  base.forced = (const uint8_t*)d_f;
+  base.run = (const RunParams*)d_runs;
+  base.err = (int32_t*)d_err;
+  if (e == cudaSuccess)
+    e = launch_batch(m.d_steps, (int)pr.steps.size(), base, K, (int)nb, d_in, d_out, ni, no, pr.out_slot.data(),
+                     pr.phys_bits, ctx->prec, ctx->stream);
+  std::vector<int32_t> herr(nb, 0);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(outputs, d_out, out_b, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess && outcomes && K > 0 && mode != OWQS_EOWQS)
+    e = cudaMemcpyAsync(outcomes, d_oc, (size_t)K * nb, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess && prob0 && K > 0 && mode != OWQS_EOWQS)
+    e = cudaMemcpyAsync(prob0, d_p0, (size_t)K * nb * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(herr.data(), d_err, nb * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cleanup();
+  if (e != cudaSuccess) return fail(ctx, OWQS_E_CUDA, std::string("batch: ") + cudaGetErrorString(e));
+  if (mode == OWQS_EOWQS && K > 0) {
+    if (outcomes) memset(outcomes, 0, (size_t)K * nb);
+    if (prob0)
+      for (size_t i = 0; i < (size_t)K * nb; ++i) prob0[i] = -1.0;
+  }
+  for (int64_t b = 0; b < nb; ++b)
+    if (herr[b]) return fail(ctx, OWQS_E_BRANCH, "forced outcome on a branch with probability < 1e-12 (batch item " +
+                                                     std::to_string(b) + ")");
+  if (mode == OWQS_EOWQS) {
+    const double tol = ctx->prec == 1 ? 1e-8 : 1e-3;
+    const uint64_t nout = 1ull << no;
+    for (int64_t b = 0; b < nb; ++b) {
+      double n2 = 0;
+      for (uint64_t j = 0; j < 2 * nout; ++j) n2 += outputs[2 * nout * b + j] * outputs[2 * nout * b + j];
+      if (!(std::fabs(n2 - 1.0) <= tol))
+        return fail(ctx, OWQS_E_NOT_DETERMINISTIC, "EOWQS batch item " + std::to_string(b) + " norm^2 = " +
+                                                       std::to_string(n2) + ": the pattern is not deterministic");
+    }
   }
   return OWQS_OK;
 }
@@ -695,6 +785,21 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   return OWQS_OK;
 }
 
+owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const double* inputs,
+                           const uint64_t* seeds, const uint8_t* forced, double* outputs, uint8_t* outcomes,
+                           double* prob0) {
+  if (!ctx) return OWQS_E_ARG;
+  if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "run_batch before load_pattern");
+  if (n_batch <= 0 || !inputs || !outputs) return fail(ctx, OWQS_E_ARG, "empty batch or NULL buffers");
+  if (mode != OWQS_SAMPLED && mode != OWQS_FORCED && mode != OWQS_EOWQS) return fail(ctx, OWQS_E_ARG, "bad mode");
+  if (mode == OWQS_FORCED && ctx->hp.n_measure > 0 && !forced) return fail(ctx, OWQS_E_ARG, "forced outcomes missing");
+  if (mode == OWQS_EOWQS) {
+    owqs_status g = gflow_gate(ctx);
+    if (g != OWQS_OK) return g;
+  }
+  return run_batch_internal(ctx, mode, n_batch, inputs, seeds, forced, outputs, outcomes, prob0);
+}
+
 owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
@@ -785,13 +890,21 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
   if (s != OWQS_OK) return s;
   s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
-  for (uint64_t k = 0; k < cols; ++k) {
-    CU(launch_basis(ctx->shards[0].d_state, ctx->prec, cols, k, ctx->stream));
-    ctx->has_input = true;
-    s = run_internal(ctx, 1, OWQS_EOWQS, 0, nullptr);
+  if (((size_t)ctx->elem << ctx->cm[1].prog.phys_bits) <= (size_t)kBatchMaxBytes) {
+    // all 2^n_in basis columns as one batched launch (U is column-major: column k = state k)
+    std::vector<double> in(2 * cols * cols, 0.0);
+    for (uint64_t k = 0; k < cols; ++k) in[2 * (k * cols + k)] = 1.0;
+    s = run_batch_internal(ctx, OWQS_EOWQS, (int64_t)cols, in.data(), nullptr, nullptr, U, nullptr, nullptr);
     if (s != OWQS_OK) return s;
-    s = output_to_host(ctx, U + 2 * k * rows);
-    if (s != OWQS_OK) return s;
+  } else {
+    for (uint64_t k = 0; k < cols; ++k) {
+      CU(launch_basis(ctx->shards[0].d_state, ctx->prec, cols, k, ctx->stream));
+      ctx->has_input = true;
+      s = run_internal(ctx, 1, OWQS_EOWQS, 0, nullptr);
+      if (s != OWQS_OK) return s;
+      s = output_to_host(ctx, U + 2 * k * rows);
+      if (s != OWQS_OK) return s;
+    }
   }
   if (max_unitarity_err) {
     double worst = 0;

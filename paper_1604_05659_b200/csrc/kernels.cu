@@ -172,13 +172,13 @@ struct PassShared {
   int last;
 };
 
-__device__ void pass_prologue(const StepDesc& d, const DevPtrs& p, PassShared& sh) {
+__device__ void pass_prologue(const StepDesc& d, const DevPtrs& p, PassShared& sh, bool record_all = false) {
   if (threadIdx.x == 0) {
     LocalOutcomes loc;
     loc.n = 0;
     int bi = 0;
     double scale = 1.0;
-    const bool record = blockIdx.x == 0;
+    const bool record = record_all || blockIdx.x == 0;
     for (int i = 0; i < d.n_ops; ++i) {
       const Op& op = d.ops[i];
       if (op.type == OP_BFLY) {
@@ -756,17 +756,14 @@ __global__ void __launch_bounds__(256, (PassBounds<KHI, MINB>::min_blocks)) pass
 // ------------------------------------------------------------------------------------------------
 // Small-width pass (w <= 12): one CTA, whole state in shared memory, ops applied in sequence.
 // ------------------------------------------------------------------------------------------------
+struct PermTab {
+  int8_t slot[64];
+};
+
+// ops of a pass on a state held in shared memory (general 2x2 coefficients, absorbed CZ signs)
 template <typename T>
-__global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const DevPtrs p) {
-  typedef typename VT<T>::C C;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  C* s = reinterpret_cast<C*>(smem_raw);
-  __shared__ PassShared sh;
-  pass_prologue(d, p, sh);
+__device__ void smem_apply_ops(const StepDesc& d, const DevPtrs& p, typename VT<T>::C* s, const PassShared& sh) {
   const int n = 1 << d.width;
-  C* st = reinterpret_cast<C*>(p.state);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = st[i];
-  __syncthreads();
   for (int k = 0; k < d.n_ops; ++k) {
     const Op op = d.ops[k];
     if (!sh.cond[k] || op.type == OP_FLUSH) continue;
@@ -805,12 +802,16 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
     }
     __syncthreads();
   }
-  double acc[4] = {0, 0, 0, 0};
-  if (d.red_kind == RED_NORM) {
+}
+
+// per-thread partials of the step's reduction over a shared-memory state
+template <typename T>
+__device__ void smem_reduce(int red_kind, int r, int width, const typename VT<T>::C* s, double (&acc)[4]) {
+  const int n = 1 << width;
+  if (red_kind == RED_NORM) {
     for (int i = threadIdx.x; i < n; i += blockDim.x)
       acc[0] += (double)s[i].x * s[i].x + (double)s[i].y * s[i].y;
-  } else if (d.red_kind == RED_RHO) {
-    const int r = d.red_slot;
+  } else if (red_kind == RED_RHO) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
       double nn = (double)s[i].x * s[i].x + (double)s[i].y * s[i].y;
       if ((i >> r) & 1) {
@@ -824,10 +825,144 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
       }
     }
   }
+}
+
+// block-level sum of 4 doubles into out[4] (shared), fixed order
+__device__ void block_sum4(double (&acc)[4], PassShared& sh, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(FULLMASK, acc[k], o);
+  __syncthreads();
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) sh.red[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int k = 0; k < 4; ++k) {
+      double t = 0;
+      for (int w = 0; w < nw; ++w) t += sh.red[w][k];
+      out[k] = t;
+    }
+  __syncthreads();
+}
+
+// ------------------------------------------------------------------------------------------------
+// Small-width pass (w <= 12): one CTA, whole state in shared memory, ops applied in sequence.
+// ------------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const DevPtrs p) {
+  typedef typename VT<T>::C C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  __shared__ PassShared sh;
+  pass_prologue(d, p, sh);
+  const int n = 1 << d.width;
+  C* st = reinterpret_cast<C*>(p.state);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s[i] = st[i];
+  __syncthreads();
+  smem_apply_ops<T>(d, p, s, sh);
+  double acc[4] = {0, 0, 0, 0};
+  smem_reduce<T>(d.red_kind, d.red_slot, d.width, s, acc);
   if (d.n_ops > 0)
     for (int i = threadIdx.x; i < n; i += blockDim.x) st[i] = s[i];
   if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
   else if (d.red_kind == RED_RHO) reduce_finish<4>(acc, p, sh);
+}
+
+// ------------------------------------------------------------------------------------------------
+// Batched small-width replicas: one CTA runs the WHOLE step program on one
+// state held in shared memory; the grid walks a batch of independent inputs (config 1's 64
+// inputs, recognition's basis columns, seed sweeps). Per-state outcomes / prob0 / run params.
+// ------------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) batch_kernel(const StepDesc* steps, int n_steps, DevPtrs base, int K,
+                                                    int n_batch, const double2* in, double2* out, int n_in,
+                                                    int n_out, PermTab tab) {
+  typedef typename VT<T>::C C;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  __shared__ PassShared sh;
+  __shared__ double red[4];
+  const T r2 = (T)0.70710678118654752440;
+  for (int b = blockIdx.x; b < n_batch; b += gridDim.x) {
+    DevPtrs p = base;
+    p.outcome += (size_t)b * K;
+    p.prob0 += (size_t)b * K;
+    p.forced += (size_t)b * K;
+    p.run += b;
+    p.err += b;
+    p.red_result = red;
+    const int nin = 1 << n_in;
+    for (int i = threadIdx.x; i < nin; i += blockDim.x) {
+      double2 v = in[(size_t)b * nin + i];
+      s[i] = make_c<T>((T)v.x, (T)v.y);
+    }
+    __syncthreads();
+    for (int t = 0; t < n_steps; ++t) {
+      const StepDesc& d = steps[t];
+      double acc[4] = {0, 0, 0, 0};
+      if (d.kind == ST_PASS) {
+        pass_prologue(d, p, sh, true);
+        smem_apply_ops<T>(d, p, s, sh);
+        smem_reduce<T>(d.red_kind, d.red_slot, d.width, s, acc);
+      } else if (d.kind == ST_GROW) {
+        const int n = 1 << d.width;
+        for (int i = threadIdx.x; i < n; i += blockDim.x) {
+          C v = s[i];
+          v.x *= r2;
+          v.y *= r2;
+          s[i] = v;
+          s[i + n] = v;
+          acc[0] += 2.0 * ((double)v.x * v.x + (double)v.y * v.y);
+        }
+        __syncthreads();
+      } else if (d.kind == ST_SHRINK) {
+        if (threadIdx.x == 0) {
+          LocalOutcomes loc;
+          loc.n = 0;
+          decide(p, d.shrink_m, true, d.first_full_rho != 0, true, sh.coef[0], loc);
+        }
+        __syncthreads();
+        const T u0r = (T)sh.coef[0][0], u0i = (T)sh.coef[0][1], u1r = (T)sh.coef[0][2], u1i = (T)sh.coef[0][3];
+        const int w = d.width, bb = d.slot, top = w - 1;
+        if (bb == top) {
+          const int h = 1 << (w - 1);
+          for (int i = threadIdx.x; i < h; i += blockDim.x) {
+            C x0 = s[i], x1 = s[i + h];
+            T orr, oi;
+            cmul_add<T>(u0r, u0i, x0.x, x0.y, u1r, u1i, x1.x, x1.y, orr, oi);
+            s[i] = make_c<T>(orr, oi);
+            acc[0] += (double)orr * orr + (double)oi * oi;
+          }
+        } else {
+          const int nq = 1 << (w - 2);
+          for (int i = threadIdx.x; i < nq; i += blockDim.x) {
+            int rr = ((i >> bb) << (bb + 1)) | (i & ((1 << bb) - 1));
+            rr = ((rr >> top) << (top + 1)) | (rr & ((1 << top) - 1));
+            const int B = 1 << bb, TT = 1 << top;
+            C x00 = s[rr], x10 = s[rr | B], x01 = s[rr | TT], x11 = s[rr | B | TT];
+            T o0r, o0i, o1r, o1i;
+            cmul_add<T>(u0r, u0i, x00.x, x00.y, u1r, u1i, x10.x, x10.y, o0r, o0i);
+            cmul_add<T>(u0r, u0i, x01.x, x01.y, u1r, u1i, x11.x, x11.y, o1r, o1i);
+            s[rr] = make_c<T>(o0r, o0i);
+            s[rr | B] = make_c<T>(o1r, o1i);
+            acc[0] += (double)o0r * o0r + (double)o0i * o0i + (double)o1r * o1r + (double)o1i * o1i;
+          }
+        }
+        __syncthreads();
+      }
+      if (d.red_kind != RED_NONE) block_sum4(acc, sh, red);
+    }
+    const int nout = 1 << n_out;
+    for (int j = threadIdx.x; j < nout; j += blockDim.x) {
+      int src = 0;
+      for (int k = 0; k < n_out; ++k) src |= ((j >> k) & 1) << tab.slot[k];
+      C v = s[src];
+      out[(size_t)b * nout + j] = make_double2((double)v.x, (double)v.y);
+    }
+    __syncthreads();
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -902,9 +1037,6 @@ __global__ void __launch_bounds__(256) shrink_kernel(const StepDesc d, const Dev
 // I/O and helpers
 // ------------------------------------------------------------------------------------------------
 
-struct PermTab {
-  int8_t slot[64];
-};
 
 // shard scatter: out[perm(G)] = shard[L] with G = (rank << wl) | L (output bit k <- position slot[k])
 template <typename T, typename TO>
@@ -1175,6 +1307,24 @@ cudaError_t launch_scatter_out(const void* shard, int prec, void* out, int out_p
   else if (prec == 0) scatter_out_kernel<float, float><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
   else if (out_prec == 1) scatter_out_kernel<double, double><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
   else scatter_out_kernel<double, float><<<b, 256, 0, s>>>(shard, out, nbits, t, rank, wl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base, int K, int n_batch, const void* in,
+                         void* out, int n_in, int n_out, const int* out_slot, int phys, int prec, cudaStream_t s) {
+  PermTab t;
+  for (int k = 0; k < 64; ++k) t.slot[k] = (int8_t)(k < n_out ? out_slot[k] : 0);
+  const size_t sm = (size_t)(prec == 0 ? 8 : 16) << phys;
+  const unsigned grid = (unsigned)std::min(n_batch, 148 * 16);
+  if (prec == 0) {
+    cudaFuncSetAttribute(batch_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    batch_kernel<float><<<grid, 128, sm, s>>>(steps, n_steps, base, K, n_batch, (const double2*)in, (double2*)out,
+                                              n_in, n_out, t);
+  } else {
+    cudaFuncSetAttribute(batch_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    batch_kernel<double><<<grid, 128, sm, s>>>(steps, n_steps, base, K, n_batch, (const double2*)in, (double2*)out,
+                                               n_in, n_out, t);
+  }
   return cudaGetLastError();
 }
 

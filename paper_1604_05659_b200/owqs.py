@@ -139,6 +139,29 @@ class Simulator:
         self._check(st)
         return (out[:K], p0[:K]) if want else (None, None)
 
+    def run_batch(self, inputs: np.ndarray, mode: str = "sampled", seeds: Optional[Sequence[int]] = None,
+                  forced: Optional[np.ndarray] = None):
+        """Batched replicas: inputs [B, 2^n_in] -> (outputs [B, 2^n_out], outcomes [B, K], prob0 [B, K])."""
+        x = np.ascontiguousarray(inputs, dtype=np.complex128)
+        B = x.shape[0]
+        K = self.n_measure
+        out = np.empty((B, 2 ** self.n_out), dtype=np.complex128)
+        oc = np.zeros((B, max(K, 1)), dtype=np.uint8)
+        p0 = np.zeros((B, max(K, 1)), dtype=np.float64)
+        sd = None
+        if seeds is not None:
+            sa = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint64))
+            sd = sa.ctypes.data_as(C.POINTER(C.c_uint64))
+        fd = None
+        if forced is not None:
+            fa = np.ascontiguousarray(np.asarray(forced, dtype=np.uint8).reshape(B, K))
+            fd = fa.ctypes.data_as(C.POINTER(C.c_uint8))
+        self._check(self._lib.owqs_run_batch(self._h, MODES[mode], B, x.ctypes.data_as(C.POINTER(C.c_double)), sd, fd,
+                                             out.ctypes.data_as(C.POINTER(C.c_double)),
+                                             oc.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                             p0.ctypes.data_as(C.POINTER(C.c_double))))
+        return out, oc[:, :K], p0[:, :K]
+
     def get_output(self, out: Optional[np.ndarray] = None) -> Optional[np.ndarray]:
         """Full output (rank 0 / single rank / loopback); None on the other ranks (collective)."""
         root = self.n_ranks == 1 or self.rank == 0
