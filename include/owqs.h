@@ -90,6 +90,9 @@ typedef struct {
                                        record nodes in the graph); see owqs_launch_profile       */
 #define OWQS_FLAG_NO_GFLOW    0x40u /* EOWQS without the gflow pre-check of L372 (the final-norm
                                        check still reports OWQS_E_NOT_DETERMINISTIC)             */
+#define OWQS_FLAG_NO_JIT      0x80u /* run every pass with the ahead-of-time (op-interpreting) pass
+                                       kernel instead of the kernels generated for the pattern at
+                                       owqs_load_pattern (NVRTC, sm_100a)          */
 #define OWQS_FLAG_LOOPBACK    0x20u /* n_ranks > 1 on ONE device: the context holds every rank's
                                        shard and runs them one after the other (swaps and
                                        all-reduces by device copies); for testing the sharded path
@@ -119,7 +122,10 @@ typedef struct {
   double bytes_per_run;      /* analytic HBM bytes per owqs_run (all ranks' shards, this rank) */
   double last_run_ms;        /* device time of the last owqs_run (CUDA events)               */
   double schedule_ms;        /* host time spent in PROA + compile for the last mode          */
-  double reserved[4];
+  double jit_ms;             /* host time generating + NVRTC-compiling the pass kernels of
+                                both modes at load_pattern (0 when all came from the cache)    */
+  double n_jit_steps;        /* steps of the last mode's program run by generated kernels    */
+  double reserved[2];
 } owqs_stats_t;
 
 /* Create / destroy a context on cfg->device.

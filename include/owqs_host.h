@@ -54,6 +54,16 @@ owqs_status owqs_host_program(const owqs_host_plan* h, void* steps, void* mst, i
 /* gflow of the loaded pattern's open graph (see owqs_gflow in owqs.h): OWQS_OK or OWQS_E_NO_GFLOW;
  * layers[n_measure] by given-order ordinal (may be NULL), depth (may be NULL). */
 owqs_status owqs_host_gflow(const owqs_host_plan* h, int32_t* layers, int32_t* depth);
+/* Generated pass kernels: NVRTC-compile, for sm_100a, the kernel of every state pass
+ * of the compiled program that runs as a generated kernel (no device needed). n_kernels receives
+ * the number of distinct kernels, n_jit_steps the number of steps they cover, compile_ms the
+ * compile time (0 when every kernel came from the process cache). Any output may be NULL.
+ * OWQS_E_ARG with the NVRTC log in owqs_host_error on failure. */
+owqs_status owqs_host_jit(owqs_host_plan* h, int64_t* n_kernels, int64_t* n_jit_steps, double* compile_ms);
+/* Source of step `step`'s generated kernel (without the common prelude) into buf (capacity cap,
+ * NUL-terminated, truncated if short); returns its length in *len, 0 if the step is not generated.
+ * step = -1: the common prelude every generated translation unit starts with. */
+owqs_status owqs_host_jit_source(const owqs_host_plan* h, int64_t step, char* buf, int64_t cap, int64_t* len);
 const char* owqs_host_error(const owqs_host_plan* h);
 void owqs_host_free(owqs_host_plan* h);
 

@@ -20,8 +20,9 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernels.cu"]
-CPP_SOURCES = ["scheduler.cpp", "gflow.cpp", "capi.cpp", "host_api.cpp"]
-HEADERS = ["owqs_internal.h", "scheduler.h"]
+CPP_SOURCES = ["scheduler.cpp", "gflow.cpp", "jit.cpp", "capi.cpp", "host_api.cpp"]
+HEADERS = ["owqs_internal.h", "scheduler.h", "device_common.cuh", "jit.h"]
+PRELUDE = [("kPreludeInternal", "owqs_internal.h"), ("kPreludeCommon", "device_common.cuh")]
 
 
 def _run(cmd):
@@ -39,8 +40,26 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def _write_prelude():
+    """build/jit_prelude.inc: the device headers the generated pass kernels start with (raw strings)."""
+    out = []
+    for var, name in PRELUDE:
+        with open(os.path.join(CSRC, name)) as f:
+            text = "".join(l for l in f if not l.startswith("#pragma once"))
+        if ')OWQSPRE"' in text:
+            raise RuntimeError("raw-string delimiter inside " + name)
+        out.append(f'const char* {var} = R"OWQSPRE(\n{text})OWQSPRE";\n')
+    path = os.path.join(BUILD, "jit_prelude.inc")
+    data = "".join(out)
+    if not os.path.exists(path) or open(path).read() != data:
+        with open(path, "w") as f:
+            f.write(data)
+    return path
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
+    prelude = _write_prelude()
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(INCLUDE, "owqs.h"), os.path.join(INCLUDE, "owqs_host.h")]
     objs = []
     for src in CU_SOURCES:
@@ -58,13 +77,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
         s = os.path.join(CSRC, src)
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
-        if force or _stale(o, [s] + hdrs):
+        if force or _stale(o, [s, prelude] + hdrs):
             _run(["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function",
-                  "-I", INCLUDE, "-I", CSRC, "-I", os.path.join(CUDA_HOME, "include"), "-c", s, "-o", o])
+                  "-I", INCLUDE, "-I", CSRC, "-I", BUILD, "-I", os.path.join(CUDA_HOME, "include"), "-c", s, "-o", o])
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
         _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xlinker", "--no-undefined",
-              "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lpthread", "-ldl", "-lrt"])
+              "-L/usr/lib/x86_64-linux-gnu", "-lnccl",
+              "-L" + os.path.join(CUDA_HOME, "lib64"), "-lnvrtc", "-Xlinker", "-rpath=" + os.path.join(CUDA_HOME, "lib64"), "-lpthread", "-ldl", "-lrt"])
         shutil.move(tmp, LIB)
     return LIB
 

@@ -14,6 +14,7 @@ STATUS_NAMES = {0: "OWQS_OK", 1: "OWQS_E_ARG", 2: "OWQS_E_PATTERN", 3: "OWQS_E_N
 MODES = {"sampled": 0, "forced": 1, "eowqs": 2}
 FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE, FLAG_LOOPBACK = 1, 2, 4, 8, 16, 32
 FLAG_NO_GFLOW = 64
+FLAG_NO_JIT = 128
 KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
@@ -40,7 +41,8 @@ class owqs_stats_t(C.Structure):
                 ("phys_bits", C.c_int32), ("n_passes", C.c_int32), ("n_grow", C.c_int32),
                 ("n_shrink", C.c_int32), ("n_reduce", C.c_int32), ("n_launches", C.c_int32),
                 ("n_swaps", C.c_int32), ("bytes_per_run", C.c_double), ("last_run_ms", C.c_double),
-                ("schedule_ms", C.c_double), ("reserved", C.c_double * 4)]
+                ("schedule_ms", C.c_double), ("jit_ms", C.c_double), ("n_jit_steps", C.c_double),
+                ("reserved", C.c_double * 2)]
 
 
 assert C.sizeof(owqs_cmd) == 40
@@ -88,7 +90,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 # ---- include/owqs_host.h (host-only introspection; no CUDA calls) ------------------------------
 HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_gflow",
-                 "owqs_host_error", "owqs_host_free"]
+                 "owqs_host_jit", "owqs_host_jit_source", "owqs_host_error", "owqs_host_free"]
 KMAX_HI, MAX_OPS, MAX_BFLY = 4, 64, 24
 
 
@@ -129,6 +131,8 @@ def declare_host(lib: C.CDLL) -> C.CDLL:
         "owqs_host_program": (C.c_int, [h, C.c_void_p, C.c_void_p, P(C.c_int32), P(C.c_int32), P(C.c_int32),
                                         P(C.c_int32)]),
         "owqs_host_gflow": (C.c_int, [h, P(C.c_int32), P(C.c_int32)]),
+        "owqs_host_jit": (C.c_int, [h, P(C.c_int64), P(C.c_int64), P(C.c_double)]),
+        "owqs_host_jit_source": (C.c_int, [h, C.c_int64, C.c_char_p, C.c_int64, P(C.c_int64)]),
         "owqs_host_error": (C.c_char_p, [h]),
         "owqs_host_free": (None, [h]),
     }

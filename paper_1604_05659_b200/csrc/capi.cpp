@@ -10,6 +10,7 @@
 #include <string>
 #include <vector>
 
+#include "jit.h"
 #include "owqs.h"
 #include "scheduler.h"
 
@@ -33,6 +34,7 @@ cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_w
                              cudaStream_t s);
 cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
+cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s);
 cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base, int K, int n_batch, const void* in,
                          void* out, int n_in, int n_out, const int* out_slot, int phys, int prec, cudaStream_t s);
 }  // namespace owqs
@@ -49,6 +51,14 @@ struct CompiledMode {
   StepDesc* d_steps = nullptr;  // device copy of the program (batched replicas)
   cudaGraphExec_t gexec = nullptr;
   double schedule_ms = 0;
+  // generated pass kernels (jit.h): per step kernel name ("" = ahead-of-time kernel), the cubins,
+  // and once loaded on the device the kernel handles and their grid caps
+  std::vector<std::string> jit_name;
+  std::vector<JitModule> jit_mods;
+  std::vector<cudaLibrary_t> jit_libs;
+  std::vector<cudaKernel_t> jit_fn;
+  std::vector<int> jit_blocks;
+  int n_jit = 0;
 };
 // one rank's part of the state and its reduction scratch
 struct Shard {
@@ -95,6 +105,7 @@ struct owqs_ctx {
   int last_cm = 0;
   std::vector<cudaEvent_t> prof_ev;  // OWQS_FLAG_PROFILE: event after every launch (+1 start)
   int prof_cm = -1;
+  double jit_ms = 0;
   int gflow_state = 0;  // 0 unknown, 1 has a gflow, -1 none (L372 pre-check, cached per pattern)
   std::string gflow_msg;
 
@@ -143,6 +154,7 @@ DevPtrs dev_ptrs(owqs_ctx* ctx, const CompiledMode& m, int i) {
 
 void free_mode(CompiledMode& m) {
   if (m.gexec) cudaGraphExecDestroy(m.gexec);
+  for (cudaLibrary_t l : m.jit_libs) cudaLibraryUnload(l);
   if (m.d_mst) cudaFree(m.d_mst);
   if (m.d_sig) cudaFree(m.d_sig);
   if (m.d_steps) cudaFree(m.d_steps);
@@ -171,6 +183,29 @@ owqs_status compile_modes(owqs_ctx* ctx) {
     if (!m.prog.error.empty()) return fail(ctx, OWQS_E_ARG, m.prog.error);
     m.schedule_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     m.valid = true;
+  }
+  // generated pass kernels of both modes, compiled together (one NVRTC batch, process cache)
+  ctx->jit_ms = 0;
+  if (!(ctx->cfg.flags & OWQS_FLAG_NO_JIT)) {
+    std::vector<std::string> names, srcs;
+    for (int i = 0; i < 2; ++i) {
+      CompiledMode& m = ctx->cm[i];
+      m.jit_name.assign(m.prog.steps.size(), std::string());
+      for (size_t k = 0; k < m.prog.steps.size(); ++k) {
+        if (!jit_eligible(m.prog.steps[k], ctx->prec)) continue;
+        std::string nm;
+        std::string src = jit_pass_source(m.prog.steps[k], ctx->prec, &nm);
+        if (src.empty()) return fail(ctx, OWQS_E_ARG, "pass kernel generation failed for step " + std::to_string(k));
+        m.jit_name[k] = nm;
+        ++m.n_jit;
+        names.push_back(nm);
+        srcs.push_back(src);
+      }
+    }
+    std::vector<JitModule> mods;
+    std::string e = jit_compile(names, srcs, mods, &ctx->jit_ms);
+    if (!e.empty()) return fail(ctx, OWQS_E_ARG, "pass kernel compilation (NVRTC, sm_100a) failed: " + e);
+    for (int i = 0; i < 2; ++i) ctx->cm[i].jit_mods = mods;  // each mode loads what it uses
   }
   if (ctx->n_global > 0 && ctx->cm[0].prog.phys_bits != ctx->cm[1].prog.phys_bits)
     return fail(ctx, OWQS_E_ARG, "multi-rank: OWQS and EOWQS programs differ in width");
@@ -223,6 +258,34 @@ owqs_status ensure_device(owqs_ctx* ctx) {
     if (!m.d_sig && !m.prog.sig_pool.empty()) {
       CU(cudaMalloc(&m.d_sig, m.prog.sig_pool.size() * sizeof(int32_t)));
       CU(cudaMemcpy(m.d_sig, m.prog.sig_pool.data(), m.prog.sig_pool.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
+    if (m.n_jit > 0 && m.jit_fn.empty()) {
+      std::vector<cudaKernel_t> fn(m.prog.steps.size(), nullptr);
+      std::vector<int> blocks(m.prog.steps.size(), 0);
+      int sms = 0;
+      CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->cfg.device));
+      for (const JitModule& jm : m.jit_mods) {
+        bool used = false;
+        for (const std::string& n : jm.names)
+          for (const std::string& want : m.jit_name) used = used || (n == want);
+        if (!used) continue;
+        cudaLibrary_t lib = nullptr;
+        CU(cudaLibraryLoadData(&lib, jm.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+        m.jit_libs.push_back(lib);
+        for (size_t k = 0; k < m.jit_name.size(); ++k) {
+          if (m.jit_name[k].empty() || fn[k]) continue;
+          if (std::find(jm.names.begin(), jm.names.end(), m.jit_name[k]) == jm.names.end()) continue;
+          CU(cudaLibraryGetKernel(&fn[k], lib, m.jit_name[k].c_str()));
+          int nb = 0;
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], 256, 0));
+          blocks[k] = std::max(1, nb) * sms;
+        }
+      }
+      for (size_t k = 0; k < m.jit_name.size(); ++k)
+        if (!m.jit_name[k].empty() && !fn[k])
+          return fail(ctx, OWQS_E_CUDA, "generated kernel " + m.jit_name[k] + " missing from its cubin");
+      m.jit_fn = fn;
+      m.jit_blocks = blocks;
     }
   }
   return OWQS_OK;
@@ -301,8 +364,12 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
         owqs_status st = do_swap(ctx, s);
         if (st != OWQS_OK) return st;
       } else {
-        for (size_t r = 0; r < ctx->shards.size(); ++r)
-          CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
+        for (size_t r = 0; r < ctx->shards.size(); ++r) {
+          if (!m.jit_fn.empty() && m.jit_fn[i])
+            CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
+          else
+            CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
+        }
         if (s.red_kind != RED_NONE) {
           owqs_status st = allreduce_red(ctx);
           if (st != OWQS_OK) return st;
@@ -657,6 +724,8 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
   ctx->stats.n_launches = (int32_t)pr.steps.size();
   ctx->stats.bytes_per_run = pr.bytes_per_run(ctx->elem);
   ctx->stats.schedule_ms = ctx->cm[0].schedule_ms;
+  ctx->stats.jit_ms = ctx->jit_ms;
+  ctx->stats.n_jit_steps = ctx->cm[0].n_jit;
   if (pr.phys_bits - ctx->n_global > 40) return fail(ctx, OWQS_E_NOMEM, "shard width above 40 bits");
   ctx->loaded = true;
   return OWQS_OK;
@@ -773,6 +842,8 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   ctx->stats.n_launches = (int32_t)pr.steps.size();
   ctx->stats.bytes_per_run = pr.bytes_per_run(ctx->elem);
   ctx->stats.schedule_ms = ctx->cm[cmi].schedule_ms;
+  ctx->stats.jit_ms = ctx->jit_ms;
+  ctx->stats.n_jit_steps = ctx->cm[cmi].n_jit;
   ctx->stats.phys_bits = pr.phys_bits;
   if (mode == OWQS_EOWQS) {
     double red[4];

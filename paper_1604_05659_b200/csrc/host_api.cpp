@@ -5,6 +5,7 @@
 #include <string>
 
 #include "owqs_host.h"
+#include "jit.h"
 #include "scheduler.h"
 
 using namespace owqs;
@@ -103,6 +104,52 @@ owqs_status owqs_host_gflow(const owqs_host_plan* h, int32_t* layers, int32_t* d
   }
   if (depth) *depth = d;
   return e.empty() ? OWQS_OK : OWQS_E_NO_GFLOW;
+}
+
+owqs_status owqs_host_jit(owqs_host_plan* h, int64_t* n_kernels, int64_t* n_jit_steps, double* compile_ms) {
+  if (!h) return OWQS_E_ARG;
+  const int prec = h->elem == 8 ? 0 : 1;
+  std::vector<std::string> names, srcs;
+  for (const StepDesc& d : h->prog.steps) {
+    if (!jit_eligible(d, prec)) continue;
+    std::string nm;
+    std::string src = jit_pass_source(d, prec, &nm);
+    if (src.empty()) {
+      h->err = "pass kernel generation failed";
+      return OWQS_E_ARG;
+    }
+    names.push_back(nm);
+    srcs.push_back(src);
+  }
+  std::vector<JitModule> mods;
+  double ms = 0;
+  std::string e = jit_compile(names, srcs, mods, &ms);
+  if (!e.empty()) {
+    h->err = e;
+    return OWQS_E_ARG;
+  }
+  int64_t nk = 0;
+  for (auto& m : mods) nk += (int64_t)m.names.size();
+  if (n_kernels) *n_kernels = nk;
+  if (n_jit_steps) *n_jit_steps = (int64_t)names.size();
+  if (compile_ms) *compile_ms = ms;
+  return OWQS_OK;
+}
+
+owqs_status owqs_host_jit_source(const owqs_host_plan* h, int64_t step, char* buf, int64_t cap, int64_t* len) {
+  if (!h || step < -1 || step >= (int64_t)h->prog.steps.size()) return OWQS_E_ARG;
+  const int prec = h->elem == 8 ? 0 : 1;
+  std::string src;
+  if (step == -1)
+    src = jit_prelude();
+  else if (jit_eligible(h->prog.steps[step], prec)) src = jit_pass_source(h->prog.steps[step], prec, nullptr);
+  if (len) *len = (int64_t)src.size();
+  if (buf && cap > 0) {
+    const size_t n = std::min<size_t>((size_t)cap - 1, src.size());
+    memcpy(buf, src.data(), n);
+    buf[n] = 0;
+  }
+  return OWQS_OK;
 }
 
 const char* owqs_host_error(const owqs_host_plan* h) { return h ? h->err.c_str() : "NULL handle"; }

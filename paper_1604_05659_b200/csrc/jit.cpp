@@ -1,0 +1,675 @@
+// Load-time generated pass kernels (see jit.h and DESIGN.md §5).
+//
+// A pass of the compiled program reads every amplitude of the (shard) state once, applies the
+// pass's ops in registers and writes it back once (2S bytes, the algorithmic minimum per pass).
+// The ahead-of-time pass kernel interprets the op list at run time; these kernels instead bake
+// the op list into straight-line code, so that
+//   * complex64 butterflies run on packed fp32x2 arithmetic (FFMA2 / FMUL2 / FADD2 on sm_100a):
+//     y = a x1 (FMUL2 + FFMA2 with the swapped-operand modifier), x0 +- y (FADD2) = 2 instructions
+//     per amplitude for a butterfly on a register slot;
+//   * an unconditional X on a register slot is a compile-time renaming (no instruction);
+//   * the CZ sign of an absorbed E is a compile-time add/sub swap when its slot is a register bit,
+//     a per-thread coefficient sign when it is a lane, group-base or rank bit;
+//   * no register reconciliation at op-dispatch merge points (there are none).
+// Layout per warp unit (identical to the AOT kernel, so both agree on every index): a warp moves a
+// 512 B contiguous segment per vector (complex64: float4 = 2 amplitudes per lane, slot 0 in the
+// vector, slots 1..5 on lane bits; complex128: double2, slots 0..4 on lane bits); every thread
+// holds the 2^KHI segments that differ in the pass's group slots, UNR units per loop trip.
+#include "jit.h"
+
+#include <cuda_runtime.h>
+#include <nvrtc.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <chrono>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <thread>
+#include <unordered_map>
+
+namespace owqs {
+
+namespace {
+#include "jit_prelude.inc"  // kPreludeInternal (owqs_internal.h), kPreludeCommon (device_common.cuh)
+
+// Device helpers used only by the generated kernels: packed fp32x2 arithmetic (PTX ISA f32x2,
+// sm_100a) on a complex64 amplitude held as one 64-bit register pair (re = low, im = high).
+const char* kHelpers = R"OWQS(
+typedef unsigned long long u64;
+#define OWQS_SIGN2 0x8000000080000000ull
+static __device__ __forceinline__ u64 pk(float a, float b) { u64 r; asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
+static __device__ __forceinline__ float lo(u64 r) { float a, b; asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); return a; }
+static __device__ __forceinline__ float hi(u64 r) { float a, b; asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); return b; }
+static __device__ __forceinline__ u64 swp(u64 x) { return pk(hi(x), lo(x)); }
+static __device__ __forceinline__ u64 bc(float a) { return pk(a, a); }
+static __device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 r; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
+static __device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 r; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+static __device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+static __device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+static __device__ __forceinline__ u64 shfl2(u64 x, int m) { return pk(__shfl_xor_sync(0xffffffffu, lo(x), m), __shfl_xor_sync(0xffffffffu, hi(x), m)); }
+static __device__ __forceinline__ u64 flip2(u64 x, unsigned f) { return x ^ (((u64)f << 63) | ((u64)f << 31)); }
+static __device__ __forceinline__ double fld(double x, unsigned f) { return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)f << 63)); }
+)OWQS";
+
+// FNV-1a 64
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+std::string hex64(uint64_t v) {
+  char b[17];
+  snprintf(b, sizeof b, "%016llx", (unsigned long long)v);
+  return b;
+}
+
+enum SlotKind { SK_ELEM, SK_LANE, SK_GROUP, SK_BASE, SK_RANK };
+
+struct Gen {
+  const StepDesc& d;
+  const int prec, SB, EPV, KHI, G, UNR, NV, P;
+  std::ostringstream o;
+  std::vector<int> perm;  // logical register position -> variable id
+  struct Pend {
+    int a, b, idx;
+    bool cond;
+  };
+  std::vector<Pend> pend;
+
+  Gen(const StepDesc& dd, int pr)
+      : d(dd), prec(pr), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1), KHI(dd.nb_hi), G(1 << dd.nb_hi),
+        UNR(jit_unr_of(dd.nb_hi)), NV(UNR << dd.nb_hi), P((UNR << dd.nb_hi) * (pr == 0 ? 2 : 1)) {
+    for (int p = 0; p < P; ++p) perm.push_back(p);
+  }
+
+  int kind(int s, int* bit) const {
+    if (s >= d.width) {
+      *bit = s - d.width;
+      return SK_RANK;
+    }
+    if (EPV == 2 && s == 0) {
+      *bit = 0;
+      return SK_ELEM;
+    }
+    if (s < SB) {
+      *bit = s - (EPV == 2 ? 1 : 0);
+      return SK_LANE;
+    }
+    for (int j = 0; j < KHI; ++j)
+      if (d.bhi[j] == s) {
+        *bit = j;
+        return SK_GROUP;
+      }
+    *bit = s - SB;
+    return SK_BASE;
+  }
+  bool is_reg(int s) const {
+    int b;
+    int k = kind(s, &b);
+    return k == SK_ELEM || k == SK_GROUP;
+  }
+  // position-index bit that a register slot occupies
+  int pbit(int s) const {
+    int b;
+    int k = kind(s, &b);
+    return k == SK_ELEM ? 1 : (EPV << b);
+  }
+  int regval(int s, int p) const { return (p & pbit(s)) ? 1 : 0; }
+  int unit_of(int p) const { return p / (G * EPV); }
+
+  std::string X(int p) const { return "x" + std::to_string(perm[p]); }
+  std::string XR(int p) const { return "xr" + std::to_string(perm[p]); }
+  std::string XI(int p) const { return "xi" + std::to_string(perm[p]); }
+
+  // parity of the runtime (non-register) bits of slot mask m for unit u; "" if none
+  std::string rt_parity(uint64_t m, int u) const {
+    uint32_t L = 0, R = 0;
+    uint64_t B = 0;
+    for (int s = 0; s < 64; ++s) {
+      if (!((m >> s) & 1)) continue;
+      int b;
+      int k = kind(s, &b);
+      if (k == SK_LANE) L |= 1u << b;
+      if (k == SK_BASE) B |= 1ull << b;
+      if (k == SK_RANK) R |= 1u << b;
+    }
+    std::vector<std::string> t;
+    if (L) t.push_back("__popc(lane & " + std::to_string(L) + "u)");
+    if (B) t.push_back("__popcll(gb" + std::to_string(u) + " & " + std::to_string(B) + "ull)");
+    if (R) t.push_back("__popc(rk & " + std::to_string(R) + "u)");
+    if (t.empty()) return "";
+    std::string e = "((";
+    for (size_t i = 0; i < t.size(); ++i) e += (i ? " + " : "") + t[i];
+    return e + ") & 1u)";
+  }
+  // static parity of the register bits of mask m at position p
+  int st_parity(uint64_t m, int p) const {
+    int r = 0;
+    for (int s = 0; s < 64; ++s)
+      if (((m >> s) & 1) && is_reg(s)) r ^= regval(s, p);
+    return r;
+  }
+  // runtime value (0/1) of bit s for unit u (s not a register slot)
+  std::string rt_bit(int s, int u) const {
+    int b;
+    int k = kind(s, &b);
+    if (k == SK_LANE) return "((unsigned)(lane >> " + std::to_string(b) + ") & 1u)";
+    if (k == SK_BASE) return "((unsigned)(gb" + std::to_string(u) + " >> " + std::to_string(b) + ") & 1u)";
+    return "((rk >> " + std::to_string(b) + ") & 1u)";
+  }
+
+  void bfly(int i, int bi) {
+    const Op& op = d.ops[i];
+    const int a = op.a;
+    const uint64_t am = d.absorb[bi];
+    int lb;
+    const int ka = kind(a, &lb);
+    o << "    {  // op " << i << ": butterfly " << bi << " on slot " << a << "\n";
+    if (prec == 0)
+      o << "      const float ar = s_ar[" << bi << "]; const u64 cB = s_B[" << bi << "];\n";
+    else
+      o << "      const double ar = s_ar[" << bi << "], ai = s_ai[" << bi << "];\n";
+    // coefficient with the runtime part of the absorbed-CZ sign, per unit
+    for (int u = 0; u < UNR; ++u) {
+      std::string t = rt_parity(am, u);
+      if (t.empty()) {
+        if (prec == 0)
+          o << "      const float ar" << u << " = ar; const u64 B" << u << " = cB;\n";
+        else
+          o << "      const double ar" << u << " = ar, ai" << u << " = ai;\n";
+      } else {
+        o << "      const unsigned t" << u << " = " << t << ";\n";
+        if (prec == 0)
+          o << "      const float ar" << u << " = t" << u << " ? -ar : ar; const u64 B" << u << " = t" << u
+            << " ? (cB ^ OWQS_SIGN2) : cB;\n";
+        else
+          o << "      const double ar" << u << " = t" << u << " ? -ar : ar, ai" << u << " = t" << u << " ? -ai : ai;\n";
+      }
+    }
+    if (ka == SK_ELEM || ka == SK_GROUP) {
+      const int pb = pbit(a);
+      for (int p = 0; p < P; ++p) {
+        if (p & pb) continue;
+        const int p1 = p | pb, u = unit_of(p);
+        const int s = st_parity(am, p);
+        if (prec == 0) {
+          o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
+            << ")); const u64 t = " << X(p) << "; " << X(p) << " = " << (s ? "sub2" : "add2") << "(t, y); " << X(p1)
+            << " = " << (s ? "add2" : "sub2") << "(t, y); }\n";
+        } else {
+          const std::string u_ = std::to_string(u);
+          o << "      { const double yr = ar" << u_ << " * " << XR(p1) << " - ai" << u_ << " * " << XI(p1)
+            << ", yi = ar" << u_ << " * " << XI(p1) << " + ai" << u_ << " * " << XR(p1) << "; const double tr = "
+            << XR(p) << ", ti = " << XI(p) << "; " << XR(p) << " = tr " << (s ? "-" : "+") << " yr; " << XI(p)
+            << " = ti " << (s ? "-" : "+") << " yi; " << XR(p1) << " = tr " << (s ? "+" : "-") << " yr; "
+            << XI(p1) << " = ti " << (s ? "+" : "-") << " yi; }\n";
+        }
+      }
+    } else if (ka == SK_LANE) {
+      // lower lane holds x0, upper x1. Each lane sends y = c x (c = 1 lower, +-a upper) and keeps
+      // out = r + sg y (sg = +1 lower, -1 upper): lower x0 + a x1, upper x0 - a x1.
+      const int LM = 1 << lb;
+      o << "      const bool h = (lane >> " << lb << ") & 1; const " << (prec == 0 ? "float" : "double")
+        << " sg = h ? -1 : 1;\n";
+      bool need[8][2] = {};
+      for (int p = 0; p < P; ++p) need[unit_of(p)][st_parity(am, p)] = true;
+      for (int u = 0; u < UNR; ++u)
+        for (int s = 0; s < 2; ++s) {
+          if (!need[u][s]) continue;
+          if (prec == 0)
+            o << "      const float c" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : 1.f; const u64 cB"
+              << u << s << " = h ? (B" << u << (s ? " ^ OWQS_SIGN2" : "") << ") : 0ull;\n";
+          else
+            o << "      const double cr" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : 1.0, ci" << u << s
+              << " = h ? " << (s ? "-" : "") << "ai" << u << " : 0.0;\n";
+        }
+      for (int p = 0; p < P; ++p) {
+        const int u = unit_of(p), s = st_parity(am, p);
+        if (prec == 0) {
+          o << "      { const u64 y = fma2(cB" << u << s << ", swp(" << X(p) << "), mul2(bc(c" << u << s << "), " << X(p)
+            << ")); " << X(p) << " = fma2(bc(sg), y, shfl2(y, " << LM << ")); }\n";
+        } else {
+          const std::string c = std::to_string(u) + std::to_string(s);
+          o << "      { const double yr = cr" << c << " * " << XR(p) << " - ci" << c << " * " << XI(p) << ", yi = cr" << c
+            << " * " << XI(p) << " + ci" << c << " * " << XR(p) << "; " << XR(p) << " = __shfl_xor_sync(0xffffffffu, yr, "
+            << LM << ") + sg * yr; " << XI(p) << " = __shfl_xor_sync(0xffffffffu, yi, " << LM << ") + sg * yi; }\n";
+        }
+      }
+    } else {
+      error = "butterfly on a slot outside the pass";
+    }
+    o << "    }\n";
+  }
+
+  void xop(int i) {
+    const Op& op = d.ops[i];
+    const int a = op.a;
+    int lb;
+    const int ka = kind(a, &lb);
+    o << "    // op " << i << ": X on slot " << a << (op.cond ? " (conditional)" : "") << "\n";
+    if (ka == SK_ELEM || ka == SK_GROUP) {
+      const int pb = pbit(a);
+      if (!op.cond) {  // compile-time renaming
+        for (int p = 0; p < P; ++p)
+          if (!(p & pb)) std::swap(perm[p], perm[p | pb]);
+        return;
+      }
+      o << "    if (sh.cond[" << i << "]) {\n";
+      for (int p = 0; p < P; ++p) {
+        if (p & pb) continue;
+        const int p1 = p | pb;
+        if (prec == 0)
+          o << "      { const u64 t = " << X(p) << "; " << X(p) << " = " << X(p1) << "; " << X(p1) << " = t; }\n";
+        else
+          o << "      { const double tr = " << XR(p) << ", ti = " << XI(p) << "; " << XR(p) << " = " << XR(p1) << "; "
+            << XI(p) << " = " << XI(p1) << "; " << XR(p1) << " = tr; " << XI(p1) << " = ti; }\n";
+      }
+      o << "    }\n";
+    } else if (ka == SK_LANE) {
+      const std::string lm = op.cond ? "(sh.cond[" + std::to_string(i) + "] ? " + std::to_string(1 << lb) + " : 0)"
+                                     : std::to_string(1 << lb);
+      o << "    { const int lm = " << lm << ";\n";
+      for (int p = 0; p < P; ++p) {
+        if (prec == 0)
+          o << "      " << X(p) << " = shfl2(" << X(p) << ", lm);\n";
+        else
+          o << "      " << XR(p) << " = __shfl_xor_sync(0xffffffffu, " << XR(p) << ", lm); " << XI(p)
+            << " = __shfl_xor_sync(0xffffffffu, " << XI(p) << ", lm);\n";
+      }
+      o << "    }\n";
+    } else {
+      error = "X on a slot outside the pass";
+    }
+  }
+
+  // apply the pending diagonal sign flips (E = CZ, Z^s): sign of an amplitude = XOR over pending
+  // ops whose register bits are all 1 there of (cond AND the op's runtime bits)
+  void flush() {
+    if (pend.empty()) return;
+    o << "    {  // flush " << pend.size() << " pending diagonal(s)\n";
+    struct Term {
+      std::vector<int> regs;      // register slots of the op
+      bool stat1;                 // runtime factor is the constant 1
+      std::vector<std::string> rt;  // per unit: runtime variable name
+    };
+    std::vector<Term> terms;
+    for (size_t k = 0; k < pend.size(); ++k) {
+      const Pend& pe = pend[k];
+      Term t;
+      std::vector<int> slots = {pe.a};
+      if (pe.b != pe.a) slots.push_back(pe.b);
+      std::vector<int> rts;
+      for (int s : slots) (is_reg(s) ? t.regs : rts).push_back(s);
+      t.stat1 = rts.empty() && !pe.cond;
+      if (!t.stat1)
+        for (int u = 0; u < UNR; ++u) {
+          std::string nm = "f" + std::to_string(k) + "_" + std::to_string(u);
+          std::string e = pe.cond ? "(unsigned)sh.cond[" + std::to_string(pe.idx) + "]" : "1u";
+          for (int s : rts) e += " & " + rt_bit(s, u);
+          o << "      const unsigned " << nm << " = " << e << ";\n";
+          t.rt.push_back(nm);
+        }
+      terms.push_back(t);
+    }
+    for (int p = 0; p < P; ++p) {
+      int stat = 0;
+      std::vector<std::string> dyn;
+      for (const Term& t : terms) {
+        bool on = true;
+        for (int s : t.regs) on = on && regval(s, p);
+        if (!on) continue;
+        if (t.stat1)
+          stat ^= 1;
+        else
+          dyn.push_back(t.rt[unit_of(p)]);
+      }
+      if (dyn.empty() && !stat) continue;
+      if (dyn.empty()) {
+        if (prec == 0)
+          o << "      " << X(p) << " ^= OWQS_SIGN2;\n";
+        else
+          o << "      " << XR(p) << " = -" << XR(p) << "; " << XI(p) << " = -" << XI(p) << ";\n";
+        continue;
+      }
+      std::string f = stat ? "1u" : "0u";
+      for (auto& s : dyn) f += " ^ " + s;
+      if (prec == 0)
+        o << "      " << X(p) << " = flip2(" << X(p) << ", " << f << ");\n";
+      else
+        o << "      { const unsigned f = " << f << "; " << XR(p) << " = fld(" << XR(p) << ", f); " << XI(p) << " = fld("
+          << XI(p) << ", f); }\n";
+    }
+    o << "    }\n";
+    pend.clear();
+  }
+
+  void reduce() {
+    if (d.red_kind == RED_NONE) return;
+    const char* T = prec == 0 ? "u64" : "double";
+    (void)T;
+    if (d.red_kind == RED_NORM) {
+      if (prec == 0) {
+        o << "    { u64 n0 = 0ull, n1 = 0ull;\n";
+        for (int p = 0; p < P; ++p) o << "      n" << (p & 1) << " = fma2(" << X(p) << ", " << X(p) << ", n" << (p & 1) << ");\n";
+        o << "      const u64 n = add2(n0, n1); acc0 += (double)lo(n) + (double)hi(n); }\n";
+      } else {
+        o << "    { double n0 = 0.0, n1 = 0.0;\n";
+        for (int p = 0; p < P; ++p)
+          o << "      n" << (p & 1) << " += " << XR(p) << " * " << XR(p) << " + " << XI(p) << " * " << XI(p) << ";\n";
+        o << "      acc0 += n0 + n1; }\n";
+      }
+      return;
+    }
+    // RED_RHO on slot r: n0 = sum |x|^2 over bit r = 0, n1 over bit r = 1, c = sum conj(x0) x1
+    const int r = d.red_slot;
+    int lb;
+    const int kr = kind(r, &lb);
+    if (kr == SK_ELEM || kr == SK_GROUP) {
+      const int pb = pbit(r);
+      if (prec == 0) {
+        o << "    { u64 n0 = 0ull, n1 = 0ull, cc = 0ull, cd = 0ull;\n";
+        for (int p = 0; p < P; ++p) {
+          if (p & pb) continue;
+          const int p1 = p | pb;
+          o << "      n0 = fma2(" << X(p) << ", " << X(p) << ", n0); n1 = fma2(" << X(p1) << ", " << X(p1)
+            << ", n1); cc = fma2(" << X(p) << ", " << X(p1) << ", cc); cd = fma2(" << X(p) << ", swp(" << X(p1)
+            << "), cd);\n";
+        }
+        o << "      acc0 += (double)lo(n0) + (double)hi(n0); acc1 += (double)lo(n1) + (double)hi(n1);\n"
+             "      acc2 += (double)lo(cc) + (double)hi(cc); acc3 += (double)lo(cd) - (double)hi(cd); }\n";
+      } else {
+        o << "    {\n";
+        for (int p = 0; p < P; ++p) {
+          if (p & pb) continue;
+          const int p1 = p | pb;
+          o << "      acc0 += " << XR(p) << " * " << XR(p) << " + " << XI(p) << " * " << XI(p) << "; acc1 += " << XR(p1)
+            << " * " << XR(p1) << " + " << XI(p1) << " * " << XI(p1) << "; acc2 += " << XR(p) << " * " << XR(p1)
+            << " + " << XI(p) << " * " << XI(p1) << "; acc3 += " << XR(p) << " * " << XI(p1) << " - " << XI(p)
+            << " * " << XR(p1) << ";\n";
+        }
+        o << "    }\n";
+      }
+    } else if (kr == SK_LANE) {
+      const int LM = 1 << lb;
+      if (prec == 0) {
+        o << "    { u64 nn = 0ull, cc = 0ull, cd = 0ull;\n";
+        for (int p = 0; p < P; ++p)
+          o << "      { const u64 q = shfl2(" << X(p) << ", " << LM << "); nn = fma2(" << X(p) << ", " << X(p)
+            << ", nn); cc = fma2(" << X(p) << ", q, cc); cd = fma2(" << X(p) << ", swp(q), cd); }\n";
+        o << "      const double nd = (double)lo(nn) + (double)hi(nn);\n"
+             "      if ((lane >> " << lb << ") & 1) { acc1 += nd; } else { acc0 += nd; acc2 += (double)lo(cc) + (double)hi(cc); acc3 += (double)lo(cd) - (double)hi(cd); } }\n";
+      } else {
+        o << "    { double nn = 0.0, cc = 0.0, cd = 0.0;\n";
+        for (int p = 0; p < P; ++p)
+          o << "      { const double qr = __shfl_xor_sync(0xffffffffu, " << XR(p) << ", " << LM
+            << "), qi = __shfl_xor_sync(0xffffffffu, " << XI(p) << ", " << LM << "); nn += " << XR(p) << " * " << XR(p)
+            << " + " << XI(p) << " * " << XI(p) << "; cc += " << XR(p) << " * qr + " << XI(p) << " * qi; cd += " << XR(p)
+            << " * qi - " << XI(p) << " * qr; }\n";
+        o << "      if ((lane >> " << lb << ") & 1) { acc1 += nn; } else { acc0 += nn; acc2 += cc; acc3 += cd; } }\n";
+      }
+    } else {
+      error = "reduction slot outside the pass";
+    }
+  }
+
+  std::string error;
+
+  std::string run() {
+    const int nbf = d.n_bfly;
+    const int red = d.red_kind;
+    const int nred = red == RED_NONE ? 0 : (red == RED_NORM ? 1 : 4);
+    const int minb = KHI <= 3 ? 3 : 2;
+    const int slack = d.width - SB - KHI - (UNR == 4 ? 2 : (UNR == 2 ? 1 : 0)) - 3;
+    const uint64_t nbu = 1ull << slack;
+    o << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p) {\n"
+      << "  using namespace owqs;\n"
+      << "  // width " << d.width << ", group slots";
+    for (int j = 0; j < KHI; ++j) o << " " << d.bhi[j];
+    o << ", " << d.n_ops << " ops, " << nbf << " butterflies, reduction " << red << "\n";
+    o << "  __shared__ PassShared sh;\n";
+    if (prec == 0)
+      o << "  __shared__ float s_ar[" << std::max(1, nbf) << "]; __shared__ u64 s_B[" << std::max(1, nbf) << "];\n";
+    else
+      o << "  __shared__ double s_ar[" << std::max(1, nbf) << "], s_ai[" << std::max(1, nbf) << "];\n";
+    o << "  pass_prologue(d, p, sh);\n";
+    if (nbf > 0) {
+      o << "  if (threadIdx.x < " << nbf << ") {\n";
+      if (prec == 0)
+        o << "    const float ai = (float)sh.ka[threadIdx.x][1]; s_ar[threadIdx.x] = (float)sh.ka[threadIdx.x][0]; s_B[threadIdx.x] = pk(-ai, ai);\n";
+      else
+        o << "    s_ar[threadIdx.x] = sh.ka[threadIdx.x][0]; s_ai[threadIdx.x] = sh.ka[threadIdx.x][1];\n";
+      o << "  }\n  __syncthreads();\n";
+    }
+    o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+      << "  const unsigned rk = p.rank; (void)rk;\n"
+      << "  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;\n";
+    if (nbf > 0) {
+      if (prec == 0)
+        o << "  const u64 scale = bc((float)sh.scale);\n";
+      else
+        o << "  const double scale = sh.scale;\n";
+    }
+    if (prec == 0)
+      o << "  float4* __restrict__ st = reinterpret_cast<float4*>(p.state);\n";
+    else
+      o << "  double2* __restrict__ st = reinterpret_cast<double2*>(p.state);\n";
+    o << "  for (unsigned long long ub = blockIdx.x; ub < " << nbu << "ull; ub += gridDim.x) {\n"
+      << "    const unsigned long long unit = ub * 8 + warp;\n";
+    for (int u = 0; u < UNR; ++u) {
+      o << "    unsigned long long gb" << u << " = unit * " << UNR << " + " << u << ";\n";
+      for (int j = 0; j < KHI; ++j) {
+        const int q = d.bhi[j] - SB;
+        o << "    gb" << u << " = ((gb" << u << " >> " << q << ") << " << (q + 1) << ") | (gb" << u << " & "
+          << ((1ull << q) - 1) << "ull);\n";
+      }
+    }
+    // loads
+    auto off = [&](int c) {
+      uint64_t s = 0;
+      for (int j = 0; j < KHI; ++j)
+        if ((c >> j) & 1) s |= 1ull << (d.bhi[j] - SB);
+      return s;
+    };
+    for (int u = 0; u < UNR; ++u)
+      for (int c = 0; c < G; ++c) {
+        const int v = u * G + c;
+        const std::string addr = "st + (((gb" + std::to_string(u) + " | " + std::to_string(off(c)) + "ull) << 5) + lane)";
+        if (prec == 0)
+          o << "    u64 x" << 2 * v << ", x" << 2 * v + 1 << "; { const float4 w = __ldcs(" << addr << "); x" << 2 * v
+            << " = pk(w.x, w.y); x" << 2 * v + 1 << " = pk(w.z, w.w); }\n";
+        else
+          o << "    double xr" << v << ", xi" << v << "; { const double2 w = __ldcs(" << addr << "); xr" << v
+            << " = w.x; xi" << v << " = w.y; }\n";
+      }
+    // ops
+    int bi = 0;
+    for (int i = 0; i < d.n_ops; ++i) {
+      const Op& op = d.ops[i];
+      switch (op.type) {
+        case OP_DIAG_E:
+        case OP_DIAG_Z:
+          pend.push_back({op.a, op.type == OP_DIAG_E ? op.b : op.a, i, op.cond != 0});
+          break;
+        case OP_FLUSH:
+          flush();
+          break;
+        case OP_X:
+          xop(i);
+          break;
+        case OP_BFLY:
+          bfly(i, bi++);
+          break;
+        default:
+          break;
+      }
+    }
+    flush();
+    if (nbf > 0) {
+      for (int p = 0; p < P; ++p) {
+        if (prec == 0)
+          o << "    " << X(p) << " = mul2(scale, " << X(p) << ");\n";
+        else
+          o << "    " << XR(p) << " *= scale; " << XI(p) << " *= scale;\n";
+      }
+    }
+    reduce();
+    if (d.n_ops > 0) {
+      for (int u = 0; u < UNR; ++u)
+        for (int c = 0; c < G; ++c) {
+          const int v = u * G + c;
+          const std::string addr = "st + (((gb" + std::to_string(u) + " | " + std::to_string(off(c)) + "ull) << 5) + lane)";
+          const int p0 = v * EPV;
+          if (prec == 0)
+            o << "    __stcs(" << addr << ", make_float4(lo(" << X(p0) << "), hi(" << X(p0) << "), lo(" << X(p0 + 1)
+              << "), hi(" << X(p0 + 1) << ")));\n";
+          else
+            o << "    __stcs(" << addr << ", make_double2(" << XR(p0) << ", " << XI(p0) << "));\n";
+        }
+    }
+    o << "  }\n";
+    if (nred > 0) o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n  reduce_finish<" << nred << ">(acc, p, sh);\n";
+    o << "}\n";
+    return o.str();
+  }
+};
+
+// ---- compile cache ------------------------------------------------------------------------------
+struct CacheEntry {
+  std::shared_ptr<JitModule> mod;
+};
+std::mutex g_mu;
+std::unordered_map<std::string, std::shared_ptr<JitModule>> g_cache;  // kernel name -> module
+
+std::string compile_tu(const std::string& src, std::vector<char>& cubin) {
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "owqs_pass_jit.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOWQS_JIT=1"};
+  r = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  std::string err;
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    if (n) nvrtcGetProgramLog(prog, &log[0]);
+    err = std::string("nvrtcCompileProgram: ") + nvrtcGetErrorString(r) + "\n" + log;
+  } else {
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    cubin.resize(n);
+    nvrtcGetCUBIN(prog, cubin.data());
+  }
+  nvrtcDestroyProgram(&prog);
+  return err;
+}
+
+}  // namespace
+
+bool jit_eligible(const StepDesc& d, int prec) {
+  if (d.kind != ST_PASS) return false;
+  const int SB = prec == 0 ? 6 : 5;
+  const int unr = jit_unr_of(d.nb_hi);
+  const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
+  return slack >= 0;
+}
+
+const std::string& jit_prelude() {
+  static const std::string s = std::string(kPreludeInternal) + "\n" + kPreludeCommon + "\n" + kHelpers;
+  return s;
+}
+
+std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
+  Gen g(d, prec);
+  std::string body = g.run();
+  if (!g.error.empty()) return "";
+  const std::string nm = "owqs_pass_" + std::string(prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
+  const std::string key = "OWQS_KNAME";
+  body.replace(body.find(key), key.size(), nm);
+  if (name) *name = nm;
+  return body;
+}
+
+std::string jit_compile(const std::vector<std::string>& names, const std::vector<std::string>& sources,
+                        std::vector<JitModule>& out, double* compile_ms) {
+  auto t0 = std::chrono::steady_clock::now();
+  out.clear();
+  // dedupe; split into cached / to compile
+  std::vector<int> todo;
+  std::map<std::string, int> seen;
+  std::vector<std::shared_ptr<JitModule>> mods;
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (size_t i = 0; i < names.size(); ++i) {
+      if (seen.count(names[i])) continue;
+      seen[names[i]] = (int)i;
+      auto it = g_cache.find(names[i]);
+      if (it != g_cache.end()) {
+        if (std::find(mods.begin(), mods.end(), it->second) == mods.end()) mods.push_back(it->second);
+      } else {
+        todo.push_back((int)i);
+      }
+    }
+  }
+  if (!todo.empty()) {
+    const int per_tu = 6;
+    const int n_tu = ((int)todo.size() + per_tu - 1) / per_tu;
+    std::vector<std::shared_ptr<JitModule>> fresh(n_tu);
+    std::vector<std::string> errs(n_tu);
+    int n_thr = (int)std::thread::hardware_concurrency();
+    n_thr = std::max(1, std::min(n_thr, std::min(n_tu, 32)));
+    std::mutex qm;
+    int next = 0;
+    auto worker = [&]() {
+      while (true) {
+        int k;
+        {
+          std::lock_guard<std::mutex> lk(qm);
+          if (next >= n_tu) return;
+          k = next++;
+        }
+        auto m = std::make_shared<JitModule>();
+        std::string src = jit_prelude();
+        for (int j = k * per_tu; j < std::min((int)todo.size(), (k + 1) * per_tu); ++j) {
+          src += "\n" + sources[todo[j]];
+          m->names.push_back(names[todo[j]]);
+        }
+        errs[k] = compile_tu(src, m->cubin);
+        fresh[k] = m;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t < n_thr; ++t) th.emplace_back(worker);
+    for (auto& t : th) t.join();
+    for (int k = 0; k < n_tu; ++k)
+      if (!errs[k].empty()) return errs[k];
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto& m : fresh) {
+      for (auto& n : m->names) g_cache[n] = m;
+      mods.push_back(m);
+    }
+  }
+  for (auto& m : mods) out.push_back(*m);
+  if (compile_ms) *compile_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  return "";
+}
+
+cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s) {
+  const int SB = prec == 0 ? 6 : 5;
+  const int unr = jit_unr_of(d.nb_hi);
+  const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
+  const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));
+  StepDesc dd = d;
+  DevPtrs pp = p;
+  void* args[] = {&dd, &pp};
+  return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(256), args, 0, s);
+}
+
+}  // namespace owqs

@@ -1,0 +1,43 @@
+// Load-time specialisation of the fused pass kernel (DESIGN.md §5 "generated pass kernels").
+//
+// Every state pass of a compiled program (StepDesc, ST_PASS) is turned into one straight-line
+// sm_100a kernel: the pass's slots, op order, absorbed-CZ masks, folded X renamings, reduction kind
+// and width are compile-time constants; only the measurement decisions (outcomes, Eq. 2 angles,
+// Eqs. 11-12 coefficients, signal conditions) stay runtime values, computed by the shared prologue
+// (device_common.cuh). NVRTC compiles the generated translation units for sm_100a at load_pattern
+// time (host only, no device needed); the cubins are loaded on the device with the runtime's
+// library API when the context first runs.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "owqs_internal.h"
+
+namespace owqs {
+
+// SB = warp-segment bits (6 complex64, 5 complex128). Same UNR rule as the AOT kernel.
+inline int jit_unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
+
+// True when the step runs as a generated pass kernel (ST_PASS wide enough for the 8-warp grid).
+bool jit_eligible(const StepDesc& d, int prec);
+
+// Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
+// a hash of the body (identical passes share one kernel).
+std::string jit_pass_source(const StepDesc& d, int prec, std::string* name);
+
+// The common prelude every generated translation unit starts with.
+const std::string& jit_prelude();
+
+struct JitModule {
+  std::vector<char> cubin;
+  std::vector<std::string> names;  // kernels in this cubin
+};
+
+// Compile the given kernel sources (deduplicated by name) into cubins for sm_100a. Results are
+// cached per process (keyed by the source text). Returns "" on success, else the NVRTC log.
+std::string jit_compile(const std::vector<std::string>& names, const std::vector<std::string>& sources,
+                        std::vector<JitModule>& out, double* compile_ms = nullptr);
+
+}  // namespace owqs

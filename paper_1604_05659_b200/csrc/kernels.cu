@@ -15,22 +15,9 @@
 #include <algorithm>
 
 #include "owqs_internal.h"
+#include "device_common.cuh"
 
 namespace owqs {
-
-#define FULLMASK 0xffffffffu
-
-__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
-  uint64_t z = x + 0x9E3779B97F4A7C15ull;
-  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-  return z ^ (z >> 31);
-}
-
-// Reading R-5: keyed uniform draw of the M with given-order ordinal `ord`.
-__device__ __forceinline__ double draw_uniform(uint64_t seed, int ord) {
-  return (double)(splitmix64(seed ^ splitmix64((uint64_t)(int64_t)ord)) >> 11) * 0x1.0p-53;
-}
 
 template <typename T> struct VT;
 template <> struct VT<float> {
@@ -71,185 +58,6 @@ __device__ __forceinline__ void vstore<float>(float4* p, const float (&re)[2], c
 template <>
 __device__ __forceinline__ void vstore<double>(double2* p, const double (&re)[2], const double (&im)[2]) {
   __stcs(p, make_double2(re[0], im[0]));
-}
-
-// ------------------------------------------------------------------------------------------------
-// Measurement decision (one thread). Eq. 2 angle, prob0 by Eq. 13 (structural or from rho),
-// outcome by Fig. 6 "rand(0,1) <= prob" / forced / EOWQS 0, coefficients of Eqs. 11-12.
-// ------------------------------------------------------------------------------------------------
-struct LocalOutcomes {
-  int n;
-  int ord[MAX_BFLY];
-  uint8_t out[MAX_BFLY];
-};
-
-__device__ int signal_parity(const DevPtrs& p, int off, int len, const LocalOutcomes& loc) {
-  int s = 0;
-  for (int i = 0; i < len; ++i) {
-    int o = p.sig_pool[off + i];
-    int v = -1;
-    for (int j = 0; j < loc.n; ++j)
-      if (loc.ord[j] == o) v = loc.out[j];
-    if (v < 0) v = p.outcome[o];
-    s ^= v;
-  }
-  return s & 1;
-}
-
-// Writes the 2x2 complex matrix (row-major re/im pairs) to coef[8]. For an elimination (reuse=0)
-// only row 0 is used. red: NORM -> red[0] = ||psi||^2; RHO -> (n0, n1, Re c, Im c).
-__device__ void decide(const DevPtrs& p, int m, bool use_red, bool full, bool record, double* coef,
-                       LocalOutcomes& loc) {
-  const MStatic ms = p.mst[m];
-  const int mode = p.run->mode;
-  int s = 0, t = 0;
-  if (mode != 2) {
-    s = signal_parity(p, ms.s_off, ms.s_len, loc);
-    t = signal_parity(p, ms.t_off, ms.t_len, loc);
-  }
-  const double PI = 3.141592653589793238462643383279502884;
-  double theta = (s ? -ms.alpha : ms.alpha) + (t ? PI : 0.0);  // Eq. 2
-  double sn, cs;
-  sincos(theta, &sn, &cs);
-  const double er = cs, ei = -sn;  // e^{-i theta}
-  int outc = 0;
-  double pS = 0.5, P0 = -1.0;
-  if (mode != 2) {
-    double P1;
-    if (full) {  // prob0 = 1/2 sum |x0 + e^{-i theta} x1|^2 = (n0 + n1)/2 + Re(e^{-i theta} c)
-      const double* r = p.red_result;
-      double tot = r[0] + r[1];
-      P0 = 0.5 * tot + (er * r[2] - ei * r[3]);
-      P0 = fmin(fmax(P0, 0.0), tot);
-      P1 = tot - P0;
-    } else {  // a fresh |+> neighbour dephases the qubit: prob0 = ||psi||^2 / 2 (R-13)
-      double nrm = use_red ? p.red_result[0] : 1.0;
-      P0 = 0.5 * nrm;
-      P1 = 0.5 * nrm;
-    }
-    if (mode == 0) {
-      outc = draw_uniform(p.run->seed, ms.ord) <= P0 ? 0 : 1;
-    } else {
-      outc = p.forced[ms.ord] & 1;
-    }
-    pS = outc ? P1 : P0;
-    if (pS < 1e-12) {
-      if (record) atomicExch(p.err, 1);
-      pS = 1.0;
-    }
-  }
-  const double sg = outc ? -1.0 : 1.0;
-  if (ms.reuse) {
-    // N_o E_io M_i: out[y] = (x0 + (-1)^{s+y} e^{-i theta} x1) / (2 sqrt(p_s)); EOWQS: sqrt2 * 1/2
-    double k = (mode == 2) ? 0.70710678118654752440 : 0.5 / sqrt(pS);
-    coef[0] = k; coef[1] = 0; coef[2] = k * sg * er; coef[3] = k * sg * ei;
-    coef[4] = k; coef[5] = 0; coef[6] = -k * sg * er; coef[7] = -k * sg * ei;
-  } else {
-    // M_s of Eqs. 11-12: out = (x0 + (-1)^s e^{-i theta} x1) / (sqrt2 sqrt(p_s)); EOWQS: * sqrt2
-    double k = (mode == 2) ? 1.0 : 1.0 / sqrt(2.0 * pS);
-    coef[0] = k; coef[1] = 0; coef[2] = k * sg * er; coef[3] = k * sg * ei;
-    coef[4] = 0; coef[5] = 0; coef[6] = 0; coef[7] = 0;
-  }
-  if (record) {
-    p.outcome[ms.ord] = (uint8_t)outc;
-    p.prob0[ms.ord] = P0;
-  }
-  if (loc.n < MAX_BFLY) {
-    loc.ord[loc.n] = ms.ord;
-    loc.out[loc.n] = (uint8_t)outc;
-    loc.n++;
-  }
-}
-
-// Prologue shared by the pass kernels: decisions of the pass's butterflies and op conditions.
-struct PassShared {
-  double coef[MAX_BFLY][8];
-  double ka[MAX_BFLY][2];  // structured butterfly U = k [[1, a], [1, -a]]: a (k folded into scale)
-  double scale;            // product of the pass's butterfly k's
-  uint8_t cond[MAX_OPS];
-  uint8_t bidx[MAX_OPS];
-  double red[32][4];
-  int last;
-};
-
-__device__ void pass_prologue(const StepDesc& d, const DevPtrs& p, PassShared& sh, bool record_all = false) {
-  if (threadIdx.x == 0) {
-    LocalOutcomes loc;
-    loc.n = 0;
-    int bi = 0;
-    double scale = 1.0;
-    const bool record = record_all || blockIdx.x == 0;
-    for (int i = 0; i < d.n_ops; ++i) {
-      const Op& op = d.ops[i];
-      if (op.type == OP_BFLY) {
-        double* cf = sh.coef[bi];
-        decide(p, op.m, bi == 0 && d.first_uses_red, false, record, cf, loc);
-        // folded X_a^s (cond/sig of a butterfly): swap the output rows when the signal is 1
-        if (op.cond && signal_parity(p, op.sig_off, op.sig_len, loc))
-          for (int j = 0; j < 4; ++j) {
-            double t = cf[j];
-            cf[j] = cf[4 + j];
-            cf[4 + j] = t;
-          }
-        // every slot-reuse butterfly has the form k [[1, a], [1, -a]] (rows swapped: a -> -a)
-        const double kk = cf[0];
-        sh.ka[bi][0] = kk != 0.0 ? cf[2] / kk : 0.0;
-        sh.ka[bi][1] = kk != 0.0 ? cf[3] / kk : 0.0;
-        scale *= kk;
-        sh.bidx[i] = (uint8_t)bi++;
-        sh.cond[i] = 1;
-      } else {
-        sh.cond[i] = op.cond ? (uint8_t)signal_parity(p, op.sig_off, op.sig_len, loc) : (uint8_t)1;
-      }
-    }
-    sh.scale = scale;
-  }
-  __syncthreads();
-}
-
-// Block reduction of up to 4 doubles; the last block to finish reduces all block partials in a
-// fixed order (deterministic) into red_result and resets the counter.
-template <int NRED>
-__device__ void reduce_finish(double (&acc)[4], const DevPtrs& p, PassShared& sh) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-#pragma unroll
-  for (int k = 0; k < NRED; ++k)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(FULLMASK, acc[k], o);
-  if (lane == 0)
-#pragma unroll
-    for (int k = 0; k < NRED; ++k) sh.red[warp][k] = acc[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot[4] = {0, 0, 0, 0};
-    for (int w = 0; w < nw; ++w)
-      for (int k = 0; k < NRED; ++k) tot[k] += sh.red[w][k];
-    for (int k = 0; k < NRED; ++k) p.partials[(size_t)blockIdx.x * 4 + k] = tot[k];
-    __threadfence();
-    unsigned t = atomicAdd(p.counter, 1u);
-    sh.last = (t == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!sh.last) return;
-  __threadfence();
-  double s[4] = {0, 0, 0, 0};
-  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
-    for (int k = 0; k < NRED; ++k) s[k] += __ldcg(&p.partials[(size_t)b * 4 + k]);
-#pragma unroll
-  for (int k = 0; k < NRED; ++k)
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s[k] += __shfl_xor_sync(FULLMASK, s[k], o);
-  __syncthreads();
-  if (lane == 0)
-    for (int k = 0; k < NRED; ++k) sh.red[warp][k] = s[k];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot[4] = {0, 0, 0, 0};
-    for (int w = 0; w < nw; ++w)
-      for (int k = 0; k < NRED; ++k) tot[k] += sh.red[w][k];
-    for (int k = 0; k < 4; ++k) p.red_result[k] = k < NRED ? tot[k] : 0.0;
-    *p.counter = 0;
-  }
 }
 
 // ------------------------------------------------------------------------------------------------

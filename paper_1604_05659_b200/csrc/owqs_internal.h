@@ -1,7 +1,15 @@
 // Internal definitions shared by the host scheduler (C++) and the sm_100a kernels (CUDA).
 // Plain-old-data only: the compiled pass program is uploaded / passed by value to kernels.
 #pragma once
+#ifdef __CUDACC_RTC__
+typedef unsigned char uint8_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+#else
 #include <stdint.h>
+#endif
 
 namespace owqs {
 

@@ -44,6 +44,49 @@ def host_gflow(pattern):
             L.owqs_host_free(h)
 
 
+def _host_handle(pattern, mode, precision, flags, weights, n_ranks):
+    L = lib()
+    i, o, arr, pool, plen = marshal_pattern(pattern.inputs, pattern.outputs, pattern.cmds)
+    w = (C.c_double * 4)(*weights) if weights is not None else None
+    h = C.c_void_p()
+    st = L.owqs_host_compile(i, len(pattern.inputs), o, len(pattern.outputs), arr, len(pattern.cmds), pool, plen,
+                             MODE_IDS[mode], precision, flags, w, n_ranks, C.byref(h))
+    if st != 0:
+        msg = L.owqs_host_error(h) if h else b""
+        if h:
+            L.owqs_host_free(h)
+        raise OwqsError(st, msg.decode() if msg else "")
+    return L, h
+
+
+def jit_host(pattern, mode: str = "sampled", precision: int = 64, flags: int = 0,
+             weights: Optional[Sequence[float]] = None, n_ranks: int = 1, sources: bool = False) -> dict:
+    """NVRTC-compile the generated pass kernels of the compiled program (no GPU needed).
+    Returns {n_kernels, n_jit_steps, compile_ms[, sources: {step: text}]}."""
+    L, h = _host_handle(pattern, mode, precision, flags, weights, n_ranks)
+    try:
+        nk, ns, ms = C.c_int64(), C.c_int64(), C.c_double()
+        st = L.owqs_host_jit(h, C.byref(nk), C.byref(ns), C.byref(ms))
+        if st != 0:
+            raise OwqsError(st, L.owqs_host_error(h).decode())
+        out = {"n_kernels": nk.value, "n_jit_steps": ns.value, "compile_ms": ms.value}
+        if sources:
+            info = _capi.owqs_host_info()
+            L.owqs_host_info_get(h, C.byref(info))
+            srcs = {}
+            for k in range(-1, info.n_steps):
+                n = C.c_int64()
+                L.owqs_host_jit_source(h, k, None, 0, C.byref(n))
+                if n.value:
+                    buf = C.create_string_buffer(n.value + 1)
+                    L.owqs_host_jit_source(h, k, buf, n.value + 1, C.byref(n))
+                    srcs[k] = buf.value.decode()
+            out["sources"] = srcs
+        return out
+    finally:
+        L.owqs_host_free(h)
+
+
 def compile_host(pattern, mode: str = "sampled", precision: int = 128, flags: int = 0,
                  weights: Optional[Sequence[float]] = None, n_ranks: int = 1) -> HostProgram:
     L = lib()
