@@ -91,7 +91,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 # ---- include/owqs_host.h (host-only introspection; no CUDA calls) ------------------------------
 HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_gflow",
                  "owqs_host_jit", "owqs_host_jit_source", "owqs_host_error", "owqs_host_free"]
-KMAX_HI, MAX_OPS, MAX_BFLY = 4, 64, 24
+KMAX_HI, MAX_OPS, MAX_BFLY = 8, 128, 64
 
 
 class Op(C.Structure):

@@ -34,7 +34,9 @@ cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_w
                              cudaStream_t s);
 cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
-cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s);
+cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
+                       cudaStream_t s);
+cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s);
 cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base, int K, int n_batch, const void* in,
                          void* out, int n_in, int n_out, const int* out_slot, int phys, int prec, cudaStream_t s);
 }  // namespace owqs
@@ -59,6 +61,7 @@ struct CompiledMode {
   std::vector<cudaKernel_t> jit_fn;
   std::vector<int> jit_blocks;
   int n_jit = 0;
+  PassCoef* d_pc = nullptr;  // one decision block per step (engine-2 generated kernels)
 };
 // one rank's part of the state and its reduction scratch
 struct Shard {
@@ -158,6 +161,7 @@ void free_mode(CompiledMode& m) {
   if (m.d_mst) cudaFree(m.d_mst);
   if (m.d_sig) cudaFree(m.d_sig);
   if (m.d_steps) cudaFree(m.d_steps);
+  if (m.d_pc) cudaFree(m.d_pc);
   m = CompiledMode();
 }
 
@@ -179,7 +183,8 @@ owqs_status compile_modes(owqs_ctx* ctx) {
     free_mode(ctx->cm[i]);
     auto t0 = std::chrono::steady_clock::now();
     CompiledMode& m = ctx->cm[i];
-    plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog, ctx->n_global);
+    plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog, ctx->n_global,
+                     (ctx->prec == 0 && !(ctx->cfg.flags & OWQS_FLAG_NO_JIT)) ? KTILE : KMAX_AOT);
     if (!m.prog.error.empty()) return fail(ctx, OWQS_E_ARG, m.prog.error);
     m.schedule_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     m.valid = true;
@@ -259,6 +264,7 @@ owqs_status ensure_device(owqs_ctx* ctx) {
       CU(cudaMalloc(&m.d_sig, m.prog.sig_pool.size() * sizeof(int32_t)));
       CU(cudaMemcpy(m.d_sig, m.prog.sig_pool.data(), m.prog.sig_pool.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
+    if (m.n_jit > 0 && !m.d_pc) CU(cudaMalloc(&m.d_pc, m.prog.steps.size() * sizeof(PassCoef)));
     if (m.n_jit > 0 && m.jit_fn.empty()) {
       std::vector<cudaKernel_t> fn(m.prog.steps.size(), nullptr);
       std::vector<int> blocks(m.prog.steps.size(), 0);
@@ -276,8 +282,12 @@ owqs_status ensure_device(owqs_ctx* ctx) {
           if (m.jit_name[k].empty() || fn[k]) continue;
           if (std::find(jm.names.begin(), jm.names.end(), m.jit_name[k]) == jm.names.end()) continue;
           CU(cudaLibraryGetKernel(&fn[k], lib, m.jit_name[k].c_str()));
+          const int eng = jit_engine(m.prog.steps[k], ctx->prec);
+          const int dyn = jit_dyn_smem(eng);
+          if (dyn > 0)
+            CU(cudaFuncSetAttribute((const void*)fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
           int nb = 0;
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], 256, 0));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], eng == 2 ? 256 : 256, dyn));
           blocks[k] = std::max(1, nb) * sms;
         }
       }
@@ -364,9 +374,12 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
         owqs_status st = do_swap(ctx, s);
         if (st != OWQS_OK) return st;
       } else {
+        const bool jit = !m.jit_fn.empty() && m.jit_fn[i];
+        const int eng = jit ? jit_engine(s, ctx->prec) : 0;
+        if (eng == 2) CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream));
         for (size_t r = 0; r < ctx->shards.size(); ++r) {
-          if (!m.jit_fn.empty() && m.jit_fn[i])
-            CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
+          if (jit)
+            CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream));
           else
             CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
         }
@@ -608,7 +621,9 @@ extern "C" {
 
 const char* owqs_version(void) { return "owqs-b200 0.2 (sm_100a)"; }
 
-const char* owqs_last_error(const owqs_ctx* ctx) { return ctx ? ctx->err.c_str() : "NULL context"; }
+static thread_local std::string g_create_err;  // why the last owqs_create on this thread failed
+
+const char* owqs_last_error(const owqs_ctx* ctx) { return ctx ? ctx->err.c_str() : g_create_err.c_str(); }
 
 owqs_status owqs_nccl_unique_id(void* out) {
   if (!out) return OWQS_E_ARG;
@@ -634,38 +649,48 @@ owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
   while ((1 << ctx->n_global) < nr) ++ctx->n_global;
   ctx->prec = cfg->precision == 64 ? 0 : 1;
   ctx->elem = cfg->precision == 64 ? 8 : 16;
-  auto bail = [&](owqs_status s) {
+  g_create_err.clear();
+  auto bail = [&](owqs_status s, const char* what = "") {
+    const cudaError_t ce = cudaGetLastError();
+    g_create_err = std::string("owqs_create: ") + what + (ce != cudaSuccess ? std::string(": ") + cudaGetErrorString(ce) : "");
     owqs_destroy(ctx);
     return s;
   };
-  if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(OWQS_E_CUDA);
-  if (init_kernel_limits(cfg->device) != cudaSuccess) return bail(OWQS_E_CUDA);
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return bail(OWQS_E_CUDA, "cudaSetDevice");
+  {
+    const cudaError_t e = init_kernel_limits(cfg->device);
+    if (e != cudaSuccess) {
+      g_create_err = std::string("owqs_create: kernel limits: ") + cudaGetErrorString(e);
+      owqs_destroy(ctx);
+      return OWQS_E_CUDA;
+    }
+  }
   if (cfg->stream) {
     ctx->stream = (cudaStream_t)cfg->stream;
   } else {
-    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(OWQS_E_CUDA);
+    if (cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking) != cudaSuccess) return bail(OWQS_E_CUDA, "allocation/stream/event setup");
     ctx->own_stream = true;
   }
-  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return bail(OWQS_E_CUDA);
+  if (cudaEventCreate(&ctx->ev0) != cudaSuccess || cudaEventCreate(&ctx->ev1) != cudaSuccess) return bail(OWQS_E_CUDA, "allocation/stream/event setup");
   const int n_sh = loopback ? nr : 1;
   ctx->shards.resize(n_sh);
-  if (cudaMalloc(&ctx->d_red_all, (size_t)n_sh * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM);
+  if (cudaMalloc(&ctx->d_red_all, (size_t)n_sh * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   const int nb = max_partial_blocks();
   for (int i = 0; i < n_sh; ++i) {
     Shard& s = ctx->shards[i];
     s.d_red = ctx->d_red_all + 4 * i;
-    if (cudaMalloc(&s.d_partials, (size_t)nb * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM);
-    if (cudaMalloc(&s.d_counter, sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_NOMEM);
-    if (cudaMemset(s.d_counter, 0, sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_CUDA);
-    if (cudaMalloc(&s.d_err, sizeof(int32_t)) != cudaSuccess) return bail(OWQS_E_NOMEM);
+    if (cudaMalloc(&s.d_partials, (size_t)nb * 4 * sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
+    if (cudaMalloc(&s.d_counter, (1 + RED_MAX_GROUPS) * sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
+    if (cudaMemset(s.d_counter, 0, (1 + RED_MAX_GROUPS) * sizeof(unsigned)) != cudaSuccess) return bail(OWQS_E_CUDA, "allocation/stream/event setup");
+    if (cudaMalloc(&s.d_err, sizeof(int32_t)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   }
-  if (cudaMalloc(&ctx->d_run, sizeof(RunParams)) != cudaSuccess) return bail(OWQS_E_NOMEM);
-  if (cudaMalloc(&ctx->d_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM);
-  if (cudaMallocHost(&ctx->h_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM);
+  if (cudaMalloc(&ctx->d_run, sizeof(RunParams)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
+  if (cudaMalloc(&ctx->d_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
+  if (cudaMallocHost(&ctx->h_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (nr > 1 && !loopback) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_id, sizeof(id));
-    if (ncclCommInitRank(&ctx->comm, nr, id, cfg->rank) != ncclSuccess) return bail(OWQS_E_NCCL);
+    if (ncclCommInitRank(&ctx->comm, nr, id, cfg->rank) != ncclSuccess) return bail(OWQS_E_NCCL, "allocation/stream/event setup");
   }
   *out = ctx;
   return OWQS_OK;

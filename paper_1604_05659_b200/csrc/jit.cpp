@@ -20,9 +20,11 @@
 #include <cuda_runtime.h>
 #include <nvrtc.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <map>
 #include <memory>
@@ -52,6 +54,17 @@ static __device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm("add.rn.f3
 static __device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 static __device__ __forceinline__ u64 shfl2(u64 x, int m) { return pk(__shfl_xor_sync(0xffffffffu, lo(x), m), __shfl_xor_sync(0xffffffffu, hi(x), m)); }
 static __device__ __forceinline__ u64 flip2(u64 x, unsigned f) { return x ^ (((u64)f << 63) | ((u64)f << 31)); }
+static __device__ __forceinline__ void mbar_init(unsigned a, unsigned n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory"); }
+static __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+static __device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned tx) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(tx) : "memory"); }
+static __device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) {
+  unsigned done;
+  do { asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.b32 %0, 1, 0, P1; }" : "=r"(done) : "r"(a), "r"(par) : "memory"); } while (!done);
+}
+static __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+static __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 static __device__ __forceinline__ double fld(double x, unsigned f) { return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)f << 63)); }
 )OWQS";
 
@@ -71,11 +84,41 @@ std::string hex64(uint64_t v) {
   return b;
 }
 
-enum SlotKind { SK_ELEM, SK_LANE, SK_GROUP, SK_BASE, SK_RANK };
+enum SlotKind { SK_REG, SK_LANE, SK_WARP, SK_BASE, SK_RANK };
+
+// ---- engine 2: the complex64 CTA tile ----------------------------------------------------------
+// A CTA (8 warps) owns a tile of 2^13 amplitudes: tile bits t0..t5 = slots 0..5 (one 512 B
+// segment), t6..t12 = the pass's group slots ascending (padded with untouched base slots). A layout
+// maps the tile bits onto (register position bit k: R[k], lane bit j: Lb[j], warp bit j: Wb[j]);
+// R[0] = t0 always, so every thread holds slot-0 neighbours as float4 pairs. Layouts whose lanes are
+// t1..t5 and registers t0 + 4 group bits ("A-type") are the ones global loads and stores use
+// (coalesced 512 B per warp instruction); the others are reached through the shared-memory tile.
+// Shared-memory 16 B unit of tile index t: u(t) = v + (v >> 3) + (v >> 6) + (v >> 9), v = t >> 1.
+// u is injective and additive over disjoint bit sets (per-thread base + per-register immediate),
+// and tile bit k >= 1 lands in bank group 2^((k - 1) mod 3) (mod 8): a quarter-warp is
+// conflict-free when lane bits 0, 1, 2 carry tile bits of the three classes (k - 1) mod 3.
+struct CLayout {
+  int R[5];
+  int Lb[5];
+  int Wb[3];
+};
+constexpr int kNW = 8;  // warps per CTA
+constexpr int kTileBits = 13;
+inline int umap(int t) {
+  const int v = t >> 1;
+  return v + (v >> 3) + (v >> 6) + (v >> 9);
+}
+constexpr int kTileSmem = 16 * (4095 + 511 + 63 + 7 + 1);  // 16 * (u(8191) + 1)
 
 struct Gen {
   const StepDesc& d;
-  const int prec, SB, EPV, KHI, G, UNR, NV, P;
+  const int prec;
+  const bool tile;  // engine 2
+  const int SB, EPV;
+  int KHI, G, UNR, P;
+  int gs[KMAX_HI];  // group slots (engine 2: padded to KTILE)
+  std::vector<CLayout> lays;  // engine 2 layouts used by this kernel
+  int lay = 0;                // engine 2: current layout index
   std::ostringstream o;
   std::vector<int> perm;  // logical register position -> variable id
   struct Pend {
@@ -83,47 +126,93 @@ struct Gen {
     bool cond;
   };
   std::vector<Pend> pend;
+  std::string error;
 
-  Gen(const StepDesc& dd, int pr)
-      : d(dd), prec(pr), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1), KHI(dd.nb_hi), G(1 << dd.nb_hi),
-        UNR(jit_unr_of(dd.nb_hi)), NV(UNR << dd.nb_hi), P((UNR << dd.nb_hi) * (pr == 0 ? 2 : 1)) {
+  Gen(const StepDesc& dd, int pr, bool use_tile)
+      : d(dd), prec(pr), tile(use_tile), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1) {
+    if (tile) {
+      KHI = KTILE;
+      UNR = 1;
+      int n = 0;
+      for (int j = 0; j < d.nb_hi; ++j) gs[n++] = d.bhi[j];
+      for (int s = 6; n < KTILE && s < d.width; ++s) {
+        bool used = false;
+        for (int j = 0; j < n; ++j) used = used || gs[j] == s;
+        if (!used) gs[n++] = s;
+      }
+      if (n < KTILE) error = "tile engine needs width >= 13";
+      std::sort(gs, gs + KTILE);
+      P = 32;
+    } else {
+      KHI = d.nb_hi;
+      UNR = jit_unr_of(KHI);
+      for (int j = 0; j < KHI; ++j) gs[j] = d.bhi[j];
+      P = (UNR << KHI) * EPV;
+    }
+    G = 1 << KHI;
     for (int p = 0; p < P; ++p) perm.push_back(p);
   }
 
-  int kind(int s, int* bit) const {
+  int tilebit(int s) const {
+    if (s < SB) return s;
+    for (int j = 0; j < KHI; ++j)
+      if (gs[j] == s) return SB + j;
+    return -1;
+  }
+  // kind of slot s in layout l (engine 2) / the fixed direct layout (engine 1); *bit = position
+  // mask (REG), lane bit (LANE), warp bit (WARP), bit of gb (BASE) or rank bit (RANK)
+  int kind_l(int s, int l, int* bit) const {
     if (s >= d.width) {
       *bit = s - d.width;
       return SK_RANK;
     }
+    const int tb = tilebit(s);
+    if (tb < 0) {
+      *bit = s - SB;
+      return SK_BASE;
+    }
+    if (tile) {
+      const CLayout& L = lays[l];
+      for (int k = 0; k < 5; ++k)
+        if (L.R[k] == tb) {
+          *bit = 1 << k;
+          return SK_REG;
+        }
+      for (int j = 0; j < 5; ++j)
+        if (L.Lb[j] == tb) {
+          *bit = j;
+          return SK_LANE;
+        }
+      for (int j = 0; j < 3; ++j)
+        if (L.Wb[j] == tb) {
+          *bit = j;
+          return SK_WARP;
+        }
+      return SK_BASE;  // unreachable
+    }
     if (EPV == 2 && s == 0) {
-      *bit = 0;
-      return SK_ELEM;
+      *bit = 1;
+      return SK_REG;
     }
     if (s < SB) {
       *bit = s - (EPV == 2 ? 1 : 0);
       return SK_LANE;
     }
-    for (int j = 0; j < KHI; ++j)
-      if (d.bhi[j] == s) {
-        *bit = j;
-        return SK_GROUP;
-      }
-    *bit = s - SB;
-    return SK_BASE;
+    *bit = EPV << (tb - SB);
+    return SK_REG;
   }
+  int kind(int s, int* bit) const { return kind_l(s, lay, bit); }
   bool is_reg(int s) const {
     int b;
-    int k = kind(s, &b);
-    return k == SK_ELEM || k == SK_GROUP;
+    return kind(s, &b) == SK_REG;
   }
-  // position-index bit that a register slot occupies
   int pbit(int s) const {
     int b;
-    int k = kind(s, &b);
-    return k == SK_ELEM ? 1 : (EPV << b);
+    kind(s, &b);
+    return b;
   }
   int regval(int s, int p) const { return (p & pbit(s)) ? 1 : 0; }
-  int unit_of(int p) const { return p / (G * EPV); }
+  int unit_of(int p) const { return tile ? 0 : p / (G * EPV); }
 
   std::string X(int p) const { return "x" + std::to_string(perm[p]); }
   std::string XR(int p) const { return "xr" + std::to_string(perm[p]); }
@@ -131,18 +220,20 @@ struct Gen {
 
   // parity of the runtime (non-register) bits of slot mask m for unit u; "" if none
   std::string rt_parity(uint64_t m, int u) const {
-    uint32_t L = 0, R = 0;
+    uint32_t L = 0, R = 0, W = 0;
     uint64_t B = 0;
     for (int s = 0; s < 64; ++s) {
       if (!((m >> s) & 1)) continue;
       int b;
       int k = kind(s, &b);
       if (k == SK_LANE) L |= 1u << b;
+      if (k == SK_WARP) W |= 1u << b;
       if (k == SK_BASE) B |= 1ull << b;
       if (k == SK_RANK) R |= 1u << b;
     }
     std::vector<std::string> t;
     if (L) t.push_back("__popc(lane & " + std::to_string(L) + "u)");
+    if (W) t.push_back("__popc(warp & " + std::to_string(W) + "u)");
     if (B) t.push_back("__popcll(gb" + std::to_string(u) + " & " + std::to_string(B) + "ull)");
     if (R) t.push_back("__popc(rk & " + std::to_string(R) + "u)");
     if (t.empty()) return "";
@@ -162,9 +253,11 @@ struct Gen {
     int b;
     int k = kind(s, &b);
     if (k == SK_LANE) return "((unsigned)(lane >> " + std::to_string(b) + ") & 1u)";
+    if (k == SK_WARP) return "((unsigned)(warp >> " + std::to_string(b) + ") & 1u)";
     if (k == SK_BASE) return "((unsigned)(gb" + std::to_string(u) + " >> " + std::to_string(b) + ") & 1u)";
     return "((rk >> " + std::to_string(b) + ") & 1u)";
   }
+  std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
   void bfly(int i, int bi) {
     const Op& op = d.ops[i];
@@ -172,8 +265,11 @@ struct Gen {
     const uint64_t am = d.absorb[bi];
     int lb;
     const int ka = kind(a, &lb);
-    o << "    {  // op " << i << ": butterfly " << bi << " on slot " << a << "\n";
-    if (prec == 0)
+    o << "    {  // op " << i << ": butterfly " << bi << " on slot " << a << (ka == SK_REG ? " (register)" : " (lane)")
+      << "\n";
+    if (tile)
+      o << "      const float ar = pc->ar[" << bi << "]; const u64 cB = pc->B[" << bi << "];\n";
+    else if (prec == 0)
       o << "      const float ar = s_ar[" << bi << "]; const u64 cB = s_B[" << bi << "];\n";
     else
       o << "      const double ar = s_ar[" << bi << "], ai = s_ai[" << bi << "];\n";
@@ -194,8 +290,8 @@ struct Gen {
           o << "      const double ar" << u << " = t" << u << " ? -ar : ar, ai" << u << " = t" << u << " ? -ai : ai;\n";
       }
     }
-    if (ka == SK_ELEM || ka == SK_GROUP) {
-      const int pb = pbit(a);
+    if (ka == SK_REG) {
+      const int pb = lb;
       for (int p = 0; p < P; ++p) {
         if (p & pb) continue;
         const int p1 = p | pb, u = unit_of(p);
@@ -244,7 +340,7 @@ struct Gen {
         }
       }
     } else {
-      error = "butterfly on a slot outside the pass";
+      error = "butterfly on a slot outside the thread's registers and lanes";
     }
     o << "    }\n";
   }
@@ -255,14 +351,14 @@ struct Gen {
     int lb;
     const int ka = kind(a, &lb);
     o << "    // op " << i << ": X on slot " << a << (op.cond ? " (conditional)" : "") << "\n";
-    if (ka == SK_ELEM || ka == SK_GROUP) {
-      const int pb = pbit(a);
+    if (ka == SK_REG) {
+      const int pb = lb;
       if (!op.cond) {  // compile-time renaming
         for (int p = 0; p < P; ++p)
           if (!(p & pb)) std::swap(perm[p], perm[p | pb]);
         return;
       }
-      o << "    if (sh.cond[" << i << "]) {\n";
+      o << "    if (" << cond_expr(i) << ") {\n";
       for (int p = 0; p < P; ++p) {
         if (p & pb) continue;
         const int p1 = p | pb;
@@ -274,8 +370,8 @@ struct Gen {
       }
       o << "    }\n";
     } else if (ka == SK_LANE) {
-      const std::string lm = op.cond ? "(sh.cond[" + std::to_string(i) + "] ? " + std::to_string(1 << lb) + " : 0)"
-                                     : std::to_string(1 << lb);
+      const std::string lm =
+          op.cond ? "(" + cond_expr(i) + " ? " + std::to_string(1 << lb) + " : 0)" : std::to_string(1 << lb);
       o << "    { const int lm = " << lm << ";\n";
       for (int p = 0; p < P; ++p) {
         if (prec == 0)
@@ -286,7 +382,7 @@ struct Gen {
       }
       o << "    }\n";
     } else {
-      error = "X on a slot outside the pass";
+      error = "X on a slot outside the thread's registers and lanes";
     }
   }
 
@@ -296,9 +392,9 @@ struct Gen {
     if (pend.empty()) return;
     o << "    {  // flush " << pend.size() << " pending diagonal(s)\n";
     struct Term {
-      std::vector<int> regs;      // register slots of the op
-      bool stat1;                 // runtime factor is the constant 1
-      std::vector<std::string> rt;  // per unit: runtime variable name
+      std::vector<int> regs;
+      bool stat1;
+      std::vector<std::string> rt;
     };
     std::vector<Term> terms;
     for (size_t k = 0; k < pend.size(); ++k) {
@@ -312,7 +408,7 @@ struct Gen {
       if (!t.stat1)
         for (int u = 0; u < UNR; ++u) {
           std::string nm = "f" + std::to_string(k) + "_" + std::to_string(u);
-          std::string e = pe.cond ? "(unsigned)sh.cond[" + std::to_string(pe.idx) + "]" : "1u";
+          std::string e = pe.cond ? "(unsigned)" + cond_expr(pe.idx) : "1u";
           for (int s : rts) e += " & " + rt_bit(s, u);
           o << "      const unsigned " << nm << " = " << e << ";\n";
           t.rt.push_back(nm);
@@ -353,8 +449,6 @@ struct Gen {
 
   void reduce() {
     if (d.red_kind == RED_NONE) return;
-    const char* T = prec == 0 ? "u64" : "double";
-    (void)T;
     if (d.red_kind == RED_NORM) {
       if (prec == 0) {
         o << "    { u64 n0 = 0ull, n1 = 0ull;\n";
@@ -372,8 +466,8 @@ struct Gen {
     const int r = d.red_slot;
     int lb;
     const int kr = kind(r, &lb);
-    if (kr == SK_ELEM || kr == SK_GROUP) {
-      const int pb = pbit(r);
+    if (kr == SK_REG) {
+      const int pb = lb;
       if (prec == 0) {
         o << "    { u64 n0 = 0ull, n1 = 0ull, cc = 0ull, cd = 0ull;\n";
         for (int p = 0; p < P; ++p) {
@@ -416,13 +510,49 @@ struct Gen {
         o << "      if ((lane >> " << lb << ") & 1) { acc1 += nn; } else { acc0 += nn; acc2 += cc; acc3 += cd; } }\n";
       }
     } else {
-      error = "reduction slot outside the pass";
+      error = "reduction slot outside the thread's registers and lanes";
     }
   }
 
-  std::string error;
+  // unit index -> group base (zeros inserted at the group slots, ascending)
+  void emit_gb(const std::string& dst, const std::string& unit) {
+    o << "    unsigned long long " << dst << " = " << unit << ";\n";
+    for (int j = 0; j < KHI; ++j) {
+      const int q = gs[j] - SB;
+      o << "    " << dst << " = ((" << dst << " >> " << q << ") << " << (q + 1) << ") | (" << dst << " & "
+        << ((1ull << q) - 1) << "ull);\n";
+    }
+  }
+  uint64_t seg_off(int c) const {
+    uint64_t s = 0;
+    for (int j = 0; j < KHI; ++j)
+      if ((c >> j) & 1) s |= 1ull << (gs[j] - SB);
+    return s;
+  }
 
-  std::string run() {
+  void emit_op(int i, int bi) {
+    const Op& op = d.ops[i];
+    switch (op.type) {
+      case OP_DIAG_E:
+      case OP_DIAG_Z:
+        pend.push_back({op.a, op.type == OP_DIAG_E ? op.b : op.a, i, op.cond != 0});
+        break;
+      case OP_FLUSH:
+        flush();
+        break;
+      case OP_X:
+        xop(i);
+        break;
+      case OP_BFLY:
+        bfly(i, bi);
+        break;
+      default:
+        break;
+    }
+  }
+
+  // ---- engine 1: direct coalesced loads into registers (complex128, and narrow complex64) ----
+  std::string run_direct() {
     const int nbf = d.n_bfly;
     const int red = d.red_kind;
     const int nred = red == RED_NONE ? 0 : (red == RED_NORM ? 1 : 4);
@@ -431,8 +561,8 @@ struct Gen {
     const uint64_t nbu = 1ull << slack;
     o << "extern \"C\" __global__ void __launch_bounds__(256, " << minb << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p) {\n"
       << "  using namespace owqs;\n"
-      << "  // width " << d.width << ", group slots";
-    for (int j = 0; j < KHI; ++j) o << " " << d.bhi[j];
+      << "  // direct engine: width " << d.width << ", group slots";
+    for (int j = 0; j < KHI; ++j) o << " " << gs[j];
     o << ", " << d.n_ops << " ops, " << nbf << " butterflies, reduction " << red << "\n";
     o << "  __shared__ PassShared sh;\n";
     if (prec == 0)
@@ -441,11 +571,11 @@ struct Gen {
       o << "  __shared__ double s_ar[" << std::max(1, nbf) << "], s_ai[" << std::max(1, nbf) << "];\n";
     o << "  pass_prologue(d, p, sh);\n";
     if (nbf > 0) {
-      o << "  if (threadIdx.x < " << nbf << ") {\n";
+      o << "  for (int b = threadIdx.x; b < " << nbf << "; b += blockDim.x) {\n";
       if (prec == 0)
-        o << "    const float ai = (float)sh.ka[threadIdx.x][1]; s_ar[threadIdx.x] = (float)sh.ka[threadIdx.x][0]; s_B[threadIdx.x] = pk(-ai, ai);\n";
+        o << "    const float ai = (float)sh.ka[b][1]; s_ar[b] = (float)sh.ka[b][0]; s_B[b] = pk(-ai, ai);\n";
       else
-        o << "    s_ar[threadIdx.x] = sh.ka[threadIdx.x][0]; s_ai[threadIdx.x] = sh.ka[threadIdx.x][1];\n";
+        o << "    s_ar[b] = sh.ka[b][0]; s_ai[b] = sh.ka[b][1];\n";
       o << "  }\n  __syncthreads();\n";
     }
     o << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
@@ -463,25 +593,11 @@ struct Gen {
       o << "  double2* __restrict__ st = reinterpret_cast<double2*>(p.state);\n";
     o << "  for (unsigned long long ub = blockIdx.x; ub < " << nbu << "ull; ub += gridDim.x) {\n"
       << "    const unsigned long long unit = ub * 8 + warp;\n";
-    for (int u = 0; u < UNR; ++u) {
-      o << "    unsigned long long gb" << u << " = unit * " << UNR << " + " << u << ";\n";
-      for (int j = 0; j < KHI; ++j) {
-        const int q = d.bhi[j] - SB;
-        o << "    gb" << u << " = ((gb" << u << " >> " << q << ") << " << (q + 1) << ") | (gb" << u << " & "
-          << ((1ull << q) - 1) << "ull);\n";
-      }
-    }
-    // loads
-    auto off = [&](int c) {
-      uint64_t s = 0;
-      for (int j = 0; j < KHI; ++j)
-        if ((c >> j) & 1) s |= 1ull << (d.bhi[j] - SB);
-      return s;
-    };
+    for (int u = 0; u < UNR; ++u) emit_gb("gb" + std::to_string(u), "unit * " + std::to_string(UNR) + " + " + std::to_string(u));
     for (int u = 0; u < UNR; ++u)
       for (int c = 0; c < G; ++c) {
         const int v = u * G + c;
-        const std::string addr = "st + (((gb" + std::to_string(u) + " | " + std::to_string(off(c)) + "ull) << 5) + lane)";
+        const std::string addr = "st + (((gb" + std::to_string(u) + " | " + std::to_string(seg_off(c)) + "ull) << 5) + lane)";
         if (prec == 0)
           o << "    u64 x" << 2 * v << ", x" << 2 * v + 1 << "; { const float4 w = __ldcs(" << addr << "); x" << 2 * v
             << " = pk(w.x, w.y); x" << 2 * v + 1 << " = pk(w.z, w.w); }\n";
@@ -489,43 +605,16 @@ struct Gen {
           o << "    double xr" << v << ", xi" << v << "; { const double2 w = __ldcs(" << addr << "); xr" << v
             << " = w.x; xi" << v << " = w.y; }\n";
       }
-    // ops
     int bi = 0;
-    for (int i = 0; i < d.n_ops; ++i) {
-      const Op& op = d.ops[i];
-      switch (op.type) {
-        case OP_DIAG_E:
-        case OP_DIAG_Z:
-          pend.push_back({op.a, op.type == OP_DIAG_E ? op.b : op.a, i, op.cond != 0});
-          break;
-        case OP_FLUSH:
-          flush();
-          break;
-        case OP_X:
-          xop(i);
-          break;
-        case OP_BFLY:
-          bfly(i, bi++);
-          break;
-        default:
-          break;
-      }
-    }
+    for (int i = 0; i < d.n_ops; ++i) emit_op(i, d.ops[i].type == OP_BFLY ? bi++ : -1);
     flush();
-    if (nbf > 0) {
-      for (int p = 0; p < P; ++p) {
-        if (prec == 0)
-          o << "    " << X(p) << " = mul2(scale, " << X(p) << ");\n";
-        else
-          o << "    " << XR(p) << " *= scale; " << XI(p) << " *= scale;\n";
-      }
-    }
+    emit_scale(nbf);
     reduce();
     if (d.n_ops > 0) {
       for (int u = 0; u < UNR; ++u)
         for (int c = 0; c < G; ++c) {
           const int v = u * G + c;
-          const std::string addr = "st + (((gb" + std::to_string(u) + " | " + std::to_string(off(c)) + "ull) << 5) + lane)";
+          const std::string addr = "st + (((gb" + std::to_string(u) + " | " + std::to_string(seg_off(c)) + "ull) << 5) + lane)";
           const int p0 = v * EPV;
           if (prec == 0)
             o << "    __stcs(" << addr << ", make_float4(lo(" << X(p0) << "), hi(" << X(p0) << "), lo(" << X(p0 + 1)
@@ -539,6 +628,318 @@ struct Gen {
     o << "}\n";
     return o.str();
   }
+
+  void emit_scale(int nbf) {
+    if (nbf == 0) return;
+    for (int p = 0; p < P; ++p) {
+      if (prec == 0)
+        o << "    " << X(p) << " = mul2(scale, " << X(p) << ");\n";
+      else
+        o << "    " << XR(p) << " *= scale; " << XI(p) << " *= scale;\n";
+    }
+  }
+
+  // ---- engine 2: phase planning ---------------------------------------------------------------
+  // ops of the pass in a dependency DAG (two ops conflict when one's non-diagonal slot is touched
+  // by the other; diagonals commute; FLUSH is a barrier); index n = the reduction (after all).
+  // A phase = a register set (t0 + 4 tile bits) and the ops it runs; greedy: each phase picks the
+  // 4 tile bits that let the most ready ops run, one bit at a time.
+  struct Phase {
+    int S[4];
+    std::vector<int> ops;
+  };
+  int n_ops_ = 0;
+  std::vector<std::vector<int>> preds;
+  std::vector<int> op_tb;  // tile bit an op needs in registers (-1: none)
+  uint64_t tile_iters = 1;
+
+  void build_dag() {
+    const int n = d.n_ops;
+    n_ops_ = n;
+    preds.assign(n + 1, {});
+    op_tb.assign(n + 1, -1);
+    std::vector<uint64_t> nd(n + 1, 0), dg(n + 1, 0);
+    std::vector<char> bar(n + 1, 0);
+    int bi = 0;
+    for (int i = 0; i < n; ++i) {
+      const Op& op = d.ops[i];
+      if (op.type == OP_BFLY) {
+        nd[i] = 1ull << op.a;
+        dg[i] = d.absorb[bi++];
+        op_tb[i] = tilebit(op.a);
+      } else if (op.type == OP_X) {
+        nd[i] = 1ull << op.a;
+        op_tb[i] = tilebit(op.a);
+      } else if (op.type == OP_DIAG_E) {
+        dg[i] = (1ull << op.a) | (1ull << op.b);
+      } else if (op.type == OP_DIAG_Z) {
+        dg[i] = 1ull << op.a;
+      } else if (op.type == OP_FLUSH) {
+        bar[i] = 1;
+      }
+    }
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < i; ++j)
+        if (bar[i] || bar[j] || (nd[j] & (nd[i] | dg[i])) || (dg[j] & nd[i])) preds[i].push_back(j);
+    for (int j = 0; j < n; ++j) preds[n].push_back(j);
+    if (d.red_kind == RED_RHO) op_tb[n] = tilebit(d.red_slot);
+  }
+  bool exec_in(int i, unsigned regmask) const { return op_tb[i] < 0 || ((regmask >> op_tb[i]) & 1); }
+  // ops (ascending) that run in a phase with register tile-bit mask regmask, given done
+  std::vector<int> closure(unsigned regmask, const std::vector<char>& done) const {
+    std::vector<char> take(n_ops_ + 1, 0);
+    std::vector<int> out;
+    for (int i = 0; i <= n_ops_; ++i) {
+      if (done[i] || !exec_in(i, regmask)) continue;
+      bool ok = true;
+      for (int j : preds[i])
+        if (!done[j] && !take[j]) {
+          ok = false;
+          break;
+        }
+      if (ok) {
+        take[i] = 1;
+        out.push_back(i);
+      }
+    }
+    return out;
+  }
+  std::vector<Phase> plan_greedy(bool first_group_only) const {
+    std::vector<Phase> ph;
+    std::vector<char> done(n_ops_ + 1, 0);
+    int left = n_ops_ + 1;
+    bool first = true;
+    while (left > 0) {
+      Phase P_;
+      unsigned regs = 1u;  // t0
+      for (int k = 0; k < 4; ++k) {
+        int best = -1;
+        size_t bestn = 0;
+        for (int b = 1; b < kTileBits; ++b) {
+          if ((regs >> b) & 1) continue;
+          if (first && first_group_only && b < 6) continue;
+          const size_t nn = closure(regs | (1u << b), done).size();
+          // prefer more ops, then group bits (keeps A-type layouts), then the lowest bit
+          const bool better = best < 0 || nn > bestn || (nn == bestn && (b >= 6) && best < 6);
+          if (better) {
+            best = b;
+            bestn = nn;
+          }
+        }
+        regs |= 1u << best;
+        P_.S[k] = best;
+      }
+      P_.ops = closure(regs, done);
+      if (P_.ops.empty()) return {};  // cannot happen (every op's slot is a tile bit)
+      for (int i : P_.ops) done[i] = 1;
+      left -= (int)P_.ops.size();
+      std::sort(P_.S, P_.S + 4);
+      ph.push_back(P_);
+      first = false;
+    }
+    // merge a trailing phase's register set into its predecessor when it needs no new bits
+    return ph;
+  }
+  static bool a_type(const int* S) {
+    for (int k = 0; k < 4; ++k)
+      if (S[k] < 6) return false;
+    return true;
+  }
+  static int n_transitions(const std::vector<Phase>& ph) {
+    if (ph.empty()) return 1 << 20;
+    int t = (int)ph.size() - 1;
+    if (!a_type(ph.front().S)) ++t;
+    if (!a_type(ph.back().S)) ++t;
+    return t;
+  }
+  // lanes / warps for a register set
+  CLayout make_layout(const int* S) const {
+    CLayout L;
+    L.R[0] = 0;
+    for (int k = 0; k < 4; ++k) L.R[k + 1] = S[k];
+    if (a_type(S)) {
+      for (int j = 0; j < 5; ++j) L.Lb[j] = j + 1;
+      int w = 0;
+      for (int b = 6; b < kTileBits; ++b) {
+        bool in = false;
+        for (int k = 0; k < 4; ++k) in = in || S[k] == b;
+        if (!in) L.Wb[w++] = b;
+      }
+      return L;
+    }
+    std::vector<int> rest;
+    for (int b = 1; b < kTileBits; ++b) {
+      bool in = false;
+      for (int k = 0; k < 4; ++k) in = in || S[k] == b;
+      if (!in) rest.push_back(b);
+    }
+    // lane bits 0..2: one tile bit of each bank class (k - 1) mod 3, lowest first
+    std::vector<char> used(rest.size(), 0);
+    for (int c = 0; c < 3; ++c) {
+      int pick = -1;
+      for (size_t i = 0; i < rest.size(); ++i)
+        if (!used[i] && (rest[i] - 1) % 3 == c) {
+          pick = (int)i;
+          break;
+        }
+      if (pick < 0)  // no bit of this class left: 2-way bank conflicts, still correct
+        for (size_t i = 0; i < rest.size(); ++i)
+          if (!used[i]) {
+            pick = (int)i;
+            break;
+          }
+      used[pick] = 1;
+      L.Lb[c] = rest[pick];
+    }
+    int j = 3, w = 0;
+    for (size_t i = 0; i < rest.size(); ++i) {
+      if (used[i]) continue;
+      if (j < 5)
+        L.Lb[j++] = rest[i];
+      else
+        L.Wb[w++] = rest[i];
+    }
+    return L;
+  }
+  int treg(const CLayout& L, int p) const {
+    int t = 0;
+    for (int k = 0; k < 5; ++k)
+      if ((p >> k) & 1) t |= 1 << L.R[k];
+    return t;
+  }
+  int add_layout(const CLayout& L) {
+    for (size_t i = 0; i < lays.size(); ++i)
+      if (!memcmp(&lays[i], &L, sizeof L)) return (int)i;
+    lays.push_back(L);
+    return (int)lays.size() - 1;
+  }
+  // segment offset (relative to gb) of register pair p in A-type layout l (group bits only)
+  uint64_t a_seg(int l, int p) const {
+    uint64_t s = 0;
+    const CLayout& L = lays[l];
+    for (int k = 1; k < 5; ++k)
+      if ((p >> k) & 1) s |= 1ull << (gs[L.R[k] - 6] - 6);
+    return s;
+  }
+  void emit_tile_transition(int to, bool last) {
+    o << "    // layout " << lay << " -> " << to << " (shared-memory tile)\n";
+    const CLayout& A = lays[lay];
+    const CLayout& B = lays[to];
+    for (int p = 0; p < P; p += 2)
+      o << "    *reinterpret_cast<float4*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_float4(lo("
+        << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
+    o << "    __syncthreads();\n";
+    for (int p = 0; p < P; p += 2)
+      o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
+        << "); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
+    for (int p = 0; p < P; ++p) perm[p] = p;
+    if (!last || tile_iters > 1) o << "    __syncthreads();\n";
+    lay = to;
+  }
+
+  // ---- engine 2 kernel: one CTA = one 13-bit tile (non-persistent grid), coalesced global IO in
+  // A-type layouts, phases separated by shared-memory transposes, decisions from PassCoef,
+  // deterministic two-level grid reduction ----
+  std::string run_tile() {
+    const int nbf = d.n_bfly;
+    const int red = d.red_kind;
+    const int nred = red == RED_NONE ? 0 : (red == RED_NORM ? 1 : 4);
+    const uint64_t nbu = 1ull << (d.width - kTileBits);
+    const uint64_t iters = nbu > (uint64_t)RED_MAX_BLOCKS ? nbu / RED_MAX_BLOCKS : 1;
+    tile_iters = iters;
+    build_dag();
+    std::vector<Phase> pa = plan_greedy(true), pb = plan_greedy(false);
+    const std::vector<Phase>& ph = n_transitions(pb) < n_transitions(pa) ? pb : pa;
+    if (ph.empty()) {
+      error = "phase planning failed";
+      return "";
+    }
+    // layouts: load layout, phase layouts, store layout
+    std::vector<int> plays;
+    for (const Phase& f : ph) plays.push_back(add_layout(make_layout(f.S)));
+    const int l_load = a_type(ph.front().S) ? plays.front() : add_layout(make_layout(std::array<int, 4>{6, 7, 8, 9}.data()));
+    const int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(std::array<int, 4>{6, 7, 8, 9}.data()));
+    int n_trans = 0;
+    {
+      int cur = l_load;
+      for (int l : plays) n_trans += l != cur, cur = l;
+      n_trans += l_store != cur;
+    }
+    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * kNW << ", 2) OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* __restrict__ pc) {\n"
+      << "  using namespace owqs;\n"
+      << "  // tile engine: width " << d.width << ", tile group slots";
+    for (int j = 0; j < KTILE; ++j) o << " " << gs[j];
+    o << " (pass's " << d.nb_hi << "), " << d.n_ops << " ops, " << nbf << " butterflies, reduction " << red << ", "
+      << ph.size() << " phase(s), " << n_trans << " transpose(s), " << iters << " tile(s) per CTA\n";
+    for (size_t f = 0; f < ph.size(); ++f) {
+      o << "  // phase " << f << ": registers t0";
+      for (int k = 0; k < 4; ++k) o << " t" << ph[f].S[k];
+      o << ", " << ph[f].ops.size() << " op(s)\n";
+    }
+    if (n_trans) o << "  extern __shared__ __align__(16) unsigned char dsm[];\n";
+    o << "  __shared__ double red_s[32][4];\n  __shared__ int flag_s;\n"
+      << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
+      << "  const unsigned rk = p.rank; (void)rk; (void)d;\n"
+      << "  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;\n";
+    if (nbf > 0) o << "  const u64 scale = bc((float)pc->scale);\n";
+    if (n_trans)
+      for (size_t l = 0; l < lays.size(); ++l) {
+        o << "  const int sb" << l << " = 16 * (";
+        for (int j = 0; j < 5; ++j) o << (j ? " + " : "") << "((lane >> " << j << ") & 1) * " << umap(1 << lays[l].Lb[j]);
+        for (int j = 0; j < 3; ++j) o << " + ((warp >> " << j << ") & 1) * " << umap(1 << lays[l].Wb[j]);
+        o << ");\n";
+      }
+    auto wseg = [&](int l) {
+      std::string e = "(";
+      for (int j = 0; j < 3; ++j)
+        e += std::string(j ? " | " : "") + "((unsigned long long)((warp >> " + std::to_string(j) + ") & 1) << " +
+             std::to_string(gs[lays[l].Wb[j] - 6] - 6) + ")";
+      return e + ")";
+    };
+    o << "  const unsigned long long wsl = " << wseg(l_load) << ";\n";
+    o << "  const unsigned long long wss = " << wseg(l_store) << ";\n";
+    o << "  float4* __restrict__ st = reinterpret_cast<float4*>(p.state);\n"
+      << "  for (unsigned it = 0; it < " << iters << "u; ++it) {\n"
+      << "    const unsigned long long ub = (unsigned long long)blockIdx.x * " << iters << "ull + it;\n";
+    emit_gb("gb0", "ub");
+    for (int q = 0; q < P; q += 2)
+      o << "    u64 x" << q << ", x" << q + 1 << "; { const float4 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
+        << "ull) << 5) + lane)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
+    lay = l_load;
+    for (int q = 0; q < P; ++q) perm[q] = q;
+    std::vector<int> bidx(d.n_ops, -1);
+    {
+      int bi = 0;
+      for (int i = 0; i < d.n_ops; ++i)
+        if (d.ops[i].type == OP_BFLY) bidx[i] = bi++;
+    }
+    int left = n_trans;
+    for (size_t f = 0; f < ph.size(); ++f) {
+      if (plays[f] != lay) emit_tile_transition(plays[f], --left == 0);
+      o << "    // ---- phase " << f << "\n";
+      for (int i : ph[f].ops) {
+        if (i == n_ops_) {  // the reduction (after every op)
+          flush();
+          emit_scale(nbf);
+          reduce();
+        } else {
+          emit_op(i, bidx[i]);
+        }
+      }
+    }
+    if (l_store != lay) emit_tile_transition(l_store, --left == 0);
+    if (d.n_ops > 0)
+      for (int q = 0; q < P; q += 2)
+        o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_float4(lo(" << X(q)
+          << "), hi(" << X(q) << "), lo(" << X(q + 1) << "), hi(" << X(q + 1) << ")));\n";
+    o << "  }\n";
+    if (nred > 0)
+      o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n  reduce_finish_grid<" << nred << ">(acc, p, red_s, &flag_s);\n";
+    o << "}\n";
+    return o.str();
+  }
+
+  std::string run() { return tile ? run_tile() : run_direct(); }
 };
 
 // ---- compile cache ------------------------------------------------------------------------------
@@ -573,13 +974,19 @@ std::string compile_tu(const std::string& src, std::vector<char>& cubin) {
 
 }  // namespace
 
-bool jit_eligible(const StepDesc& d, int prec) {
-  if (d.kind != ST_PASS) return false;
+int jit_engine(const StepDesc& d, int prec) {
+  if (d.kind != ST_PASS) return 0;
+  if (prec == 0 && d.width >= kTileBits && d.nb_hi <= KTILE && !getenv("OWQS_JIT_NO_TILE")) return 2;
+  if (d.nb_hi > KMAX_AOT) return -1;  // needs the tile engine
   const int SB = prec == 0 ? 6 : 5;
   const int unr = jit_unr_of(d.nb_hi);
   const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
-  return slack >= 0;
+  return slack >= 0 ? 1 : 0;
 }
+
+bool jit_eligible(const StepDesc& d, int prec) { return jit_engine(d, prec) > 0; }
+
+int jit_dyn_smem(int engine) { return engine == 2 ? kTileSmem : 0; }
 
 const std::string& jit_prelude() {
   static const std::string s = std::string(kPreludeInternal) + "\n" + kPreludeCommon + "\n" + kHelpers;
@@ -587,10 +994,13 @@ const std::string& jit_prelude() {
 }
 
 std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
-  Gen g(d, prec);
+  const int eng = jit_engine(d, prec);
+  if (!eng) return "";
+  Gen g(d, prec, eng == 2);
+  if (!g.error.empty()) return "";
   std::string body = g.run();
   if (!g.error.empty()) return "";
-  const std::string nm = "owqs_pass_" + std::string(prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
+  const std::string nm = std::string(eng == 2 ? "owqs_tma_" : "owqs_pass_") + (prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
   const std::string key = "OWQS_KNAME";
   body.replace(body.find(key), key.size(), nm);
   if (name) *name = nm;
@@ -661,15 +1071,25 @@ std::string jit_compile(const std::vector<std::string>& names, const std::vector
   return "";
 }
 
-cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s) {
+cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
+                       cudaStream_t s) {
+  const int eng = jit_engine(d, prec);
   const int SB = prec == 0 ? 6 : 5;
   const int unr = jit_unr_of(d.nb_hi);
-  const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
-  const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));
   StepDesc dd = d;
   DevPtrs pp = p;
+  const PassCoef* pcc = pc;
+  if (eng == 2) {  // non-persistent: one CTA per 13-bit tile (or iters tiles above RED_MAX_BLOCKS)
+    const uint64_t nbu = 1ull << (d.width - kTileBits);
+    const uint64_t blocks = nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu;
+    void* args[] = {&dd, &pp, &pcc};
+    return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(32 * kNW), args, (size_t)jit_dyn_smem(eng), s);
+  }
+  const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
+  const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));
   void* args[] = {&dd, &pp};
-  return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(256), args, 0, s);
+  return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(eng == 2 ? 32 * kNW : 256), args,
+                          (size_t)jit_dyn_smem(eng), s);
 }
 
 }  // namespace owqs

@@ -20,8 +20,13 @@ namespace owqs {
 // SB = warp-segment bits (6 complex64, 5 complex128). Same UNR rule as the AOT kernel.
 inline int jit_unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
 
-// True when the step runs as a generated pass kernel (ST_PASS wide enough for the 8-warp grid).
+// Engine of a step: 0 = not generated (ahead-of-time kernel), 1 = direct-load kernel (complex128,
+// narrow complex64), 2 = TMA-pipelined complex64 kernel with shared-memory transposes (width >= 13).
+int jit_engine(const StepDesc& d, int prec);
+// True when the step runs as a generated pass kernel.
 bool jit_eligible(const StepDesc& d, int prec);
+// Dynamic shared memory (bytes) an engine's kernels are launched with.
+int jit_dyn_smem(int engine);
 
 // Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
 // a hash of the body (identical passes share one kernel).

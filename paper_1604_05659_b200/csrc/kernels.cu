@@ -949,8 +949,8 @@ __global__ void __launch_bounds__(256) dot_kernel(DevPtrs p, const double2* a, c
 // Host-side launchers (C++ linkage inside namespace owqs; used by runtime.cpp)
 // ------------------------------------------------------------------------------------------------
 struct KernelLimits {
-  int max_blocks_pass[2][KMAX_HI + 1];
-  int one_cta[KMAX_HI + 1];  // use the 1-CTA/SM (uncapped registers) variant
+  int max_blocks_pass[2][KMAX_AOT + 1];
+  int one_cta[KMAX_AOT + 1];  // use the 1-CTA/SM (uncapped registers) variant
   int max_blocks_elem;
   int sm_count;
 };
@@ -966,16 +966,16 @@ cudaError_t init_kernel_limits(int device) {
   cudaError_t e = cudaGetDeviceProperties(&prop, device);
   if (e != cudaSuccess) return e;
   g_lim.sm_count = prop.multiProcessorCount;
-  void* fns[2][KMAX_HI + 1] = {
+  void* fns[2][KMAX_AOT + 1] = {
       {pass_fn<float, 0, 4>(), pass_fn<float, 1, 2>(), pass_fn<float, 2, 1>(), pass_fn<float, 3, 1>(), pass_fn<float, 4, 1>()},
       {pass_fn<double, 0, 4>(), pass_fn<double, 1, 2>(), pass_fn<double, 2, 1>(), pass_fn<double, 3, 1>(), pass_fn<double, 4, 1>()}};
-  for (int k = 0; k <= KMAX_HI; ++k) g_lim.one_cta[k] = 0;
+  for (int k = 0; k <= KMAX_AOT; ++k) g_lim.one_cta[k] = 0;
   if (const char* env = getenv("OWQS_ONE_CTA"))  // bit k: KHI = k uses the 1-CTA/SM variant
-    for (int k = 3; k <= KMAX_HI; ++k) g_lim.one_cta[k] = (atoi(env) >> k) & 1;
+    for (int k = 3; k <= KMAX_AOT; ++k) g_lim.one_cta[k] = (atoi(env) >> k) & 1;
   void* one[2][2] = {{(void*)pass_kernel<float, 3, 1, 1>, (void*)pass_kernel<float, 4, 1, 1>},
                      {(void*)pass_kernel<double, 3, 1, 1>, (void*)pass_kernel<double, 4, 1, 1>}};
   for (int pr = 0; pr < 2; ++pr)
-    for (int k = 0; k <= KMAX_HI; ++k) {
+    for (int k = 0; k <= KMAX_AOT; ++k) {
       int nb = 0;
       void* f = (k >= 3 && g_lim.one_cta[k]) ? one[pr][k - 3] : fns[pr][k];
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, 256, 0);
@@ -991,7 +991,29 @@ cudaError_t init_kernel_limits(int device) {
   return cudaSuccess;
 }
 
-int max_partial_blocks() { return 16 * 148 * 2; }
+int max_partial_blocks() { return RED_MAX_BLOCKS + RED_MAX_GROUPS; }
+
+// Decisions of one pass for the generated pass kernels (one warp; PassCoef read by every CTA).
+__global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevPtrs p, PassCoef* pc) {
+  __shared__ PassShared sh;
+  pass_prologue(d, p, sh, true);
+  const int t = threadIdx.x;
+  for (int b = t; b < d.n_bfly; b += 32) {
+    const double ar = sh.ka[b][0], ai = sh.ka[b][1];
+    pc->ard[b] = ar;
+    pc->aid[b] = ai;
+    pc->ar[b] = (float)ar;
+    const float fai = (float)ai;
+    pc->B[b] = ((uint64_t)__float_as_uint(fai) << 32) | (uint64_t)__float_as_uint(-fai);
+  }
+  for (int i = t; i < d.n_ops; i += 32) pc->cond[i] = sh.cond[i];
+  if (t == 0) pc->scale = sh.scale;
+}
+
+cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s) {
+  decide_kernel<<<1, 32, 0, s>>>(d, p, pc);
+  return cudaGetLastError();
+}
 
 static inline int unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
 static inline int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; }
@@ -1051,6 +1073,7 @@ cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStrea
   const int SB = prec == 0 ? 6 : 5;
   if (d.kind == ST_PASS) {
     const int khi = d.nb_hi;
+    if (khi > KMAX_AOT) return cudaErrorInvalidValue;  // wide passes run only as generated tile kernels
     const int unr = unr_of(khi);
     const int slack = d.width - SB - khi - log2i(unr) - 3;  // units come in groups of 8 warps
     if (slack < 0) {

@@ -36,9 +36,11 @@ struct Op {
 };
 static_assert(sizeof(Op) == 16, "Op layout");
 
-constexpr int MAX_OPS = 64;      // ops per pass (incl. compiler-placed flushes)
-constexpr int KMAX_HI = 4;       // group slots above the warp segment per pass
-constexpr int MAX_BFLY = 24;     // butterflies per pass (fused mode)
+constexpr int MAX_OPS = 128;     // ops per pass (incl. compiler-placed flushes)
+constexpr int KMAX_HI = 8;       // group slots above the warp segment per pass (storage)
+constexpr int KMAX_AOT = 4;      // ... in passes run by the ahead-of-time / direct-load kernels
+constexpr int KTILE = 7;         // ... in passes run by the complex64 tile engine (13-bit CTA tile)
+constexpr int MAX_BFLY = 64;     // butterflies per pass (fused mode)
 
 enum StepKind : int32_t { ST_PASS = 0, ST_GROW = 1, ST_SHRINK = 2, ST_SWAP = 3 };
 enum RedKind : int32_t { RED_NONE = 0, RED_NORM = 1, RED_RHO = 2 };
@@ -66,6 +68,24 @@ struct StepDesc {
   // one at local position swap_local; each rank trades half of its shard with rank ^ (1 << (g - wl))
   int32_t swap_local, swap_global;
 };
+
+// Decisions of one pass, computed once by decide_kernel and read by every CTA of the generated pass
+// kernel: the structured butterfly coefficient a = ar + i ai of each butterfly (k folded into
+// scale), as fp32 (ar, packed (-ai, ai)) and fp64, and the condition of every op.
+struct PassCoef {
+  uint64_t B[MAX_BFLY];   // complex64: packed float pair (-ai, ai)
+  double ard[MAX_BFLY];   // complex128
+  double aid[MAX_BFLY];
+  double scale;           // product of the pass's butterfly k's
+  float ar[MAX_BFLY];     // complex64
+  uint8_t cond[MAX_OPS];
+};
+
+// Grid-reduction scratch sizes (per shard): block partials and group partials (deterministic
+// two-level reduction of the generated pass kernels).
+constexpr int RED_MAX_BLOCKS = 1 << 18;
+constexpr int RED_GROUP = 256;
+constexpr int RED_MAX_GROUPS = RED_MAX_BLOCKS / RED_GROUP;
 
 // Static record of one measurement (plan order). Uploaded once per compiled plan.
 struct MStatic {

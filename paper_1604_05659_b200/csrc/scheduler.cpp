@@ -625,19 +625,28 @@ struct Packer {
   const bool eowqs;
   const int max_bfly;
   int width;
-  int kmax_hi = KMAX_HI;
+  int kmax_hi = KMAX_AOT;       // group slots per pass (ahead-of-time / direct kernels)
+  int kwide = KMAX_AOT;         // group slots per pass of width >= 13 run by the tile engine
+  // butterflies per pass on warp-lane slots (cross-lane shuffles, ~4x the cost of a butterfly on a
+  // register slot): capped for HBM-resident states so that no pass turns instruction-bound; the
+  // deferred lane work lands in passes with idle issue slots (L2-resident states are launch-bound:
+  // no cap, fewest passes)
+  int max_lane_bfly = -1;
   const int n_global;         // log2(ranks); positions >= width - n_global are rank bits
   std::vector<int> pos, at;   // virtual slot -> physical position, and back
 
   Packer(const std::vector<LOp>& o, Program& p, int sb, bool e, int mb, int ng)
       : ops(o), mst(p.mst), pr(p), SB(sb), eowqs(e), max_bfly(mb), width(p.in_width), n_global(ng) {
-    if (const char* env = getenv("OWQS_KMAX_HI")) kmax_hi = std::max(0, std::min(KMAX_HI, atoi(env)));
+    if (const char* env = getenv("OWQS_KMAX_HI")) kmax_hi = std::max(0, std::min(KMAX_AOT, atoi(env)));
+    if (const char* env = getenv("OWQS_MAX_LANE_BFLY")) max_lane_bfly = std::max(1, atoi(env));
     for (int v = 0; v < 64; ++v) {
       pos.push_back(v);
       at.push_back(v);
     }
   }
   int wl() const { return width - n_global; }
+  // group slots allowed in a pass of (shard) width w
+  int wide_at(int w) const { return (kwide > KMAX_AOT && SB == 6 && w >= 13) ? kwide : kmax_hi; }
   // last step that computes something (a SWAP only permutes: it preserves the norm)
   StepDesc* last_compute() {
     for (int i = (int)pr.steps.size() - 1; i >= 0; --i)
@@ -825,8 +834,15 @@ struct Packer {
     for (int i = 0; i < N; ++i)
       if (nodes[i].npred == 0) ready.push_back(i);
     int remaining = N;
+    auto is_lane = [&](int a) { return a < SB && !(SB == 6 && a == 0); };
+    // tile engine (complex64, width >= 13): up to kwide group slots; lane slots reach registers
+    // through shared-memory transposes, so no lane cap
+    const bool wide = wide_at(wl()) > KMAX_AOT;
+    const int kmax = wide_at(wl());
+    const int lane_cap = max_lane_bfly > 0 ? max_lane_bfly : (!wide && wl() + (SB == 6 ? 3 : 4) >= 28 ? 4 : 64);
     while (remaining > 0) {
       StepDesc cur = blank(ST_PASS);
+      int n_lane = 0;
       const int WL = wl();
       auto has_slot = [&](int a) {
         if (a < SB) return true;
@@ -842,12 +858,13 @@ struct Packer {
           const Node& n = nodes[ready[k]];
           const LOp& l = ops[n.op];
           if (l.type == 4 && cur.n_bfly >= max_bfly) continue;
+          if (l.type == 4 && is_lane(pos[l.a]) && n_lane >= lane_cap) continue;
           const bool diag = l.type == 1 || l.type == 2;
           if (!diag && pos[l.a] >= WL) continue;  // 2x2 on a rank bit: needs a SWAP first
           bool fits = diag || has_slot(pos[l.a]);
           if (fits) {
             if (best < 0 || n.op < nodes[ready[best]].op) best = k;
-          } else if (cur.nb_hi < kmax_hi) {
+          } else if (cur.nb_hi < kmax) {
             if (best_new < 0 || n.op < nodes[ready[best_new]].op) best_new = k;
           }
         }
@@ -871,6 +888,7 @@ struct Packer {
           push_sig(o, n.xsig);  // cond/sig of a butterfly = folded X_a^s
           if (cur.n_bfly == 0 && !eowqs) cur.first_uses_red = 1;
           ++cur.n_bfly;
+          if (is_lane(pos[l.a])) ++n_lane;
         } else {
           push_sig(o, l.sig);
         }
@@ -938,7 +956,7 @@ struct Packer {
         if (!eowqs) {  // rho of the measured slot from the last pass (or a read-only pass)
           StepDesc* last = pr.steps.empty() ? nullptr : &pr.steps.back();
           bool room = last && last->kind == ST_PASS && last->red_kind == RED_NONE && last->width == width &&
-                      (l.a < SB || last->nb_hi < kmax_hi ||
+                      (l.a < SB || last->nb_hi < wide_at(last->width) ||
                        std::find(last->bhi, last->bhi + last->nb_hi, l.a) != last->bhi + last->nb_hi);
           if (room) {
             if (l.a >= SB && std::find(last->bhi, last->bhi + last->nb_hi, l.a) == last->bhi + last->nb_hi) {
@@ -980,7 +998,8 @@ struct Packer {
 
 }  // namespace
 
-Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse, int n_global) {
+Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse, int n_global,
+                        int kwide) {
   const bool eowqs = mode == 2;
   Emitter em(hp, eowqs);
   em.run(plan);
@@ -1002,20 +1021,22 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
     }
   }
   Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1, n_global);
+  pk.kwide = std::max(KMAX_AOT, std::min(KTILE, kwide));
+  if (const char* env = getenv("OWQS_KWIDE")) pk.kwide = std::max(KMAX_AOT, std::min(KTILE, atoi(env)));
   pk.run();
   for (int o : hp.outputs) pr.out_slot.push_back(pk.pos[em.slot_of[o]]);
   return pr;
 }
 
 void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool given, const ProaWeights& w,
-                      Plan& plan, Program& prog, int n_global) {
+                      Plan& plan, Program& prog, int n_global, int kwide) {
   if (mode != 2) {
     plan = make_plan(hp, false, given, w);
-    prog = compile_program(hp, plan, mode, SB, fuse, n_global);
+    prog = compile_program(hp, plan, mode, SB, fuse, n_global, kwide);
     return;
   }
   plan = make_plan(hp, true, given, w);
-  prog = compile_program(hp, plan, 2, SB, fuse, n_global);
+  prog = compile_program(hp, plan, 2, SB, fuse, n_global, kwide);
   Plan alt = make_plan(hp, false, given, w);
   Plan filt;
   for (int c : alt.order)
@@ -1023,7 +1044,7 @@ void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool g
   filt.m_cmds = alt.m_cmds;
   filt.ms = alt.ms;
   filt.paper_m = alt.paper_m;
-  Program ap = compile_program(hp, filt, 2, SB, fuse, n_global);
+  Program ap = compile_program(hp, filt, 2, SB, fuse, n_global, kwide);
   if (!prog.error.empty() ||
       (ap.error.empty() && (ap.phys_bits < prog.phys_bits ||
                             (ap.phys_bits == prog.phys_bits && ap.n_passes + ap.n_swaps < prog.n_passes + prog.n_swaps)))) {

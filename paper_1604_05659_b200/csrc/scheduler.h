@@ -66,14 +66,16 @@ struct Program {
 };
 
 // mode: 0 sampled / 1 forced (OWQS) or 2 EOWQS. seg_bits: 6 for complex64, 5 for complex128.
+// kwide: group slots per pass for passes of width >= 13 (complex64 tile engine, up to KMAX_HI);
+// narrower passes and the ahead-of-time kernels use KMAX_AOT.
 Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int seg_bits, bool fuse,
-                        int n_global = 0);
+                        int n_global = 0, int kwide = KMAX_AOT);
 
 // Plan + compile for a mode. For EOWQS two candidates are compiled — PROA without dependencies
 // and the OWQS plan with its (identity) corrections dropped — and the one with the
 // smaller physical width, then fewer passes, is kept.
 void plan_and_compile(const HostPattern& hp, int mode, int seg_bits, bool fuse, bool given_order,
-                      const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0);
+                      const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0, int kwide = KMAX_AOT);
 
 // gflow of the pattern's open graph ([25]): "" if found, else the reason. layer[q] = 0
 // for outputs, k >= 1 for the k-th backward layer; g[q] = correction set of measured q.

@@ -77,7 +77,9 @@ class Simulator:
         h = C.c_void_p()
         st = self._lib.owqs_create(C.byref(cfg), C.byref(h))
         if st != 0:
-            raise OwqsError(st, "owqs_create failed (CUDA device visible? NCCL id / rank valid?)")
+            why = self._lib.owqs_last_error(None)
+            raise OwqsError(st, "owqs_create failed (CUDA device visible? NCCL id / rank valid?) " +
+                            (why.decode() if why else ""))
         self.n_ranks, self.rank = n_ranks, rank
         self._h = h
         self.precision = precision
