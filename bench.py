@@ -351,35 +351,68 @@ def run_ours(args, rank, world, local_rank):
     hbm_gbs = st["bytes_per_run"] * (1 if shard else 1) / (ms_per_step / 1e3) / 1e9  # per GPU
 
     # ---- roofline of the dominant kernel: per-launch CUDA events over profiled runs ----
+    # A state pass moves 2S bytes (S = 2^w amplitudes x 8/16 B; S for a read-only reduction pass) and
+    # issues, per amplitude, 4 FP32-pipe lane-ops per butterfly (y = a x1: FMUL2 + FFMA2 per pair;
+    # x0 +- y: 2 FADD2 per pair), 2 for the normalisation scale, 2 (norm) or 4 (rho) for the
+    # probability reduction. Its roofline time is max(bytes / HBM peak, ops / FP32
+    # peak); light passes are HBM-bound, heavy ones FP32-bound.
     peak, peak_src = peaks()
+    fp_peak = 148 * 128 * 1.965e9  # FP32 lanes x SMs x max SM clock (B200_PROFILING.md unit counts)
     prof = make_sim(FLAG_PROFILE)
     prof.load(pattern)
-    agg = {}
+    per_step = None
+    runs = 0
     for r in range(3):
         set_input(prof, r)
         prof.run(mode, seed=77 + r, want=False)
         if r == 0:
             continue  # first run captures the graph
         kc, by, tm = prof.launch_profile()
-        for c in set(kc.tolist()):
-            m = kc == c
-            a = agg.setdefault(int(c), [0.0, 0.0, 0])
-            a[0] += float(by[m].sum())
-            a[1] += float(tm[m].sum())
-            a[2] += int(m.sum())
+        per_step = (kc, by, tm.astype(np.float64)) if per_step is None else (kc, by, per_step[2] + tm)
+        runs += 1
     prof_step_ms = prof.stats()["last_run_ms"]
     prof.close()
+    kc, by, tm = per_step[0], per_step[1], per_step[2] / runs
+    from paper_1604_05659_b200.host import compile_host
+    hp = compile_host(pattern, "eowqs" if mode == "eowqs" else "sampled", prec, args.flags,
+                      n_ranks=n_shards if (shard or loop > 1) else 1)
+    ops = np.zeros(len(kc))
+    for i, sd in enumerate(hp.steps[:len(kc)]):
+        if sd.kind == 0:  # state pass
+            amps = float(2 ** sd.width) * n_shards / (n_shards if shard else 1)
+            per_amp = 4 * sd.n_bfly + (2 if sd.n_bfly else 0) + {0: 0, 1: 2, 2: 4}[sd.red_kind]
+            ops[i] = amps * per_amp
+    agg = {}
+    for c in set(kc.tolist()):
+        m = kc == c
+        agg[int(c)] = [float(by[m].sum()), float(tm[m].sum()), int(m.sum()), float(ops[m].sum())]
     dom = max(agg, key=lambda c: agg[c][1])
-    by_sum, ms_sum, cnt = agg[dom]
-    achieved = by_sum / (ms_sum / 1e3) / 1e9  # bytes of all shards on this GPU / their time
+    by_sum, ms_sum, cnt, ops_sum = agg[dom]
+    m = kc == dom
+    t_mem = by[m] / (peak * 1e9) * 1e3
+    t_fp = ops[m] / fp_peak * 1e3
+    roof_ms = float(np.maximum(t_mem, t_fp).sum())
+    bw = by_sum / (ms_sum / 1e3) / 1e9
+    fp = ops_sum / (ms_sum / 1e3)
+    hbm_bound = t_mem.sum() >= t_fp.sum()
     traffic = ncu_traffic()
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+    roofline = {"bound": "hbm" if hbm_bound else "alu",
+                "achieved": bw if hbm_bound else fp / 1e12, "peak": peak if hbm_bound else fp_peak / 1e12,
+                "unit": "GB/s" if hbm_bound else "Tlane-op/s",
+                "frac": bw / peak if hbm_bound else fp / fp_peak,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
-                "kernel": f"owqs::{KCLASS_NAMES[dom]}_kernel", "launches": cnt,
+                "kernel": f"owqs::{KCLASS_NAMES[dom]}_kernel (generated tile kernels)", "launches": cnt,
                 "bytes_per_launch": by_sum / cnt, "avg_launch_us": 1e3 * ms_sum / cnt,
-                "share_of_step": ms_sum / 2 / prof_step_ms if prof_step_ms else None,
-                "per_class_ms": {KCLASS_NAMES[c]: v[1] / 2 for c, v in agg.items()},
-                "peak_source": peak_src, "algorithmic_bytes": "read + write of the 2^w-amplitude state per pass"}
+                "share_of_step": ms_sum / prof_step_ms if prof_step_ms else None,
+                "per_class_ms": {KCLASS_NAMES[c]: v[1] for c, v in agg.items()},
+                "peak_source": peak_src, "algorithmic_bytes": "read + write of the 2^w-amplitude state per pass",
+                "hbm": {"achieved_gbs": bw, "peak_gbs": peak, "frac": bw / peak,
+                        "roofline_ms": float(t_mem.sum())},
+                "alu": {"achieved_tops": fp / 1e12, "peak_tops": fp_peak / 1e12, "frac": fp / fp_peak,
+                        "unit": "FP32-pipe lane-ops/s (FFMA2/FMUL2/FADD2 count 2)", "roofline_ms": float(t_fp.sum()),
+                        "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz"},
+                "per_pass_roofline_frac": roof_ms / ms_sum,
+                "per_pass_roofline_note": "sum over passes of max(bytes/HBM peak, lane-ops/FP32 peak) over measured time"}
 
     # ---- e2e through the C-ABI with host buffers (pinned), H2D + D2H inside the timed region ----
     e2e = None
@@ -451,7 +484,7 @@ def run_ours(args, rank, world, local_rank):
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": st["n_launches"] * args.steps,
+        "gpu_launches": int(round(st.get("n_kernels") or st["n_launches"])) * args.steps * n_shards // (n_shards if shard else 1),
         "clocks": clocks,
     }
     sim.close()

@@ -125,7 +125,9 @@ typedef struct {
   double jit_ms;             /* host time generating + NVRTC-compiling the pass kernels of
                                 both modes at load_pattern (0 when all came from the cache)    */
   double n_jit_steps;        /* steps of the last mode's program run by generated kernels    */
-  double reserved[2];
+  double n_kernels;          /* kernel launches per owqs_run of the last mode (steps + the
+                                decision kernels of tile-engine passes), per shard            */
+  double reserved[1];
 } owqs_stats_t;
 
 /* Create / destroy a context on cfg->device.

@@ -42,7 +42,7 @@ class owqs_stats_t(C.Structure):
                 ("n_shrink", C.c_int32), ("n_reduce", C.c_int32), ("n_launches", C.c_int32),
                 ("n_swaps", C.c_int32), ("bytes_per_run", C.c_double), ("last_run_ms", C.c_double),
                 ("schedule_ms", C.c_double), ("jit_ms", C.c_double), ("n_jit_steps", C.c_double),
-                ("reserved", C.c_double * 2)]
+                ("n_kernels", C.c_double), ("reserved", C.c_double * 1)]
 
 
 assert C.sizeof(owqs_cmd) == 40

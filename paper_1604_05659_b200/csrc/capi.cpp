@@ -117,6 +117,17 @@ struct owqs_ctx {
 
 namespace {
 
+// kernel launches of one run (per shard): every step, plus the decide kernel of each tile pass
+double kernels_per_run(const owqs_ctx* ctx, const CompiledMode& m) {
+  double n = 0;
+  for (size_t i = 0; i < m.prog.steps.size(); ++i) {
+    const StepDesc& s = m.prog.steps[i];
+    n += 1;
+    if (i < m.jit_name.size() && !m.jit_name[i].empty() && jit_engine(s, ctx->prec) == 2) n += 1;
+  }
+  return n;
+}
+
 owqs_status fail(owqs_ctx* c, owqs_status s, const std::string& m) {
   if (c) c->err = m;
   return s;
@@ -751,6 +762,7 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
   ctx->stats.schedule_ms = ctx->cm[0].schedule_ms;
   ctx->stats.jit_ms = ctx->jit_ms;
   ctx->stats.n_jit_steps = ctx->cm[0].n_jit;
+  ctx->stats.n_kernels = kernels_per_run(ctx, ctx->cm[0]);
   if (pr.phys_bits - ctx->n_global > 40) return fail(ctx, OWQS_E_NOMEM, "shard width above 40 bits");
   ctx->loaded = true;
   return OWQS_OK;
@@ -869,6 +881,7 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   ctx->stats.schedule_ms = ctx->cm[cmi].schedule_ms;
   ctx->stats.jit_ms = ctx->jit_ms;
   ctx->stats.n_jit_steps = ctx->cm[cmi].n_jit;
+  ctx->stats.n_kernels = kernels_per_run(ctx, ctx->cm[cmi]);
   ctx->stats.phys_bits = pr.phys_bits;
   if (mode == OWQS_EOWQS) {
     double red[4];

@@ -652,6 +652,13 @@ struct Gen {
   std::vector<std::vector<int>> preds;
   std::vector<int> op_tb;  // tile bit an op needs in registers (-1: none)
   uint64_t tile_iters = 1;
+  // CTAs per SM the tile kernel is compiled for (register cap 65536 / (256 * minb)). 2: measured on
+  // C3, 3 (80 registers) is 18% slower (serialised loads)
+  static int tile_minb() {
+    const char* e = getenv("OWQS_TILE_MINB");
+    return e ? std::max(1, std::min(3, atoi(e))) : 2;
+  }
+  int n_local_ = 0, n_cta_ = 0;
 
   void build_dag() {
     const int n = d.n_ops;
@@ -704,41 +711,55 @@ struct Gen {
     }
     return out;
   }
+  // Phases: each picks, among all C(12, 4) register sets (t0 + 4 of t1..t12), the one that runs the
+  // most ready ops (ties: fewer bits outside the pass's preferred warp bits, then A-type sets).
   std::vector<Phase> plan_greedy(bool first_group_only) const {
     std::vector<Phase> ph;
     std::vector<char> done(n_ops_ + 1, 0);
     int left = n_ops_ + 1;
     bool first = true;
     while (left > 0) {
-      Phase P_;
-      unsigned regs = 1u;  // t0
-      for (int k = 0; k < 4; ++k) {
-        int best = -1;
-        size_t bestn = 0;
-        for (int b = 1; b < kTileBits; ++b) {
-          if ((regs >> b) & 1) continue;
-          if (first && first_group_only && b < 6) continue;
-          const size_t nn = closure(regs | (1u << b), done).size();
-          // prefer more ops, then group bits (keeps A-type layouts), then the lowest bit
-          const bool better = best < 0 || nn > bestn || (nn == bestn && (b >= 6) && best < 6);
-          if (better) {
-            best = b;
-            bestn = nn;
-          }
-        }
-        regs |= 1u << best;
-        P_.S[k] = best;
-      }
-      P_.ops = closure(regs, done);
-      if (P_.ops.empty()) return {};  // cannot happen (every op's slot is a tile bit)
-      for (int i : P_.ops) done[i] = 1;
-      left -= (int)P_.ops.size();
-      std::sort(P_.S, P_.S + 4);
-      ph.push_back(P_);
+      Phase best{};
+      long best_score = -1;
+      for (int a = 1; a < kTileBits; ++a)
+        for (int b = a + 1; b < kTileBits; ++b)
+          for (int c = b + 1; c < kTileBits; ++c)
+            for (int e = c + 1; e < kTileBits; ++e) {
+              const int S[4] = {a, b, c, e};
+              if (first && first_group_only && !a_type(S)) continue;
+              const unsigned regs = 1u | (1u << a) | (1u << b) | (1u << c) | (1u << e);
+              if (regs & warp_pref) continue;  // keep the pass's warp bits out of registers
+              std::vector<int> cl = closure(regs, done);
+              const long score = (long)cl.size() * 4 + (a_type(S) ? 1 : 0);
+              if (score > best_score) {
+                best_score = score;
+                for (int k = 0; k < 4; ++k) best.S[k] = S[k];
+                best.ops = cl;
+              }
+            }
+      if (best.ops.empty()) return {};
+      for (int i : best.ops) done[i] = 1;
+      left -= (int)best.ops.size();
+      ph.push_back(best);
       first = false;
     }
-    // merge a trailing phase's register set into its predecessor when it needs no new bits
     return ph;
+  }
+  // the pass's warp bits: the 3 group tile bits with the fewest non-diagonal ops (untouched padding
+  // slots first), so that phase changes keep them and transpose within each warp
+  unsigned warp_pref = 0;
+  void choose_warp_bits() {
+    std::vector<int> use(kTileBits, 0);
+    for (int i = 0; i <= n_ops_; ++i)
+      if (op_tb[i] >= 0) ++use[op_tb[i]];
+    std::vector<int> cand;
+    for (int b = 6; b < kTileBits; ++b) cand.push_back(b);
+    std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return use[x] < use[y]; });
+    warp_pref = 0;
+    for (int k = 0; k < 3; ++k) warp_pref |= 1u << cand[k];
+    // a bit needed in registers by some op cannot be a warp bit for the whole pass: drop it
+    for (int k = 0; k < 3; ++k)
+      if (use[cand[k]] > 0) warp_pref &= ~(1u << cand[k]);
   }
   static bool a_type(const int* S) {
     for (int k = 0; k < 4; ++k)
@@ -757,22 +778,35 @@ struct Gen {
     CLayout L;
     L.R[0] = 0;
     for (int k = 0; k < 4; ++k) L.R[k + 1] = S[k];
-    if (a_type(S)) {
-      for (int j = 0; j < 5; ++j) L.Lb[j] = j + 1;
-      int w = 0;
-      for (int b = 6; b < kTileBits; ++b) {
-        bool in = false;
-        for (int k = 0; k < 4; ++k) in = in || S[k] == b;
-        if (!in) L.Wb[w++] = b;
+    auto in_s = [&](int b) {
+      for (int k = 0; k < 4; ++k)
+        if (S[k] == b) return true;
+      return false;
+    };
+    // warp bits: the pass's preferred ones first (ascending), then the highest free group bits
+    int w = 0;
+    for (int b = 6; b < kTileBits && w < 3; ++b)
+      if (((warp_pref >> b) & 1) && !in_s(b)) L.Wb[w++] = b;
+    for (int b = kTileBits - 1; b >= 6 && w < 3; --b) {
+      bool taken = in_s(b);
+      for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
+      if (!taken) L.Wb[w++] = b;
+    }
+    if (w < 3)  // S holds 4 group bits and the preferred set overlaps: any remaining bits
+      for (int b = kTileBits - 1; b >= 1 && w < 3; --b) {
+        bool taken = in_s(b);
+        for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
+        if (!taken) L.Wb[w++] = b;
       }
+    std::sort(L.Wb, L.Wb + 3);
+    auto in_w = [&](int b) { return b == L.Wb[0] || b == L.Wb[1] || b == L.Wb[2]; };
+    if (a_type(S) && !in_w(1) && !in_w(2) && !in_w(3) && !in_w(4) && !in_w(5)) {
+      for (int j = 0; j < 5; ++j) L.Lb[j] = j + 1;
       return L;
     }
     std::vector<int> rest;
-    for (int b = 1; b < kTileBits; ++b) {
-      bool in = false;
-      for (int k = 0; k < 4; ++k) in = in || S[k] == b;
-      if (!in) rest.push_back(b);
-    }
+    for (int b = 1; b < kTileBits; ++b)
+      if (!in_s(b) && !in_w(b)) rest.push_back(b);
     // lane bits 0..2: one tile bit of each bank class (k - 1) mod 3, lowest first
     std::vector<char> used(rest.size(), 0);
     for (int c = 0; c < 3; ++c) {
@@ -791,14 +825,9 @@ struct Gen {
       used[pick] = 1;
       L.Lb[c] = rest[pick];
     }
-    int j = 3, w = 0;
-    for (size_t i = 0; i < rest.size(); ++i) {
-      if (used[i]) continue;
-      if (j < 5)
-        L.Lb[j++] = rest[i];
-      else
-        L.Wb[w++] = rest[i];
-    }
+    int j = 3;
+    for (size_t i = 0; i < rest.size(); ++i)
+      if (!used[i] && j < 5) L.Lb[j++] = rest[i];
     return L;
   }
   int treg(const CLayout& L, int p) const {
@@ -825,15 +854,19 @@ struct Gen {
     o << "    // layout " << lay << " -> " << to << " (shared-memory tile)\n";
     const CLayout& A = lays[lay];
     const CLayout& B = lays[to];
+    // warp bits unchanged: every warp exchanges only its own amplitudes (warp-local barrier)
+    const bool local = !memcmp(A.Wb, B.Wb, sizeof A.Wb);
+    const char* bar = local ? "    __syncwarp();\n" : "    __syncthreads();\n";
     for (int p = 0; p < P; p += 2)
       o << "    *reinterpret_cast<float4*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_float4(lo("
         << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
-    o << "    __syncthreads();\n";
+    o << bar;
     for (int p = 0; p < P; p += 2)
       o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
         << "); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
     for (int p = 0; p < P; ++p) perm[p] = p;
-    if (!last || tile_iters > 1) o << "    __syncthreads();\n";
+    if (!last || tile_iters > 1) o << bar;
+    ++(local ? n_local_ : n_cta_);
     lay = to;
   }
 
@@ -848,6 +881,7 @@ struct Gen {
     const uint64_t iters = nbu > (uint64_t)RED_MAX_BLOCKS ? nbu / RED_MAX_BLOCKS : 1;
     tile_iters = iters;
     build_dag();
+    choose_warp_bits();
     std::vector<Phase> pa = plan_greedy(true), pb = plan_greedy(false);
     const std::vector<Phase>& ph = n_transitions(pb) < n_transitions(pa) ? pb : pa;
     if (ph.empty()) {
@@ -857,20 +891,29 @@ struct Gen {
     // layouts: load layout, phase layouts, store layout
     std::vector<int> plays;
     for (const Phase& f : ph) plays.push_back(add_layout(make_layout(f.S)));
-    const int l_load = a_type(ph.front().S) ? plays.front() : add_layout(make_layout(std::array<int, 4>{6, 7, 8, 9}.data()));
-    const int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(std::array<int, 4>{6, 7, 8, 9}.data()));
+    // global IO layout when a phase is not A-type: the A-type layout keeping the preferred warp bits
+    int sa[4] = {6, 7, 8, 9};
+    if (__builtin_popcount(warp_pref) == 3) {
+      int k = 0;
+      for (int b = 6; b < kTileBits; ++b)
+        if (!((warp_pref >> b) & 1)) sa[k++] = b;
+    }
+    const int l_load = a_type(ph.front().S) ? plays.front() : add_layout(make_layout(sa));
+    const int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(sa));
     int n_trans = 0;
     {
       int cur = l_load;
       for (int l : plays) n_trans += l != cur, cur = l;
       n_trans += l_store != cur;
     }
-    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * kNW << ", 2) OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* __restrict__ pc) {\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * kNW << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* __restrict__ pc) {\n"
       << "  using namespace owqs;\n"
       << "  // tile engine: width " << d.width << ", tile group slots";
     for (int j = 0; j < KTILE; ++j) o << " " << gs[j];
     o << " (pass's " << d.nb_hi << "), " << d.n_ops << " ops, " << nbf << " butterflies, reduction " << red << ", "
-      << ph.size() << " phase(s), " << n_trans << " transpose(s), " << iters << " tile(s) per CTA\n";
+      << ph.size() << " phase(s), " << n_trans << " transpose(s), " << iters << " tile(s) per CTA, warp bits";
+    for (int j = 0; j < 3; ++j) o << " t" << lays[l_load].Wb[j];
+    o << "\n";
     for (size_t f = 0; f < ph.size(); ++f) {
       o << "  // phase " << f << ": registers t0";
       for (int k = 0; k < 4; ++k) o << " t" << ph[f].S[k];

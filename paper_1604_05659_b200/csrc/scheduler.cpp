@@ -623,7 +623,7 @@ struct Packer {
   Program& pr;
   const int SB;
   const bool eowqs;
-  const int max_bfly;
+  int max_bfly;
   int width;
   int kmax_hi = KMAX_AOT;       // group slots per pass (ahead-of-time / direct kernels)
   int kwide = KMAX_AOT;         // group slots per pass of width >= 13 run by the tile engine
@@ -1022,6 +1022,7 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
   }
   Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1, n_global);
   pk.kwide = std::max(KMAX_AOT, std::min(KTILE, kwide));
+  if (const char* env = getenv("OWQS_MAX_BFLY")) pk.max_bfly = std::max(1, std::min(MAX_BFLY, atoi(env)));
   if (const char* env = getenv("OWQS_KWIDE")) pk.kwide = std::max(KMAX_AOT, std::min(KTILE, atoi(env)));
   pk.run();
   for (int o : hp.outputs) pr.out_slot.push_back(pk.pos[em.slot_of[o]]);

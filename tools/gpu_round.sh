@@ -1,6 +1,4 @@
-timeout 1200 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo pt=$?
-tail -15 gpurun_out/pytest_gpu.log | cut -c1-300
-timeout 300 python tools/pass_profile.py --workload C3 --out gpurun_out/pp_c3_e3.json > gpurun_out/pp_c3_e3.log 2>&1; echo pp=$?
-head -1 gpurun_out/pp_c3_e3.log | cut -c1-100
-timeout 600 python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/b_c3_e3.log 2>&1; echo b1=$?
-tail -1 gpurun_out/b_c3_e3.log | cut -c1-200
+timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo b=$?
+tail -1 gpurun_out/bench_default.log
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c3_tile.csv python tools/prof_run.py --workload C3 > gpurun_out/ncu_ll.log 2>&1; echo ll=$?
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:owqs_tma_c64 --launch-skip 20 --launch-count 1 -o gpurun_out/ncu_tile_c3_p20 python tools/prof_run.py --workload C3 > gpurun_out/ncu_t.log 2>&1; echo t=$?

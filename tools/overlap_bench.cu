@@ -1,0 +1,134 @@
+// Overlap of HBM streaming with FP32 work, for the tile engine's execution scheme (2 GiB state,
+// in place, 8192-amplitude tiles of 16 KB... 64 KB): time vs synthetic FFMA2 per amplitude.
+//   np   : non-persistent grid, one tile per CTA (8 warps, 32 amps/thread), LDG -> FMA -> STG
+//   tma  : persistent, 1 CTA/SM, tile k+1 bulk-copied (cp.async.bulk) into smem while tile k computes
+// nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o /tmp/ob tools/overlap_bench.cu && /tmp/ob
+#include <cuda_runtime.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+typedef unsigned long long u64;
+__device__ __forceinline__ u64 pk(float a, float b) { u64 r; asm("mov.b64 %0, {%1,%2};" : "=l"(r) : "f"(a), "f"(b)); return r; }
+__device__ __forceinline__ float lo(u64 r) { float a, b; asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); return a; }
+__device__ __forceinline__ float hi(u64 r) { float a, b; asm("mov.b64 {%0,%1}, %2;" : "=f"(a), "=f"(b) : "l"(r)); return b; }
+__device__ __forceinline__ u64 fma2(u64 a, u64 b, u64 c) { u64 r; asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c)); return r; }
+
+template <int K>
+__device__ __forceinline__ void work(u64 (&x)[32], u64 c) {
+#pragma unroll
+  for (int k = 0; k < K; ++k)
+#pragma unroll
+    for (int p = 0; p < 32; ++p) x[p] = fma2(x[p], c, x[(p + 1) & 31]);
+}
+
+// tile = 16 segments x 8 warps? Here: tile of 8192 amps = 64 KB contiguous; warp w, lane l, reg p
+// -> float4 index (w * 16 + p/2) * 32 + l (coalesced 512 B per warp instruction)
+template <int K>
+__global__ void __launch_bounds__(256, 2) np_k(float4* __restrict__ a, u64 c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float4* t = a + (size_t)blockIdx.x * 4096;
+  u64 x[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float4 v = __ldcs(t + (warp * 16 + q) * 32 + lane);
+    x[2 * q] = pk(v.x, v.y);
+    x[2 * q + 1] = pk(v.z, v.w);
+  }
+  work<K>(x, c);
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    __stcs(t + (warp * 16 + q) * 32 + lane, make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned a, unsigned n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned tx) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(tx) : "memory"); }
+__device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) {
+  unsigned done;
+  do { asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.b32 %0, 1, 0, P1; }" : "=r"(done) : "r"(a), "r"(par) : "memory"); } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+}
+
+// persistent, 1 CTA/SM, 2 smem stages of one tile (64 KB each); thread 0 issues 4 x 16 KB bulk copies
+template <int K>
+__global__ void __launch_bounds__(256, 1) tma_k(float4* __restrict__ a, u64 c, int ntiles) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) unsigned long long mb[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned sm_s = (unsigned)__cvta_generic_to_shared(sm), mb_s = (unsigned)__cvta_generic_to_shared(mb);
+  if (threadIdx.x == 0) {
+    mbar_init(mb_s, 1);
+    mbar_init(mb_s + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int tile, int s) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(mb_s + 8 * s, 65536u);
+      for (int j = 0; j < 4; ++j)
+        bulk_g2s(sm_s + s * 65536 + j * 16384, (const char*)(a + (size_t)tile * 4096) + j * 16384, 16384u, mb_s + 8 * s);
+    }
+  };
+  int k = 0;
+  if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = k & 1;
+    const int nxt = tile + gridDim.x;
+    mbar_wait(mb_s + 8 * s, (k >> 1) & 1);
+    const float4* st = reinterpret_cast<const float4*>(sm + s * 65536);
+    u64 x[32];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const float4 v = st[(warp * 16 + q) * 32 + lane];
+      x[2 * q] = pk(v.x, v.y);
+      x[2 * q + 1] = pk(v.z, v.w);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();  // everyone done reading stage s^1's previous content? (stage s read done)
+    if (nxt < ntiles) issue(nxt, s ^ 1);  // next tile into the other stage
+    work<K>(x, c);
+    float4* t = a + (size_t)tile * 4096;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      __stcs(t + (warp * 16 + q) * 32 + lane, make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
+  }
+}
+
+int main() {
+  const size_t bytes = 2ull << 30, n4 = bytes / 16;
+  const int ntiles = (int)(n4 / 4096);
+  float4* a;
+  cudaMalloc(&a, bytes);
+  cudaMemset(a, 0, bytes);
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const u64 c = 0x3f8000003f800000ull;
+  auto run = [&](const char* name, int K, auto f) {
+    f();
+    cudaDeviceSynchronize();
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      f();
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (ms < best) best = ms;
+    }
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(err)); exit(1); }
+    const double fp_ms = (double)K * 2.0 * (bytes / 8) / (148.0 * 128 * 1.9e9) * 1e3;  // FFMA2 = 2 lane-ops
+    printf("%-6s K=%3d FFMA2/amp  %7.3f ms  (%6.1f GB/s; FP-only floor %.3f ms)\n", name, K, best, 2.0 * bytes / best / 1e6, fp_ms);
+  };
+#define BOTH(K)                                                                                  \
+  run("np", K, [&] { np_k<K><<<ntiles, 256>>>(a, c); });                                        \
+  cudaFuncSetAttribute(tma_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 65536);       \
+  run("tma", K, [&] { tma_k<K><<<sms, 256, 2 * 65536>>>(a, c, ntiles); });
+  BOTH(0) BOTH(8) BOTH(16) BOTH(24) BOTH(32) BOTH(48) BOTH(64) BOTH(96)
+  return 0;
+}
