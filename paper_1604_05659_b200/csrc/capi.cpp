@@ -195,7 +195,7 @@ owqs_status compile_modes(owqs_ctx* ctx) {
     auto t0 = std::chrono::steady_clock::now();
     CompiledMode& m = ctx->cm[i];
     plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog, ctx->n_global,
-                     (ctx->prec == 0 && !(ctx->cfg.flags & OWQS_FLAG_NO_JIT)) ? KTILE : KMAX_AOT);
+                     jit_max_group(ctx->prec, (ctx->cfg.flags & OWQS_FLAG_NO_JIT) != 0));
     if (!m.prog.error.empty()) return fail(ctx, OWQS_E_ARG, m.prog.error);
     m.schedule_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     m.valid = true;
@@ -298,7 +298,7 @@ owqs_status ensure_device(owqs_ctx* ctx) {
           if (dyn > 0)
             CU(cudaFuncSetAttribute((const void*)fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
           int nb = 0;
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], eng == 2 ? 256 : 256, dyn));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], jit_block_threads(eng), dyn));
           blocks[k] = std::max(1, nb) * sms;
         }
       }

@@ -47,7 +47,7 @@ owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t
   if (flags & OWQS_FLAG_NO_TUNE) w.tune = false;
   plan_and_compile(h->hp, mode, precision == 64 ? 6 : 5, !(flags & OWQS_FLAG_NO_FUSE),
                    (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w, h->plan, h->prog, n_global,
-                   (precision == 64 && !(flags & OWQS_FLAG_NO_JIT)) ? KTILE : KMAX_AOT);
+                   jit_max_group(precision == 64 ? 0 : 1, (flags & OWQS_FLAG_NO_JIT) != 0));
   h->elem = precision == 64 ? 8 : 16;
   if (!h->prog.error.empty()) {
     h->err = h->prog.error;

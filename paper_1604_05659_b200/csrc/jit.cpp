@@ -53,6 +53,7 @@ static __device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 r; asm("mul.rn.f3
 static __device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 static __device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
 static __device__ __forceinline__ u64 shfl2(u64 x, int m) { return pk(__shfl_xor_sync(0xffffffffu, lo(x), m), __shfl_xor_sync(0xffffffffu, hi(x), m)); }
+static __device__ __forceinline__ u64 neg2(u64 x) { return pk(-lo(x), -hi(x)); }
 static __device__ __forceinline__ u64 flip2(u64 x, unsigned f) { return x ^ (((u64)f << 63) | ((u64)f << 31)); }
 static __device__ __forceinline__ void mbar_init(unsigned a, unsigned n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory"); }
 static __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -98,11 +99,24 @@ enum SlotKind { SK_REG, SK_LANE, SK_WARP, SK_BASE, SK_RANK };
 // and tile bit k >= 1 lands in bank group 2^((k - 1) mod 3) (mod 8): a quarter-warp is
 // conflict-free when lane bits 0, 1, 2 carry tile bits of the three classes (k - 1) mod 3.
 struct CLayout {
-  int R[5];
+  int R[6];   // R[0] = t0; R[1..RB-1] used
   int Lb[5];
-  int Wb[3];
+  int Wb[3];  // Wb[0..WB-1] used
 };
-constexpr int kNW = 8;  // warps per CTA
+// Tile geometry: RB register bits per thread (2^RB amplitudes) + 5 lane bits + WB warp bits = 13.
+// RB = 5, WB = 3: 8-warp CTAs, 32 amplitudes per thread (default); RB = 6, WB = 2: 4-warp CTAs,
+// 64 amplitudes per thread (OWQS_TILE_RB=6).
+struct TileGeom {
+  int rb, wb;
+};
+inline TileGeom tile_geom() {
+  static const TileGeom g = [] {
+    const char* e = getenv("OWQS_TILE_RB");
+    const int rb = (e && atoi(e) == 6) ? 6 : 5;
+    return TileGeom{rb, 8 - rb};
+  }();
+  return g;
+}
 constexpr int kTileBits = 13;
 inline int umap(int t) {
   const int v = t >> 1;
@@ -116,6 +130,7 @@ struct Gen {
   const bool tile;  // engine 2
   const int SB, EPV;
   int KHI, G, UNR, P;
+  int RB = 5, WB = 3;  // tile engine geometry
   int gs[KMAX_HI];  // group slots (engine 2: padded to KTILE)
   std::vector<CLayout> lays;  // engine 2 layouts used by this kernel
   int lay = 0;                // engine 2: current layout index
@@ -142,7 +157,9 @@ struct Gen {
       }
       if (n < KTILE) error = "tile engine needs width >= 13";
       std::sort(gs, gs + KTILE);
-      P = 32;
+      RB = tile_geom().rb;
+      WB = tile_geom().wb;
+      P = 1 << RB;
     } else {
       KHI = d.nb_hi;
       UNR = jit_unr_of(KHI);
@@ -173,7 +190,7 @@ struct Gen {
     }
     if (tile) {
       const CLayout& L = lays[l];
-      for (int k = 0; k < 5; ++k)
+      for (int k = 0; k < RB; ++k)
         if (L.R[k] == tb) {
           *bit = 1 << k;
           return SK_REG;
@@ -183,7 +200,7 @@ struct Gen {
           *bit = j;
           return SK_LANE;
         }
-      for (int j = 0; j < 3; ++j)
+      for (int j = 0; j < WB; ++j)
         if (L.Wb[j] == tb) {
           *bit = j;
           return SK_WARP;
@@ -267,7 +284,13 @@ struct Gen {
     const int ka = kind(a, &lb);
     o << "    {  // op " << i << ": butterfly " << bi << " on slot " << a << (ka == SK_REG ? " (register)" : " (lane)")
       << "\n";
-    if (tile)
+    // the pass's normalisation scale folded into its first butterfly (tile engine): out = k x0 +- (k a) x1
+    // costs the same 4 packed ops as x0 +- a x1, and saves the separate multiply of every amplitude
+    const bool fold = tile && prec == 0 && scale_pending;
+    if (fold) scale_pending = false;
+    if (fold)
+      o << "      const float ar = pc->ar[" << bi << "] * sck; const u64 cB = mul2(pc->B[" << bi << "], bc(sck));  // scale folded\n";
+    else if (tile)
       o << "      const float ar = pc->ar[" << bi << "]; const u64 cB = pc->B[" << bi << "];\n";
     else if (prec == 0)
       o << "      const float ar = s_ar[" << bi << "]; const u64 cB = s_B[" << bi << "];\n";
@@ -296,7 +319,11 @@ struct Gen {
         if (p & pb) continue;
         const int p1 = p | pb, u = unit_of(p);
         const int s = st_parity(am, p);
-        if (prec == 0) {
+        if (prec == 0 && fold) {
+          o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
+            << ")); const u64 t = " << X(p) << "; " << X(p) << " = fma2(bc(sck), t, " << (s ? "neg2(y)" : "y") << "); "
+            << X(p1) << " = fma2(bc(sck), t, " << (s ? "y" : "neg2(y)") << "); }\n";
+        } else if (prec == 0) {
           o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
             << ")); const u64 t = " << X(p) << "; " << X(p) << " = " << (s ? "sub2" : "add2") << "(t, y); " << X(p1)
             << " = " << (s ? "add2" : "sub2") << "(t, y); }\n";
@@ -321,8 +348,8 @@ struct Gen {
         for (int s = 0; s < 2; ++s) {
           if (!need[u][s]) continue;
           if (prec == 0)
-            o << "      const float c" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : 1.f; const u64 cB"
-              << u << s << " = h ? (B" << u << (s ? " ^ OWQS_SIGN2" : "") << ") : 0ull;\n";
+            o << "      const float c" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : " << (fold ? "sck" : "1.f")
+              << "; const u64 cB" << u << s << " = h ? (B" << u << (s ? " ^ OWQS_SIGN2" : "") << ") : 0ull;\n";
           else
             o << "      const double cr" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : 1.0, ci" << u << s
               << " = h ? " << (s ? "-" : "") << "ai" << u << " : 0.0;\n";
@@ -629,8 +656,9 @@ struct Gen {
     return o.str();
   }
 
+  bool scale_pending = false;
   void emit_scale(int nbf) {
-    if (nbf == 0) return;
+    if (nbf == 0 || (tile && !scale_pending)) return;
     for (int p = 0; p < P; ++p) {
       if (prec == 0)
         o << "    " << X(p) << " = mul2(scale, " << X(p) << ");\n";
@@ -645,7 +673,7 @@ struct Gen {
   // A phase = a register set (t0 + 4 tile bits) and the ops it runs; greedy: each phase picks the
   // 4 tile bits that let the most ready ops run, one bit at a time.
   struct Phase {
-    int S[4];
+    int S[5];  // S[0..RB-2]: register tile bits besides t0
     std::vector<int> ops;
   };
   int n_ops_ = 0;
@@ -656,7 +684,7 @@ struct Gen {
   // C3, 3 (80 registers) is 18% slower (serialised loads)
   static int tile_minb() {
     const char* e = getenv("OWQS_TILE_MINB");
-    return e ? std::max(1, std::min(3, atoi(e))) : 2;
+    return e ? std::max(1, std::min(4, atoi(e))) : (tile_geom().rb == 6 ? 3 : 2);
   }
   int n_local_ = 0, n_cta_ = 0;
 
@@ -721,22 +749,23 @@ struct Gen {
     while (left > 0) {
       Phase best{};
       long best_score = -1;
-      for (int a = 1; a < kTileBits; ++a)
-        for (int b = a + 1; b < kTileBits; ++b)
-          for (int c = b + 1; c < kTileBits; ++c)
-            for (int e = c + 1; e < kTileBits; ++e) {
-              const int S[4] = {a, b, c, e};
-              if (first && first_group_only && !a_type(S)) continue;
-              const unsigned regs = 1u | (1u << a) | (1u << b) | (1u << c) | (1u << e);
-              if (regs & warp_pref) continue;  // keep the pass's warp bits out of registers
-              std::vector<int> cl = closure(regs, done);
-              const long score = (long)cl.size() * 4 + (a_type(S) ? 1 : 0);
-              if (score > best_score) {
-                best_score = score;
-                for (int k = 0; k < 4; ++k) best.S[k] = S[k];
-                best.ops = cl;
-              }
-            }
+      const int nsel = RB - 1;
+      for (unsigned m = 0; m < (1u << (kTileBits - 1)); ++m) {
+        if (__builtin_popcount(m) != nsel) continue;
+        const unsigned regs = 1u | (m << 1);  // tile bits 1..12 <- m bits 0..11
+        if (regs & warp_pref) continue;       // keep the pass's warp bits out of registers
+        int S[5], n = 0;
+        for (int b = 1; b < kTileBits; ++b)
+          if ((regs >> b) & 1) S[n++] = b;
+        if (first && first_group_only && !a_type(S)) continue;
+        std::vector<int> cl = closure(regs, done);
+        const long score = (long)cl.size() * 4 + (a_type(S) ? 1 : 0);
+        if (score > best_score) {
+          best_score = score;
+          for (int k = 0; k < nsel; ++k) best.S[k] = S[k];
+          best.ops = cl;
+        }
+      }
       if (best.ops.empty()) return {};
       for (int i : best.ops) done[i] = 1;
       left -= (int)best.ops.size();
@@ -756,17 +785,17 @@ struct Gen {
     for (int b = 6; b < kTileBits; ++b) cand.push_back(b);
     std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return use[x] < use[y]; });
     warp_pref = 0;
-    for (int k = 0; k < 3; ++k) warp_pref |= 1u << cand[k];
+    for (int k = 0; k < WB; ++k) warp_pref |= 1u << cand[k];
     // a bit needed in registers by some op cannot be a warp bit for the whole pass: drop it
-    for (int k = 0; k < 3; ++k)
+    for (int k = 0; k < WB; ++k)
       if (use[cand[k]] > 0) warp_pref &= ~(1u << cand[k]);
   }
-  static bool a_type(const int* S) {
-    for (int k = 0; k < 4; ++k)
+  bool a_type(const int* S) const {
+    for (int k = 0; k < RB - 1; ++k)
       if (S[k] < 6) return false;
     return true;
   }
-  static int n_transitions(const std::vector<Phase>& ph) {
+  int n_transitions(const std::vector<Phase>& ph) const {
     if (ph.empty()) return 1 << 20;
     int t = (int)ph.size() - 1;
     if (!a_type(ph.front().S)) ++t;
@@ -777,29 +806,33 @@ struct Gen {
   CLayout make_layout(const int* S) const {
     CLayout L;
     L.R[0] = 0;
-    for (int k = 0; k < 4; ++k) L.R[k + 1] = S[k];
+    for (int k = 0; k < RB - 1; ++k) L.R[k + 1] = S[k];
     auto in_s = [&](int b) {
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < RB - 1; ++k)
         if (S[k] == b) return true;
       return false;
     };
     // warp bits: the pass's preferred ones first (ascending), then the highest free group bits
     int w = 0;
-    for (int b = 6; b < kTileBits && w < 3; ++b)
+    for (int b = 6; b < kTileBits && w < WB; ++b)
       if (((warp_pref >> b) & 1) && !in_s(b)) L.Wb[w++] = b;
-    for (int b = kTileBits - 1; b >= 6 && w < 3; --b) {
+    for (int b = kTileBits - 1; b >= 6 && w < WB; --b) {
       bool taken = in_s(b);
       for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
       if (!taken) L.Wb[w++] = b;
     }
-    if (w < 3)  // S holds 4 group bits and the preferred set overlaps: any remaining bits
-      for (int b = kTileBits - 1; b >= 1 && w < 3; --b) {
+    if (w < WB)  // S holds group bits and the preferred set overlaps: any remaining bits
+      for (int b = kTileBits - 1; b >= 1 && w < WB; --b) {
         bool taken = in_s(b);
         for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
         if (!taken) L.Wb[w++] = b;
       }
-    std::sort(L.Wb, L.Wb + 3);
-    auto in_w = [&](int b) { return b == L.Wb[0] || b == L.Wb[1] || b == L.Wb[2]; };
+    std::sort(L.Wb, L.Wb + WB);
+    auto in_w = [&](int b) {
+      for (int j = 0; j < WB; ++j)
+        if (L.Wb[j] == b) return true;
+      return false;
+    };
     if (a_type(S) && !in_w(1) && !in_w(2) && !in_w(3) && !in_w(4) && !in_w(5)) {
       for (int j = 0; j < 5; ++j) L.Lb[j] = j + 1;
       return L;
@@ -832,7 +865,7 @@ struct Gen {
   }
   int treg(const CLayout& L, int p) const {
     int t = 0;
-    for (int k = 0; k < 5; ++k)
+    for (int k = 0; k < RB; ++k)
       if ((p >> k) & 1) t |= 1 << L.R[k];
     return t;
   }
@@ -846,7 +879,7 @@ struct Gen {
   uint64_t a_seg(int l, int p) const {
     uint64_t s = 0;
     const CLayout& L = lays[l];
-    for (int k = 1; k < 5; ++k)
+    for (int k = 1; k < RB; ++k)
       if ((p >> k) & 1) s |= 1ull << (gs[L.R[k] - 6] - 6);
     return s;
   }
@@ -855,7 +888,7 @@ struct Gen {
     const CLayout& A = lays[lay];
     const CLayout& B = lays[to];
     // warp bits unchanged: every warp exchanges only its own amplitudes (warp-local barrier)
-    const bool local = !memcmp(A.Wb, B.Wb, sizeof A.Wb);
+    const bool local = !memcmp(A.Wb, B.Wb, sizeof(int) * WB);
     const char* bar = local ? "    __syncwarp();\n" : "    __syncthreads();\n";
     for (int p = 0; p < P; p += 2)
       o << "    *reinterpret_cast<float4*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_float4(lo("
@@ -892,8 +925,8 @@ struct Gen {
     std::vector<int> plays;
     for (const Phase& f : ph) plays.push_back(add_layout(make_layout(f.S)));
     // global IO layout when a phase is not A-type: the A-type layout keeping the preferred warp bits
-    int sa[4] = {6, 7, 8, 9};
-    if (__builtin_popcount(warp_pref) == 3) {
+    int sa[5] = {6, 7, 8, 9, 10};
+    if (__builtin_popcount(warp_pref) == WB) {
       int k = 0;
       for (int b = 6; b < kTileBits; ++b)
         if (!((warp_pref >> b) & 1)) sa[k++] = b;
@@ -906,17 +939,17 @@ struct Gen {
       for (int l : plays) n_trans += l != cur, cur = l;
       n_trans += l_store != cur;
     }
-    o << "extern \"C\" __global__ void __launch_bounds__(" << 32 * kNW << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* __restrict__ pc) {\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* __restrict__ pc) {\n"
       << "  using namespace owqs;\n"
       << "  // tile engine: width " << d.width << ", tile group slots";
     for (int j = 0; j < KTILE; ++j) o << " " << gs[j];
     o << " (pass's " << d.nb_hi << "), " << d.n_ops << " ops, " << nbf << " butterflies, reduction " << red << ", "
       << ph.size() << " phase(s), " << n_trans << " transpose(s), " << iters << " tile(s) per CTA, warp bits";
-    for (int j = 0; j < 3; ++j) o << " t" << lays[l_load].Wb[j];
+    for (int j = 0; j < WB; ++j) o << " t" << lays[l_load].Wb[j];
     o << "\n";
     for (size_t f = 0; f < ph.size(); ++f) {
       o << "  // phase " << f << ": registers t0";
-      for (int k = 0; k < 4; ++k) o << " t" << ph[f].S[k];
+      for (int k = 0; k < RB - 1; ++k) o << " t" << ph[f].S[k];
       o << ", " << ph[f].ops.size() << " op(s)\n";
     }
     if (n_trans) o << "  extern __shared__ __align__(16) unsigned char dsm[];\n";
@@ -924,17 +957,18 @@ struct Gen {
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  const unsigned rk = p.rank; (void)rk; (void)d;\n"
       << "  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;\n";
-    if (nbf > 0) o << "  const u64 scale = bc((float)pc->scale);\n";
+    if (nbf > 0) o << "  const float sck = (float)pc->scale;\n  const u64 scale = bc(sck); (void)scale;\n";
+    scale_pending = nbf > 0;
     if (n_trans)
       for (size_t l = 0; l < lays.size(); ++l) {
         o << "  const int sb" << l << " = 16 * (";
         for (int j = 0; j < 5; ++j) o << (j ? " + " : "") << "((lane >> " << j << ") & 1) * " << umap(1 << lays[l].Lb[j]);
-        for (int j = 0; j < 3; ++j) o << " + ((warp >> " << j << ") & 1) * " << umap(1 << lays[l].Wb[j]);
+        for (int j = 0; j < WB; ++j) o << " + ((warp >> " << j << ") & 1) * " << umap(1 << lays[l].Wb[j]);
         o << ");\n";
       }
     auto wseg = [&](int l) {
       std::string e = "(";
-      for (int j = 0; j < 3; ++j)
+      for (int j = 0; j < WB; ++j)
         e += std::string(j ? " | " : "") + "((unsigned long long)((warp >> " + std::to_string(j) + ") & 1) << " +
              std::to_string(gs[lays[l].Wb[j] - 6] - 6) + ")";
       return e + ")";
@@ -1028,6 +1062,12 @@ int jit_engine(const StepDesc& d, int prec) {
 }
 
 bool jit_eligible(const StepDesc& d, int prec) { return jit_engine(d, prec) > 0; }
+
+int jit_max_group(int prec, bool no_jit) {
+  return (prec == 0 && !no_jit && !getenv("OWQS_JIT_NO_TILE")) ? KTILE : KMAX_AOT;
+}
+
+int jit_block_threads(int engine) { return engine == 2 ? (32 << tile_geom().wb) : 256; }
 
 int jit_dyn_smem(int engine) { return engine == 2 ? kTileSmem : 0; }
 
@@ -1126,12 +1166,13 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
     const uint64_t nbu = 1ull << (d.width - kTileBits);
     const uint64_t blocks = nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu;
     void* args[] = {&dd, &pp, &pcc};
-    return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(32 * kNW), args, (size_t)jit_dyn_smem(eng), s);
+    return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(32 << tile_geom().wb), args,
+                            (size_t)jit_dyn_smem(eng), s);
   }
   const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
   const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));
   void* args[] = {&dd, &pp};
-  return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(eng == 2 ? 32 * kNW : 256), args,
+  return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(256), args,
                           (size_t)jit_dyn_smem(eng), s);
 }
 

@@ -23,10 +23,14 @@ inline int jit_unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
 // Engine of a step: 0 = not generated (ahead-of-time kernel), 1 = direct-load kernel (complex128,
 // narrow complex64), 2 = TMA-pipelined complex64 kernel with shared-memory transposes (width >= 13).
 int jit_engine(const StepDesc& d, int prec);
+// Group slots per pass the packer may use for this precision (KTILE when the tile engine runs the
+// wide passes, else KMAX_AOT).
+int jit_max_group(int prec, bool no_jit);
 // True when the step runs as a generated pass kernel.
 bool jit_eligible(const StepDesc& d, int prec);
-// Dynamic shared memory (bytes) an engine's kernels are launched with.
+// Dynamic shared memory (bytes) and threads per block an engine's kernels are launched with.
 int jit_dyn_smem(int engine);
+int jit_block_threads(int engine);
 
 // Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
 // a hash of the body (identical passes share one kernel).

@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1604_05659_b200 import FLAG_GIVEN_ORDER, FLAG_NO_FUSE, FLAG_NO_GRAPH, OwqsError, Simulator
+from paper_1604_05659_b200 import FLAG_GIVEN_ORDER, FLAG_NO_FUSE, FLAG_NO_GRAPH, FLAG_NO_JIT, OwqsError, Simulator
 from parity_util import check, fidelity, TOL
 from workloads import patterns as W
 from workloads.inputs import basis_state, counter_haar_state, haar_state
@@ -54,10 +54,12 @@ def test_qft_vs_oracle(sim, n):
     check(sim, p, psi, "eowqs")
 
 
-@pytest.mark.parametrize("flags", [0, FLAG_NO_FUSE, FLAG_NO_GRAPH, FLAG_GIVEN_ORDER | FLAG_NO_FUSE])
+@pytest.mark.parametrize("flags", [0, FLAG_NO_FUSE, FLAG_NO_GRAPH, FLAG_GIVEN_ORDER | FLAG_NO_FUSE, FLAG_NO_JIT])
 @pytest.mark.parametrize("shape", ["BW:12x8", "BW:15x5", "BW:16x3"])
 def test_brickwork_vs_oracle(require_gpu, flags, shape):
-    """Config 3/4 family at oracle-sized widths (12-16 wires: several 2^k tiles per pass)."""
+    """Config 3/4 family at oracle-sized widths (12-16 wires: several 2^k tiles per pass). Default
+    flags run the generated kernels (complex64 width >= 13: tile engine; complex128 and narrower:
+    direct engine); FLAG_NO_JIT runs the ahead-of-time op-interpreting pass kernel."""
     n = int(shape[3:].split("x")[0])
     p = W.config_pattern(shape, seed=7)
     psi = haar_state(n, 21)
@@ -69,6 +71,22 @@ def test_brickwork_vs_oracle(require_gpu, flags, shape):
             check(s, p, psi, "eowqs")
         finally:
             s.close()
+
+
+@pytest.mark.parametrize("shape", ["BW:14x6", "BW:16x4"])
+def test_direct_engine_complex64_vs_oracle(require_gpu, monkeypatch, shape):
+    """The direct-load generated engine on complex64 (OWQS_JIT_NO_TILE: passes of width >= 13 that
+    the tile engine would run), vs the oracle; the packer keeps <= 4 group slots for it."""
+    monkeypatch.setenv("OWQS_JIT_NO_TILE", "1")
+    n = int(shape[3:].split("x")[0])
+    p = W.config_pattern(shape, seed=5)
+    psi = haar_state(n, 8)
+    s = Simulator(precision=64)
+    try:
+        check(s, p, psi, "sampled", seed=4)
+        check(s, p, psi, "eowqs")
+    finally:
+        s.close()
 
 
 @pytest.mark.parametrize("rows,cols", [(3, 4), (9, 4), (12, 3)])

@@ -1,0 +1,57 @@
+"""CPU tests of the load-time generated pass kernels (csrc/jit.cpp): the generator's
+output for representative programs NVRTC-compiles for sm_100a without a GPU, every state pass of a
+wide complex64 program runs on the tile engine, and the phase plan keeps every butterfly, X and
+reduction in registers (no cross-lane shuffles). GPU parity of the same kernels: test_gpu_parity.py."""
+import re
+
+import pytest
+
+from paper_1604_05659_b200 import FLAG_NO_JIT
+from paper_1604_05659_b200.host import compile_host, jit_host
+from workloads import patterns as W
+
+
+@pytest.mark.parametrize("shape,prec", [("BW:16x6", 64), ("BW:14x4", 128), ("QFT:13", 64)])
+def test_generated_kernels_compile(shape, prec):
+    p = W.config_pattern(shape, seed=3)
+    r = jit_host(p, "sampled", prec, sources=True)
+    hp = compile_host(p, "sampled", prec)
+    passes = [k for k, s in enumerate(hp.steps) if s.kind == 0]
+    assert r["n_jit_steps"] == sum(1 for k in passes if k in r["sources"])
+    assert r["n_kernels"] >= 1
+    for k, src in r["sources"].items():
+        if k < 0:
+            continue
+        assert "extern \"C\" __global__" in src
+        if prec == 64 and hp.steps[k].width >= 13:
+            assert "tile engine" in src
+            # every op of a tile-engine pass runs on register slots (the phase plan's guarantee)
+            assert "(lane)" not in src and "shfl2(" not in src
+
+
+def test_wide_passes_need_the_tile_engine():
+    """Group slots per pass: up to 7 on the complex64 tile engine, 4 otherwise (AOT / direct)."""
+    p = W.config_pattern("C3")
+    wide = compile_host(p, "sampled", 64)
+    narrow = compile_host(p, "sampled", 64, flags=FLAG_NO_JIT)
+    c128 = compile_host(p, "sampled", 128)
+    assert max(s.nb_hi for s in wide.steps) == 7
+    assert max(s.nb_hi for s in narrow.steps) <= 4 and max(s.nb_hi for s in c128.steps) <= 4
+    # wider tiles fuse more butterflies per state sweep: about half the passes (52 vs 100)
+    assert wide.info["n_passes"] < 0.6 * narrow.info["n_passes"]
+
+
+def test_tile_kernel_structure_c3():
+    """Config 3's tile kernels: no lane butterflies, transposes only between phases, the pass scale
+    folded into one butterfly, deterministic two-level reduction."""
+    r = jit_host(W.config_pattern("C3"), "sampled", 64, sources=True)
+    srcs = [s for k, s in r["sources"].items() if k >= 0]
+    assert srcs and all("tile engine" in s for s in srcs)
+    for s in srcs:
+        n_b = int(re.search(r"(\d+) butterflies", s).group(1))
+        if n_b:
+            assert s.count("scale folded") == 1
+        phases = int(re.search(r"(\d+) phase\(s\)", s).group(1))
+        trans = int(re.search(r"(\d+) transpose\(s\)", s).group(1))
+        assert trans <= phases + 1
+        assert "reduce_finish_grid" in s

@@ -1,4 +1,7 @@
-timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1; echo b=$?
-tail -1 gpurun_out/bench_default.log
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/launches_c3_tile.csv python tools/prof_run.py --workload C3 > gpurun_out/ncu_ll.log 2>&1; echo ll=$?
-timeout 600 ncu --set full --import-source on --clock-control none -k regex:owqs_tma_c64 --launch-skip 20 --launch-count 1 -o gpurun_out/ncu_tile_c3_p20 python tools/prof_run.py --workload C3 > gpurun_out/ncu_t.log 2>&1; echo t=$?
+for rb in 5 6; do
+OWQS_TILE_RB=$rb timeout 600 python bench.py --steps 5 --warmup 2 --no-e2e --no-cpu-baseline > gpurun_out/b_rb$rb.log 2>&1
+tail -1 gpurun_out/b_rb$rb.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('rb $rb', round(d['value']), d['ms_per_step'], d['config']['passes_per_run'], round(d['roofline']['per_pass_roofline_frac'],3), d['clocks']['sm_mhz'])"
+done
+OWQS_TILE_RB=6 timeout 300 python tools/pass_profile.py --workload C3 --out gpurun_out/pp_c3_rb6.json > gpurun_out/pp_rb6.log 2>&1
+OWQS_TILE_RB=5 timeout 300 python tools/pass_profile.py --workload C3 --out gpurun_out/pp_c3_rb5.json > gpurun_out/pp_rb5.log 2>&1
+OWQS_TILE_RB=6 timeout 900 python -m pytest tests -x -q -m gpu -k "parity" > gpurun_out/pytest_rb6.log 2>&1; echo pt=$?; tail -2 gpurun_out/pytest_rb6.log
