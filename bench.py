@@ -357,7 +357,9 @@ def run_ours(args, rank, world, local_rank):
     # probability reduction. Its roofline time is max(bytes / HBM peak, ops / FP32
     # peak); light passes are HBM-bound, heavy ones FP32-bound.
     peak, peak_src = peaks()
-    fp_peak = 148 * 128 * 1.965e9  # FP32 lanes x SMs x max SM clock (B200_PROFILING.md unit counts)
+    # FP32 (complex64) / FP64 (complex128) lanes x SMs x max SM clock (B200: 128 FP32, 64 FP64 lanes/SM)
+    fp_lanes = 128 if prec == 64 else 64
+    fp_peak = 148 * fp_lanes * 1.965e9
     prof = make_sim(FLAG_PROFILE)
     prof.load(pattern)
     per_step = None
@@ -409,8 +411,9 @@ def run_ours(args, rank, world, local_rank):
                 "hbm": {"achieved_gbs": bw, "peak_gbs": peak, "frac": bw / peak,
                         "roofline_ms": float(t_mem.sum())},
                 "alu": {"achieved_tops": fp / 1e12, "peak_tops": fp_peak / 1e12, "frac": fp / fp_peak,
-                        "unit": "FP32-pipe lane-ops/s (FFMA2/FMUL2/FADD2 count 2)", "roofline_ms": float(t_fp.sum()),
-                        "peak_source": "derived: 148 SMs x 128 FP32 lanes x 1965 MHz"},
+                        "unit": ("FP32-pipe lane-ops/s (FFMA2/FMUL2/FADD2 count 2)" if prec == 64 else
+                                 "FP64-pipe ops/s (DFMA/DMUL/DADD)"), "roofline_ms": float(t_fp.sum()),
+                        "peak_source": f"derived: 148 SMs x {fp_lanes} FP{32 if prec == 64 else 64} lanes x 1965 MHz"},
                 "per_pass_roofline_frac": roof_ms / ms_sum,
                 "per_pass_roofline_note": "sum over passes of max(bytes/HBM peak, lane-ops/FP32 peak) over measured time"}
 

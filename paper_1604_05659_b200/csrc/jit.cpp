@@ -87,17 +87,20 @@ std::string hex64(uint64_t v) {
 
 enum SlotKind { SK_REG, SK_LANE, SK_WARP, SK_BASE, SK_RANK };
 
-// ---- engine 2: the complex64 CTA tile ----------------------------------------------------------
-// A CTA (8 warps) owns a tile of 2^13 amplitudes: tile bits t0..t5 = slots 0..5 (one 512 B
-// segment), t6..t12 = the pass's group slots ascending (padded with untouched base slots). A layout
-// maps the tile bits onto (register position bit k: R[k], lane bit j: Lb[j], warp bit j: Wb[j]);
-// R[0] = t0 always, so every thread holds slot-0 neighbours as float4 pairs. Layouts whose lanes are
-// t1..t5 and registers t0 + 4 group bits ("A-type") are the ones global loads and stores use
-// (coalesced 512 B per warp instruction); the others are reached through the shared-memory tile.
-// Shared-memory 16 B unit of tile index t: u(t) = v + (v >> 3) + (v >> 6) + (v >> 9), v = t >> 1.
-// u is injective and additive over disjoint bit sets (per-thread base + per-register immediate),
-// and tile bit k >= 1 lands in bank group 2^((k - 1) mod 3) (mod 8): a quarter-warp is
-// conflict-free when lane bits 0, 1, 2 carry tile bits of the three classes (k - 1) mod 3.
+// ---- engine 2: the CTA tile ---------------------------------------------------------------------
+// A CTA (8 warps) owns a tile of 2^TB amplitudes: tile bits t0..t(SB-1) = the warp segment's slots
+// (512 B: 64 complex64 / 32 complex128 amplitudes), the next 7 = the pass's group slots ascending
+// (padded with untouched base slots); TB = 13 (complex64) / 12 (complex128). A layout maps the tile
+// bits onto (register position bit k: R[k], lane bit j: Lb[j], warp bit j: Wb[j]). complex64: R[0] =
+// t0 always, so every thread holds slot-0 neighbours as float4 pairs, 32 amplitudes per thread;
+// complex128: one double2 per amplitude, 16 per thread. Layouts whose lanes are the segment's lane
+// slots (t1..t5 / t0..t4) and whose other register bits are group bits ("A-type") are the ones
+// global loads and stores use (coalesced 512 B per warp instruction); the others are reached
+// through the shared-memory tile. 16 B unit of tile index t: u(t) = v + (v >> 3) + (v >> 6) + (v >> 9),
+// v = t >> 1 (complex64 pairs) or t (complex128). u is injective and additive over disjoint bit sets
+// (per-thread base + per-register immediate), and a tile bit lands in bank group 2^(class mod 3)
+// (mod 8), class = k - 1 (complex64) or k: a quarter-warp is conflict-free when lane bits 0, 1, 2
+// carry tile bits of the three classes.
 struct CLayout {
   int R[6];   // R[0] = t0; R[1..RB-1] used
   int Lb[5];
@@ -117,12 +120,12 @@ inline TileGeom tile_geom() {
   }();
   return g;
 }
-constexpr int kTileBits = 13;
-inline int umap(int t) {
-  const int v = t >> 1;
+inline int tile_bits(int prec) { return (prec == 0 ? 6 : 5) + KTILE; }
+inline int umap_p(int t, int prec) {
+  const int v = prec == 0 ? t >> 1 : t;
   return v + (v >> 3) + (v >> 6) + (v >> 9);
 }
-constexpr int kTileSmem = 16 * (4095 + 511 + 63 + 7 + 1);  // 16 * (u(8191) + 1)
+constexpr int kTileSmem = 16 * (4095 + 511 + 63 + 7 + 1);  // 16 * (u(2^TB - 1) + 1), both precisions
 
 struct Gen {
   const StepDesc& d;
@@ -131,6 +134,11 @@ struct Gen {
   const int SB, EPV;
   int KHI, G, UNR, P;
   int RB = 5, WB = 3;  // tile engine geometry
+  int TB = 13;         // tile bits
+  int FB = 1;          // first register-selectable tile bit (complex64: t0 is fixed in R[0])
+  int NSEL = 4;        // register tile bits a phase selects
+  int umap(int t) const { return umap_p(t, prec); }
+  int bclass(int k) const { return prec == 0 ? (k - 1) % 3 : k % 3; }
   int gs[KMAX_HI];  // group slots (engine 2: padded to KTILE)
   std::vector<CLayout> lays;  // engine 2 layouts used by this kernel
   int lay = 0;                // engine 2: current layout index
@@ -150,15 +158,25 @@ struct Gen {
       UNR = 1;
       int n = 0;
       for (int j = 0; j < d.nb_hi; ++j) gs[n++] = d.bhi[j];
-      for (int s = 6; n < KTILE && s < d.width; ++s) {
+      for (int s = SB; n < KTILE && s < d.width; ++s) {
         bool used = false;
         for (int j = 0; j < n; ++j) used = used || gs[j] == s;
         if (!used) gs[n++] = s;
       }
-      if (n < KTILE) error = "tile engine needs width >= 13";
+      if (n < KTILE) error = "tile engine needs width >= SB + 7";
       std::sort(gs, gs + KTILE);
-      RB = tile_geom().rb;
-      WB = tile_geom().wb;
+      TB = tile_bits(prec);
+      if (prec == 0) {
+        RB = tile_geom().rb;
+        WB = tile_geom().wb;
+        FB = 1;
+        NSEL = RB - 1;
+      } else {
+        RB = 4;
+        WB = 3;
+        FB = 0;
+        NSEL = 4;
+      }
       P = 1 << RB;
     } else {
       KHI = d.nb_hi;
@@ -286,12 +304,16 @@ struct Gen {
       << "\n";
     // the pass's normalisation scale folded into its first butterfly (tile engine): out = k x0 +- (k a) x1
     // costs the same 4 packed ops as x0 +- a x1, and saves the separate multiply of every amplitude
-    const bool fold = tile && prec == 0 && scale_pending;
+    const bool fold = tile && scale_pending;
     if (fold) scale_pending = false;
-    if (fold)
+    if (fold && prec == 0)
       o << "      const float ar = pc->ar[" << bi << "] * sck; const u64 cB = mul2(pc->B[" << bi << "], bc(sck));  // scale folded\n";
-    else if (tile)
+    else if (fold)
+      o << "      const double ar = pc->ard[" << bi << "] * sck, ai = pc->aid[" << bi << "] * sck;  // scale folded\n";
+    else if (tile && prec == 0)
       o << "      const float ar = pc->ar[" << bi << "]; const u64 cB = pc->B[" << bi << "];\n";
+    else if (tile)
+      o << "      const double ar = pc->ard[" << bi << "], ai = pc->aid[" << bi << "];\n";
     else if (prec == 0)
       o << "      const float ar = s_ar[" << bi << "]; const u64 cB = s_B[" << bi << "];\n";
     else
@@ -327,6 +349,13 @@ struct Gen {
           o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
             << ")); const u64 t = " << X(p) << "; " << X(p) << " = " << (s ? "sub2" : "add2") << "(t, y); " << X(p1)
             << " = " << (s ? "add2" : "sub2") << "(t, y); }\n";
+        } else if (fold) {
+          const std::string u_ = std::to_string(u);
+          o << "      { const double yr = ar" << u_ << " * " << XR(p1) << " - ai" << u_ << " * " << XI(p1)
+            << ", yi = ar" << u_ << " * " << XI(p1) << " + ai" << u_ << " * " << XR(p1) << "; const double tr = "
+            << XR(p) << ", ti = " << XI(p) << "; " << XR(p) << " = fma(sck, tr, " << (s ? "-" : "") << "yr); " << XI(p)
+            << " = fma(sck, ti, " << (s ? "-" : "") << "yi); " << XR(p1) << " = fma(sck, tr, " << (s ? "" : "-")
+            << "yr); " << XI(p1) << " = fma(sck, ti, " << (s ? "" : "-") << "yi); }\n";
         } else {
           const std::string u_ = std::to_string(u);
           o << "      { const double yr = ar" << u_ << " * " << XR(p1) << " - ai" << u_ << " * " << XI(p1)
@@ -351,8 +380,8 @@ struct Gen {
             o << "      const float c" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : " << (fold ? "sck" : "1.f")
               << "; const u64 cB" << u << s << " = h ? (B" << u << (s ? " ^ OWQS_SIGN2" : "") << ") : 0ull;\n";
           else
-            o << "      const double cr" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : 1.0, ci" << u << s
-              << " = h ? " << (s ? "-" : "") << "ai" << u << " : 0.0;\n";
+            o << "      const double cr" << u << s << " = h ? " << (s ? "-" : "") << "ar" << u << " : " << (fold ? "sck" : "1.0")
+              << ", ci" << u << s << " = h ? " << (s ? "-" : "") << "ai" << u << " : 0.0;\n";
         }
       for (int p = 0; p < P; ++p) {
         const int u = unit_of(p), s = st_parity(am, p);
@@ -749,13 +778,13 @@ struct Gen {
     while (left > 0) {
       Phase best{};
       long best_score = -1;
-      const int nsel = RB - 1;
-      for (unsigned m = 0; m < (1u << (kTileBits - 1)); ++m) {
+      const int nsel = NSEL;
+      for (unsigned m = 0; m < (1u << (TB - FB)); ++m) {
         if (__builtin_popcount(m) != nsel) continue;
-        const unsigned regs = 1u | (m << 1);  // tile bits 1..12 <- m bits 0..11
-        if (regs & warp_pref) continue;       // keep the pass's warp bits out of registers
+        const unsigned regs = (FB ? 1u : 0u) | (m << FB);  // tile bits FB..TB-1 <- m bits
+        if (regs & warp_pref) continue;                    // keep the pass's warp bits out of registers
         int S[5], n = 0;
-        for (int b = 1; b < kTileBits; ++b)
+        for (int b = FB; b < TB; ++b)
           if ((regs >> b) & 1) S[n++] = b;
         if (first && first_group_only && !a_type(S)) continue;
         std::vector<int> cl = closure(regs, done);
@@ -778,11 +807,11 @@ struct Gen {
   // slots first), so that phase changes keep them and transpose within each warp
   unsigned warp_pref = 0;
   void choose_warp_bits() {
-    std::vector<int> use(kTileBits, 0);
+    std::vector<int> use(TB, 0);
     for (int i = 0; i <= n_ops_; ++i)
       if (op_tb[i] >= 0) ++use[op_tb[i]];
     std::vector<int> cand;
-    for (int b = 6; b < kTileBits; ++b) cand.push_back(b);
+    for (int b = SB; b < TB; ++b) cand.push_back(b);
     std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) { return use[x] < use[y]; });
     warp_pref = 0;
     for (int k = 0; k < WB; ++k) warp_pref |= 1u << cand[k];
@@ -791,8 +820,8 @@ struct Gen {
       if (use[cand[k]] > 0) warp_pref &= ~(1u << cand[k]);
   }
   bool a_type(const int* S) const {
-    for (int k = 0; k < RB - 1; ++k)
-      if (S[k] < 6) return false;
+    for (int k = 0; k < NSEL; ++k)
+      if (S[k] < SB) return false;
     return true;
   }
   int n_transitions(const std::vector<Phase>& ph) const {
@@ -805,24 +834,24 @@ struct Gen {
   // lanes / warps for a register set
   CLayout make_layout(const int* S) const {
     CLayout L;
-    L.R[0] = 0;
-    for (int k = 0; k < RB - 1; ++k) L.R[k + 1] = S[k];
+    for (int k = 0; k < FB; ++k) L.R[k] = k;  // complex64: t0 in R[0]
+    for (int k = 0; k < NSEL; ++k) L.R[FB + k] = S[k];
     auto in_s = [&](int b) {
-      for (int k = 0; k < RB - 1; ++k)
-        if (S[k] == b) return true;
+      for (int k = 0; k < RB; ++k)
+        if (L.R[k] == b) return true;
       return false;
     };
     // warp bits: the pass's preferred ones first (ascending), then the highest free group bits
     int w = 0;
-    for (int b = 6; b < kTileBits && w < WB; ++b)
+    for (int b = SB; b < TB && w < WB; ++b)
       if (((warp_pref >> b) & 1) && !in_s(b)) L.Wb[w++] = b;
-    for (int b = kTileBits - 1; b >= 6 && w < WB; --b) {
+    for (int b = TB - 1; b >= SB && w < WB; --b) {
       bool taken = in_s(b);
       for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
       if (!taken) L.Wb[w++] = b;
     }
     if (w < WB)  // S holds group bits and the preferred set overlaps: any remaining bits
-      for (int b = kTileBits - 1; b >= 1 && w < WB; --b) {
+      for (int b = TB - 1; b >= 0 && w < WB; --b) {
         bool taken = in_s(b);
         for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
         if (!taken) L.Wb[w++] = b;
@@ -833,19 +862,21 @@ struct Gen {
         if (L.Wb[j] == b) return true;
       return false;
     };
-    if (a_type(S) && !in_w(1) && !in_w(2) && !in_w(3) && !in_w(4) && !in_w(5)) {
-      for (int j = 0; j < 5; ++j) L.Lb[j] = j + 1;
+    bool seg_lanes = a_type(S);
+    for (int j = 0; j < 5; ++j) seg_lanes = seg_lanes && !in_w(FB + j);
+    if (seg_lanes) {  // A-type: lanes = the segment's lane slots (global IO layout)
+      for (int j = 0; j < 5; ++j) L.Lb[j] = FB + j;
       return L;
     }
     std::vector<int> rest;
-    for (int b = 1; b < kTileBits; ++b)
+    for (int b = 0; b < TB; ++b)
       if (!in_s(b) && !in_w(b)) rest.push_back(b);
-    // lane bits 0..2: one tile bit of each bank class (k - 1) mod 3, lowest first
+    // lane bits 0..2: one tile bit of each bank class, lowest first
     std::vector<char> used(rest.size(), 0);
     for (int c = 0; c < 3; ++c) {
       int pick = -1;
       for (size_t i = 0; i < rest.size(); ++i)
-        if (!used[i] && (rest[i] - 1) % 3 == c) {
+        if (!used[i] && bclass(rest[i]) == c) {
           pick = (int)i;
           break;
         }
@@ -879,8 +910,8 @@ struct Gen {
   uint64_t a_seg(int l, int p) const {
     uint64_t s = 0;
     const CLayout& L = lays[l];
-    for (int k = 1; k < RB; ++k)
-      if ((p >> k) & 1) s |= 1ull << (gs[L.R[k] - 6] - 6);
+    for (int k = 0; k < RB; ++k)
+      if (((p >> k) & 1) && L.R[k] >= SB) s |= 1ull << (gs[L.R[k] - SB] - SB);
     return s;
   }
   void emit_tile_transition(int to, bool last) {
@@ -890,13 +921,23 @@ struct Gen {
     // warp bits unchanged: every warp exchanges only its own amplitudes (warp-local barrier)
     const bool local = !memcmp(A.Wb, B.Wb, sizeof(int) * WB);
     const char* bar = local ? "    __syncwarp();\n" : "    __syncthreads();\n";
-    for (int p = 0; p < P; p += 2)
-      o << "    *reinterpret_cast<float4*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_float4(lo("
-        << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
-    o << bar;
-    for (int p = 0; p < P; p += 2)
-      o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
-        << "); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
+    if (prec == 0) {
+      for (int p = 0; p < P; p += 2)
+        o << "    *reinterpret_cast<float4*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_float4(lo("
+          << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
+      o << bar;
+      for (int p = 0; p < P; p += 2)
+        o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
+          << "); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
+    } else {
+      for (int p = 0; p < P; ++p)
+        o << "    *reinterpret_cast<double2*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_double2("
+          << XR(p) << ", " << XI(p) << ");\n";
+      o << bar;
+      for (int p = 0; p < P; ++p)
+        o << "    { const double2 w = *reinterpret_cast<const double2*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
+          << "); xr" << p << " = w.x; xi" << p << " = w.y; }\n";
+    }
     for (int p = 0; p < P; ++p) perm[p] = p;
     if (!last || tile_iters > 1) o << bar;
     ++(local ? n_local_ : n_cta_);
@@ -910,7 +951,7 @@ struct Gen {
     const int nbf = d.n_bfly;
     const int red = d.red_kind;
     const int nred = red == RED_NONE ? 0 : (red == RED_NORM ? 1 : 4);
-    const uint64_t nbu = 1ull << (d.width - kTileBits);
+    const uint64_t nbu = 1ull << (d.width - TB);
     const uint64_t iters = nbu > (uint64_t)RED_MAX_BLOCKS ? nbu / RED_MAX_BLOCKS : 1;
     tile_iters = iters;
     build_dag();
@@ -925,11 +966,12 @@ struct Gen {
     std::vector<int> plays;
     for (const Phase& f : ph) plays.push_back(add_layout(make_layout(f.S)));
     // global IO layout when a phase is not A-type: the A-type layout keeping the preferred warp bits
-    int sa[5] = {6, 7, 8, 9, 10};
+    int sa[5];
+    for (int k = 0; k < 5; ++k) sa[k] = SB + k;
     if (__builtin_popcount(warp_pref) == WB) {
       int k = 0;
-      for (int b = 6; b < kTileBits; ++b)
-        if (!((warp_pref >> b) & 1)) sa[k++] = b;
+      for (int b = SB; b < TB; ++b)
+        if (!((warp_pref >> b) & 1) && k < NSEL) sa[k++] = b;
     }
     const int l_load = a_type(ph.front().S) ? plays.front() : add_layout(make_layout(sa));
     const int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(sa));
@@ -948,8 +990,8 @@ struct Gen {
     for (int j = 0; j < WB; ++j) o << " t" << lays[l_load].Wb[j];
     o << "\n";
     for (size_t f = 0; f < ph.size(); ++f) {
-      o << "  // phase " << f << ": registers t0";
-      for (int k = 0; k < RB - 1; ++k) o << " t" << ph[f].S[k];
+      o << "  // phase " << f << ": registers" << (FB ? " t0" : "");
+      for (int k = 0; k < NSEL; ++k) o << " t" << ph[f].S[k];
       o << ", " << ph[f].ops.size() << " op(s)\n";
     }
     if (n_trans) o << "  extern __shared__ __align__(16) unsigned char dsm[];\n";
@@ -957,7 +999,8 @@ struct Gen {
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  const unsigned rk = p.rank; (void)rk; (void)d;\n"
       << "  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;\n";
-    if (nbf > 0) o << "  const float sck = (float)pc->scale;\n  const u64 scale = bc(sck); (void)scale;\n";
+    if (nbf > 0 && prec == 0) o << "  const float sck = (float)pc->scale;\n  const u64 scale = bc(sck); (void)scale;\n";
+    if (nbf > 0 && prec == 1) o << "  const double sck = pc->scale;\n  const double scale = sck; (void)scale;\n";
     scale_pending = nbf > 0;
     if (n_trans)
       for (size_t l = 0; l < lays.size(); ++l) {
@@ -970,18 +1013,24 @@ struct Gen {
       std::string e = "(";
       for (int j = 0; j < WB; ++j)
         e += std::string(j ? " | " : "") + "((unsigned long long)((warp >> " + std::to_string(j) + ") & 1) << " +
-             std::to_string(gs[lays[l].Wb[j] - 6] - 6) + ")";
+             std::to_string(gs[lays[l].Wb[j] - SB] - SB) + ")";
       return e + ")";
     };
     o << "  const unsigned long long wsl = " << wseg(l_load) << ";\n";
     o << "  const unsigned long long wss = " << wseg(l_store) << ";\n";
-    o << "  float4* __restrict__ st = reinterpret_cast<float4*>(p.state);\n"
+    o << "  " << (prec == 0 ? "float4" : "double2") << "* __restrict__ st = reinterpret_cast<"
+      << (prec == 0 ? "float4" : "double2") << "*>(p.state);\n"
       << "  for (unsigned it = 0; it < " << iters << "u; ++it) {\n"
       << "    const unsigned long long ub = (unsigned long long)blockIdx.x * " << iters << "ull + it;\n";
     emit_gb("gb0", "ub");
-    for (int q = 0; q < P; q += 2)
-      o << "    u64 x" << q << ", x" << q + 1 << "; { const float4 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
-        << "ull) << 5) + lane)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
+    if (prec == 0)
+      for (int q = 0; q < P; q += 2)
+        o << "    u64 x" << q << ", x" << q + 1 << "; { const float4 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
+          << "ull) << 5) + lane)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
+    else
+      for (int q = 0; q < P; ++q)
+        o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
+          << "ull) << 5) + lane)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
     lay = l_load;
     for (int q = 0; q < P; ++q) perm[q] = q;
     std::vector<int> bidx(d.n_ops, -1);
@@ -1005,10 +1054,14 @@ struct Gen {
       }
     }
     if (l_store != lay) emit_tile_transition(l_store, --left == 0);
-    if (d.n_ops > 0)
+    if (d.n_ops > 0 && prec == 0)
       for (int q = 0; q < P; q += 2)
         o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_float4(lo(" << X(q)
           << "), hi(" << X(q) << "), lo(" << X(q + 1) << "), hi(" << X(q + 1) << ")));\n";
+    if (d.n_ops > 0 && prec == 1)
+      for (int q = 0; q < P; ++q)
+        o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_double2(" << XR(q)
+          << ", " << XI(q) << "));\n";
     o << "  }\n";
     if (nred > 0)
       o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n  reduce_finish_grid<" << nred << ">(acc, p, red_s, &flag_s);\n";
@@ -1053,7 +1106,7 @@ std::string compile_tu(const std::string& src, std::vector<char>& cubin) {
 
 int jit_engine(const StepDesc& d, int prec) {
   if (d.kind != ST_PASS) return 0;
-  if (prec == 0 && d.width >= kTileBits && d.nb_hi <= KTILE && !getenv("OWQS_JIT_NO_TILE")) return 2;
+  if (d.width >= tile_bits(prec) && d.nb_hi <= KTILE && !getenv("OWQS_JIT_NO_TILE")) return 2;
   if (d.nb_hi > KMAX_AOT) return -1;  // needs the tile engine
   const int SB = prec == 0 ? 6 : 5;
   const int unr = jit_unr_of(d.nb_hi);
@@ -1064,7 +1117,8 @@ int jit_engine(const StepDesc& d, int prec) {
 bool jit_eligible(const StepDesc& d, int prec) { return jit_engine(d, prec) > 0; }
 
 int jit_max_group(int prec, bool no_jit) {
-  return (prec == 0 && !no_jit && !getenv("OWQS_JIT_NO_TILE")) ? KTILE : KMAX_AOT;
+  (void)prec;
+  return (!no_jit && !getenv("OWQS_JIT_NO_TILE")) ? KTILE : KMAX_AOT;
 }
 
 int jit_block_threads(int engine) { return engine == 2 ? (32 << tile_geom().wb) : 256; }
@@ -1163,7 +1217,7 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
   DevPtrs pp = p;
   const PassCoef* pcc = pc;
   if (eng == 2) {  // non-persistent: one CTA per 13-bit tile (or iters tiles above RED_MAX_BLOCKS)
-    const uint64_t nbu = 1ull << (d.width - kTileBits);
+    const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
     const uint64_t blocks = nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu;
     void* args[] = {&dd, &pp, &pcc};
     return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(32 << tile_geom().wb), args,

@@ -646,7 +646,7 @@ struct Packer {
   }
   int wl() const { return width - n_global; }
   // group slots allowed in a pass of (shard) width w
-  int wide_at(int w) const { return (kwide > KMAX_AOT && SB == 6 && w >= 13) ? kwide : kmax_hi; }
+  int wide_at(int w) const { return (kwide > KMAX_AOT && w >= SB + KTILE) ? kwide : kmax_hi; }
   // last step that computes something (a SWAP only permutes: it preserves the norm)
   StepDesc* last_compute() {
     for (int i = (int)pr.steps.size() - 1; i >= 0; --i)
@@ -835,7 +835,7 @@ struct Packer {
       if (nodes[i].npred == 0) ready.push_back(i);
     int remaining = N;
     auto is_lane = [&](int a) { return a < SB && !(SB == 6 && a == 0); };
-    // tile engine (complex64, width >= 13): up to kwide group slots; lane slots reach registers
+    // tile engine (width >= SB + 7): up to kwide group slots; lane slots reach registers
     // through shared-memory transposes, so no lane cap
     const bool wide = wide_at(wl()) > KMAX_AOT;
     const int kmax = wide_at(wl());

@@ -23,20 +23,20 @@ def test_generated_kernels_compile(shape, prec):
         if k < 0:
             continue
         assert "extern \"C\" __global__" in src
-        if prec == 64 and hp.steps[k].width >= 13:
+        if hp.steps[k].width >= (13 if prec == 64 else 12):
             assert "tile engine" in src
             # every op of a tile-engine pass runs on register slots (the phase plan's guarantee)
             assert "(lane)" not in src and "shfl2(" not in src
 
 
 def test_wide_passes_need_the_tile_engine():
-    """Group slots per pass: up to 7 on the complex64 tile engine, 4 otherwise (AOT / direct)."""
+    """Group slots per pass: up to 7 on the tile engine (both precisions), 4 otherwise (AOT / direct)."""
     p = W.config_pattern("C3")
     wide = compile_host(p, "sampled", 64)
     narrow = compile_host(p, "sampled", 64, flags=FLAG_NO_JIT)
     c128 = compile_host(p, "sampled", 128)
-    assert max(s.nb_hi for s in wide.steps) == 7
-    assert max(s.nb_hi for s in narrow.steps) <= 4 and max(s.nb_hi for s in c128.steps) <= 4
+    assert max(s.nb_hi for s in wide.steps) == 7 and max(s.nb_hi for s in c128.steps) == 7
+    assert max(s.nb_hi for s in narrow.steps) <= 4
     # wider tiles fuse more butterflies per state sweep: about half the passes (52 vs 100)
     assert wide.info["n_passes"] < 0.6 * narrow.info["n_passes"]
 
