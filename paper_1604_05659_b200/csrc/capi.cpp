@@ -298,7 +298,7 @@ owqs_status ensure_device(owqs_ctx* ctx) {
           if (dyn > 0)
             CU(cudaFuncSetAttribute((const void*)fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
           int nb = 0;
-          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], jit_block_threads(eng), dyn));
+          CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], jit_block_threads(eng, ctx->prec), dyn));
           blocks[k] = std::max(1, nb) * sms;
         }
       }

@@ -981,7 +981,7 @@ struct Gen {
       for (int l : plays) n_trans += l != cur, cur = l;
       n_trans += l_store != cur;
     }
-    o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* __restrict__ pc) {\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* pc) {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
       << "  using namespace owqs;\n"
       << "  // tile engine: width " << d.width << ", tile group slots";
     for (int j = 0; j < KTILE; ++j) o << " " << gs[j];
@@ -999,8 +999,7 @@ struct Gen {
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  const unsigned rk = p.rank; (void)rk; (void)d;\n"
       << "  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;\n";
-    if (nbf > 0 && prec == 0) o << "  const float sck = (float)pc->scale;\n  const u64 scale = bc(sck); (void)scale;\n";
-    if (nbf > 0 && prec == 1) o << "  const double sck = pc->scale;\n  const double scale = sck; (void)scale;\n";
+
     scale_pending = nbf > 0;
     if (n_trans)
       for (size_t l = 0; l < lays.size(); ++l) {
@@ -1031,6 +1030,11 @@ struct Gen {
       for (int q = 0; q < P; ++q)
         o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
           << "ull) << 5) + lane)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
+    // launched right behind decide_kernel (programmatic dependent launch): the loads above overlap
+    // the decisions; wait for them before the first read of PassCoef
+    o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    if (nbf > 0 && prec == 0) o << "    const float sck = (float)pc->scale;\n    const u64 scale = bc(sck); (void)scale;\n";
+    if (nbf > 0 && prec == 1) o << "    const double sck = pc->scale;\n    const double scale = sck; (void)scale;\n";
     lay = l_load;
     for (int q = 0; q < P; ++q) perm[q] = q;
     std::vector<int> bidx(d.n_ops, -1);
@@ -1121,7 +1125,7 @@ int jit_max_group(int prec, bool no_jit) {
   return (!no_jit && !getenv("OWQS_JIT_NO_TILE")) ? KTILE : KMAX_AOT;
 }
 
-int jit_block_threads(int engine) { return engine == 2 ? (32 << tile_geom().wb) : 256; }
+int jit_block_threads(int engine, int prec) { return (engine == 2 && prec == 0) ? (32 << tile_geom().wb) : 256; }
 
 int jit_dyn_smem(int engine) { return engine == 2 ? kTileSmem : 0; }
 
@@ -1220,8 +1224,17 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
     const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
     const uint64_t blocks = nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu;
     void* args[] = {&dd, &pp, &pcc};
-    return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(32 << tile_geom().wb), args,
-                            (size_t)jit_dyn_smem(eng), s);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(jit_block_threads(eng, prec));
+    cfg.dynamicSmemBytes = (size_t)jit_dyn_smem(eng);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = getenv("OWQS_NO_PDL") ? 0 : 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
   }
   const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
   const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));

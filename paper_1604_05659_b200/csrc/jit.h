@@ -30,7 +30,7 @@ int jit_max_group(int prec, bool no_jit);
 bool jit_eligible(const StepDesc& d, int prec);
 // Dynamic shared memory (bytes) and threads per block an engine's kernels are launched with.
 int jit_dyn_smem(int engine);
-int jit_block_threads(int engine);
+int jit_block_threads(int engine, int prec);
 
 // Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
 // a hash of the body (identical passes share one kernel).

@@ -994,7 +994,10 @@ cudaError_t init_kernel_limits(int device) {
 int max_partial_blocks() { return RED_MAX_BLOCKS + RED_MAX_GROUPS; }
 
 // Decisions of one pass for the generated pass kernels (one warp; PassCoef read by every CTA).
-__global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevPtrs p, PassCoef* pc) {
+__global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevPtrs p, PassCoef* pc, int trigger) {
+  // the pass kernel that follows is launched with programmatic stream serialisation: let it start
+  // (it issues its state loads, then griddepcontrol.wait-s for this grid before reading pc)
+  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ PassShared sh;
   pass_prologue(d, p, sh, true);
   const int t = threadIdx.x;
@@ -1011,7 +1014,7 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
 }
 
 cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s) {
-  decide_kernel<<<1, 32, 0, s>>>(d, p, pc);
+  decide_kernel<<<1, 32, 0, s>>>(d, p, pc, getenv("OWQS_PDL_NO_TRIGGER") ? 0 : 1);
   return cudaGetLastError();
 }
 
