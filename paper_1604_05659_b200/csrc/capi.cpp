@@ -37,6 +37,7 @@ int step_kclass(const StepDesc& d, int prec);
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
                        cudaStream_t s);
 cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s);
+cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaStream_t s);
 cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base, int K, int n_batch, const void* in,
                          void* out, int n_in, int n_out, const int* out_slot, int phys, int prec, cudaStream_t s);
 }  // namespace owqs
@@ -123,7 +124,8 @@ double kernels_per_run(const owqs_ctx* ctx, const CompiledMode& m) {
   for (size_t i = 0; i < m.prog.steps.size(); ++i) {
     const StepDesc& s = m.prog.steps[i];
     n += 1;
-    if (i < m.jit_name.size() && !m.jit_name[i].empty() && jit_engine(s, ctx->prec) == 2) n += 1;
+    if (i < m.jit_name.size() && !m.jit_name[i].empty() && jit_engine(s, ctx->prec) == 2)
+      n += 1 + (s.red_kind != RED_NONE ? 1 : 0);  // decide + grid finish
   }
   return n;
 }
@@ -295,8 +297,14 @@ owqs_status ensure_device(owqs_ctx* ctx) {
           CU(cudaLibraryGetKernel(&fn[k], lib, m.jit_name[k].c_str()));
           const int eng = jit_engine(m.prog.steps[k], ctx->prec);
           const int dyn = jit_dyn_smem(eng);
-          if (dyn > 0)
+          if (dyn > 0) {
             CU(cudaFuncSetAttribute((const void*)fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
+            // shared-memory carveout just large enough for the CTAs the registers allow: the rest
+            // stays L1, which stages the in-flight global loads (a max-shared carveout, L1 <= 32 KB,
+            // costs 19 % of streaming bandwidth: profiles/r01b/overlap_bench.log)
+            CU(cudaFuncSetAttribute((const void*)fn[k], cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    jit_smem_carveout(eng, ctx->prec)));
+          }
           int nb = 0;
           CU(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, (const void*)fn[k], jit_block_threads(eng, ctx->prec), dyn));
           blocks[k] = std::max(1, nb) * sms;
@@ -394,6 +402,10 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
           else
             CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
         }
+        if (eng == 2 && s.red_kind != RED_NONE)  // tile passes leave block partials
+          for (size_t r = 0; r < ctx->shards.size(); ++r)
+            CU(launch_grid_finish(dev_ptrs(ctx, m, (int)r), jit_tile_blocks(s, ctx->prec),
+                                  s.red_kind == RED_NORM ? 1 : 4, ctx->stream));
         if (s.red_kind != RED_NONE) {
           owqs_status st = allreduce_red(ctx);
           if (st != OWQS_OK) return st;

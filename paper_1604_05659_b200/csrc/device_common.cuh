@@ -297,6 +297,27 @@ __device__ void reduce_finish(double (&acc)[4], const DevPtrs& p, PassShared& sh
   }
 }
 
+// Block partial of up to 4 doubles into p.partials[blockIdx.x * 4 + k] (no fence, no atomics: the
+// grid's partials are summed in a fixed order by grid_finish_kernel launched right after the pass,
+// so a CTA retires without waiting for its own outstanding state stores to drain).
+template <int NRED>
+__device__ void block_partial(double (&acc)[4], const DevPtrs& p, double (*red)[4]) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NRED; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_xor_sync(FULLMASK, acc[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NRED; ++k) red[warp][k] = acc[k];
+  __syncthreads();
+  if (threadIdx.x < NRED) {
+    double t = 0;
+    for (int w = 0; w < nw; ++w) t += red[w][threadIdx.x];
+    p.partials[(size_t)blockIdx.x * 4 + threadIdx.x] = t;
+  }
+}
+
 // Deterministic two-level grid reduction of up to 4 doubles for grids of up to RED_MAX_BLOCKS
 // blocks (the generated pass kernels launch one block per 8 warp units): block partials ->
 // the last block of each group of RED_GROUP blocks sums its group in a fixed order -> the last

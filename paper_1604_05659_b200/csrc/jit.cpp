@@ -711,10 +711,11 @@ struct Gen {
   uint64_t tile_iters = 1;
   // CTAs per SM the tile kernel is compiled for (register cap 65536 / (256 * minb)). 2: measured on
   // C3, 3 (80 registers) is 18% slower (serialised loads)
-  static int tile_minb() {
+  static int tile_minb_for(int prec) {
     const char* e = getenv("OWQS_TILE_MINB");
-    return e ? std::max(1, std::min(4, atoi(e))) : (tile_geom().rb == 6 ? 3 : 2);
+    return e ? std::max(1, std::min(4, atoi(e))) : ((prec == 0 && tile_geom().rb == 6) ? 3 : 2);
   }
+  int tile_minb() const { return tile_minb_for(prec); }
   int n_local_ = 0, n_cta_ = 0;
 
   void build_dag() {
@@ -1068,7 +1069,7 @@ struct Gen {
           << ", " << XI(q) << "));\n";
     o << "  }\n";
     if (nred > 0)
-      o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n  reduce_finish_grid<" << nred << ">(acc, p, red_s, &flag_s);\n";
+      o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n  block_partial<" << nred << ">(acc, p, red_s);  // grid_finish_kernel sums\n";
     o << "}\n";
     return o.str();
   }
@@ -1125,7 +1126,21 @@ int jit_max_group(int prec, bool no_jit) {
   return (!no_jit && !getenv("OWQS_JIT_NO_TILE")) ? KTILE : KMAX_AOT;
 }
 
+int jit_smem_carveout(int engine, int prec) {
+  if (engine != 2) return -1;  // cudaSharedmemCarveoutDefault
+  if (const char* e = getenv("OWQS_CARVEOUT")) return atoi(e);
+  // CTAs per SM (register-limited) x (tile + static + reserved), as a percentage of 228 KB
+  const int per = kTileSmem + 2048 + 1024;
+  const int ctas = Gen::tile_minb_for(prec);
+  return std::min(100, (ctas * per * 100 + 233471) / 233472);
+}
+
 int jit_block_threads(int engine, int prec) { return (engine == 2 && prec == 0) ? (32 << tile_geom().wb) : 256; }
+
+unsigned jit_tile_blocks(const StepDesc& d, int prec) {
+  const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
+  return (unsigned)(nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu);
+}
 
 int jit_dyn_smem(int engine) { return engine == 2 ? kTileSmem : 0; }
 

@@ -31,6 +31,10 @@ bool jit_eligible(const StepDesc& d, int prec);
 // Dynamic shared memory (bytes) and threads per block an engine's kernels are launched with.
 int jit_dyn_smem(int engine);
 int jit_block_threads(int engine, int prec);
+// Grid of a tile-engine pass (= its number of block partials for grid_finish_kernel).
+unsigned jit_tile_blocks(const StepDesc& d, int prec);
+// cudaFuncAttributePreferredSharedMemoryCarveout (percent) for an engine's kernels; -1 = default
+int jit_smem_carveout(int engine, int prec);
 
 // Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
 // a hash of the body (identical passes share one kernel).

@@ -1013,6 +1013,30 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
   if (t == 0) pc->scale = sh.scale;
 }
 
+// Sum of the block partials of a tile pass (fixed order: deterministic) into red_result.
+__global__ void __launch_bounds__(1024) grid_finish_kernel(DevPtrs p, unsigned nblk, int nred) {
+  __shared__ double red[32][4];
+  double v[4] = {0, 0, 0, 0};
+  for (unsigned b = threadIdx.x; b < nblk; b += blockDim.x)
+    for (int k = 0; k < nred; ++k) v[k] += p.partials[(size_t)b * 4 + k];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int k = 0; k < 4; ++k)
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULLMASK, v[k], o);
+  if (lane == 0)
+    for (int k = 0; k < 4; ++k) red[warp][k] = v[k];
+  __syncthreads();
+  if (threadIdx.x < 4) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
+    p.red_result[threadIdx.x] = threadIdx.x < nred ? t : 0.0;
+  }
+}
+
+cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaStream_t s) {
+  grid_finish_kernel<<<1, 1024, 0, s>>>(p, nblk, nred);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s) {
   decide_kernel<<<1, 32, 0, s>>>(d, p, pc, getenv("OWQS_PDL_NO_TRIGGER") ? 0 : 1);
   return cudaGetLastError();

@@ -95,6 +95,45 @@ __global__ void __launch_bounds__(256, 1) tma_k(float4* __restrict__ a, u64 c, i
   }
 }
 
+// np with T CTA-wide shared-memory transposes of the tile (write 16 B / amplitude pair, barrier,
+// read back in another order, barrier), as the tile engine's phase changes do
+template <int K, int T>
+__global__ void __launch_bounds__(256, 2) npt_k(float4* __restrict__ a, u64 c) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float4* t = a + (size_t)blockIdx.x * 4096;
+  u64 x[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const float4 v = __ldcs(t + (warp * 16 + q) * 32 + lane);
+    x[2 * q] = pk(v.x, v.y);
+    x[2 * q + 1] = pk(v.z, v.w);
+  }
+  float4* s4 = reinterpret_cast<float4*>(sm);
+#pragma unroll
+  for (int r = 0; r < T; ++r) {
+    work<K / (T + 1)>(x, c);
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int u = (warp * 16 + q) * 32 + lane;
+      s4[u] = make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1]));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int u = (q * 8 + warp) * 32 + lane;  // rows exchanged across warps, lanes contiguous (conflict-free)
+      const float4 v = s4[u];
+      x[2 * q] = pk(v.x, v.y);
+      x[2 * q + 1] = pk(v.z, v.w);
+    }
+    __syncthreads();
+  }
+  work<K - T * (K / (T + 1))>(x, c);
+#pragma unroll
+  for (int q = 0; q < 16; ++q)
+    __stcs(t + (warp * 16 + q) * 32 + lane, make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
+}
+
 int main() {
   const size_t bytes = 2ull << 30, n4 = bytes / 16;
   const int ntiles = (int)(n4 / 4096);
@@ -123,12 +162,29 @@ int main() {
     cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess) { printf("%s: %s\n", name, cudaGetErrorString(err)); exit(1); }
     const double fp_ms = (double)K * 2.0 * (bytes / 8) / (148.0 * 128 * 1.9e9) * 1e3;  // FFMA2 = 2 lane-ops
-    printf("%-6s K=%3d FFMA2/amp  %7.3f ms  (%6.1f GB/s; FP-only floor %.3f ms)\n", name, K, best, 2.0 * bytes / best / 1e6, fp_ms);
+    printf("%-16s K=%3d FFMA2/amp  %7.3f ms  (%6.1f GB/s; FP-only floor %.3f ms)\n", name, K, best, 2.0 * bytes / best / 1e6, fp_ms);
   };
 #define BOTH(K)                                                                                  \
   run("np", K, [&] { np_k<K><<<ntiles, 256>>>(a, c); });                                        \
   cudaFuncSetAttribute(tma_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 65536);       \
   run("tma", K, [&] { tma_k<K><<<sms, 256, 2 * 65536>>>(a, c, ntiles); });
-  BOTH(0) BOTH(8) BOTH(16) BOTH(24) BOTH(32) BOTH(48) BOTH(64) BOTH(96)
+  BOTH(16)
+  // occupancy (CTAs/SM from the shared-memory request) vs L1 size (the carveout percentage)
+  for (int kb : {64, 75, 90, 110}) {
+    for (int co : {-1, 50, 67, 80, 100}) {
+      cudaFuncSetAttribute(np_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
+      cudaFuncSetAttribute(np_k<16>, cudaFuncAttributePreferredSharedMemoryCarveout, co);
+      int nb = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, np_k<16>, 256, kb * 1024);
+      char nm[40];
+      snprintf(nm, sizeof nm, "np%dKB/c%d/%d", kb, co, nb);
+      run(nm, 16, [&] { np_k<16><<<ntiles, 256, kb * 1024>>>(a, c); });
+    }
+  }
+  cudaFuncSetAttribute(np_k<16>, cudaFuncAttributePreferredSharedMemoryCarveout, -1);
+#define TR(K, T)                                                                                   \
+  cudaFuncSetAttribute(npt_k<K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4608 * 16);        \
+  run("np+T" #T, K, [&] { npt_k<K, T><<<ntiles, 256, 4608 * 16>>>(a, c); });
+  TR(16, 0) TR(16, 1)
   return 0;
 }
