@@ -771,38 +771,108 @@ struct Gen {
   }
   // Phases: each picks, among all C(12, 4) register sets (t0 + 4 of t1..t12), the one that runs the
   // most ready ops (ties: fewer bits outside the pass's preferred warp bits, then A-type sets).
+  // Bitset form of the DAG for the phase search (ops + the reduction <= 128).
+  struct Bits {
+    uint64_t w[3] = {0, 0, 0};
+    void set(int i) { w[i >> 6] |= 1ull << (i & 63); }
+    bool get(int i) const { return (w[i >> 6] >> (i & 63)) & 1; }
+    bool disjoint(const Bits& o) const { return !(w[0] & o.w[0]) && !(w[1] & o.w[1]) && !(w[2] & o.w[2]); }
+    int count() const { return __builtin_popcountll(w[0]) + __builtin_popcountll(w[1]) + __builtin_popcountll(w[2]); }
+  };
+  std::vector<Bits> predbits;
+  void build_predbits() {
+    predbits.assign(n_ops_ + 1, Bits());
+    for (int i = 0; i <= n_ops_; ++i)
+      for (int j : preds[i]) predbits[i].set(j);
+  }
+  // ops runnable in a phase with register mask regs after `done`: closure in op order
+  Bits closure_bits(unsigned regs, const Bits& done) const {
+    Bits take = done;
+    for (int i = 0; i <= n_ops_; ++i) {
+      if (done.get(i) || !exec_in(i, regs)) continue;
+      const Bits& pb = predbits[i];
+      // every predecessor done or taken: pb & ~take == 0
+      if ((pb.w[0] & ~take.w[0]) || (pb.w[1] & ~take.w[1]) || (pb.w[2] & ~take.w[2])) continue;
+      take.set(i);
+    }
+    return take;
+  }
+  // Beam search over phase sequences: each step expands a state by the register sets that run the
+  // most ready ops (top kExpand), keeps the kBeam states with the most ops done, and stops at the
+  // first depth where a state has run every op; ties go to fewer transposes (non-A first/last
+  // phases cost one each). first_group_only: the first phase must be loadable (A-type).
   std::vector<Phase> plan_greedy(bool first_group_only) const {
-    std::vector<Phase> ph;
-    std::vector<char> done(n_ops_ + 1, 0);
-    int left = n_ops_ + 1;
-    bool first = true;
-    while (left > 0) {
-      Phase best{};
-      long best_score = -1;
-      const int nsel = NSEL;
-      for (unsigned m = 0; m < (1u << (TB - FB)); ++m) {
-        if (__builtin_popcount(m) != nsel) continue;
-        const unsigned regs = (FB ? 1u : 0u) | (m << FB);  // tile bits FB..TB-1 <- m bits
-        if (regs & warp_pref) continue;                    // keep the pass's warp bits out of registers
-        int S[5], n = 0;
-        for (int b = FB; b < TB; ++b)
-          if ((regs >> b) & 1) S[n++] = b;
-        if (first && first_group_only && !a_type(S)) continue;
-        std::vector<int> cl = closure(regs, done);
-        const long score = (long)cl.size() * 4 + (a_type(S) ? 1 : 0);
-        if (score > best_score) {
-          best_score = score;
-          for (int k = 0; k < nsel; ++k) best.S[k] = S[k];
-          best.ops = cl;
+    const int kBeam = 8, kExpand = 6;
+    struct St {
+      Bits done;
+      std::vector<Phase> ph;
+    };
+    std::vector<unsigned> sets;
+    std::vector<std::array<int, 5>> setS;
+    for (unsigned m = 0; m < (1u << (TB - FB)); ++m) {
+      if (__builtin_popcount(m) != NSEL) continue;
+      const unsigned regs = (FB ? 1u : 0u) | (m << FB);
+      if (regs & warp_pref) continue;  // keep the pass's warp bits out of registers
+      std::array<int, 5> S{};
+      int n = 0;
+      for (int b = FB; b < TB; ++b)
+        if ((regs >> b) & 1) S[n++] = b;
+      sets.push_back(regs);
+      setS.push_back(S);
+    }
+    std::vector<St> beam(1);
+    const int total = n_ops_ + 1;
+    for (int depth = 0; depth < 64; ++depth) {
+      std::vector<St> next;
+      for (const St& st : beam) {
+        const int have = st.done.count();
+        std::vector<std::pair<int, int>> cand;  // (gain * 2 + a_type, set index)
+        for (size_t k = 0; k < sets.size(); ++k) {
+          if (depth == 0 && first_group_only && !a_type(setS[k].data())) continue;
+          const int gain = closure_bits(sets[k], st.done).count() - have;
+          if (gain > 0) cand.push_back({gain * 2 + (a_type(setS[k].data()) ? 1 : 0), (int)k});
+        }
+        std::sort(cand.begin(), cand.end(), [](auto& x, auto& y) { return x.first > y.first; });
+        for (int c = 0; c < (int)cand.size() && c < kExpand; ++c) {
+          St ns = st;
+          const int k = cand[c].second;
+          Phase f{};
+          for (int j = 0; j < NSEL; ++j) f.S[j] = setS[k][j];
+          const Bits nd = closure_bits(sets[k], st.done);
+          for (int i = 0; i <= n_ops_; ++i)
+            if (nd.get(i) && !st.done.get(i)) f.ops.push_back(i);
+          ns.done = nd;
+          ns.ph.push_back(f);
+          next.push_back(ns);
         }
       }
-      if (best.ops.empty()) return {};
-      for (int i : best.ops) done[i] = 1;
-      left -= (int)best.ops.size();
-      ph.push_back(best);
-      first = false;
+      if (next.empty()) return {};
+      std::vector<const St*> fin;
+      for (const St& st : next)
+        if (st.done.count() == total) fin.push_back(&st);
+      if (!fin.empty()) {
+        const St* best = fin[0];
+        for (const St* f : fin)
+          if (n_transitions(f->ph) < n_transitions(best->ph)) best = f;
+        return best->ph;
+      }
+      std::stable_sort(next.begin(), next.end(), [](const St& x, const St& y) { return x.done.count() > y.done.count(); });
+      // drop duplicates (same done set)
+      std::vector<St> keep;
+      for (const St& st : next) {
+        bool dup = false;
+        for (const St& k2 : keep)
+          if (!memcmp(k2.done.w, st.done.w, sizeof st.done.w) && k2.ph.back().S[0] == st.ph.back().S[0] &&
+              !memcmp(k2.ph.back().S, st.ph.back().S, sizeof st.ph.back().S)) {
+            dup = true;
+            break;
+          }
+        if (!dup) keep.push_back(st);
+        if ((int)keep.size() >= kBeam) break;
+      }
+      beam.swap(keep);
     }
-    return ph;
+    return {};
   }
   // the pass's warp bits: the 3 group tile bits with the fewest non-diagonal ops (untouched padding
   // slots first), so that phase changes keep them and transpose within each warp
@@ -956,6 +1026,7 @@ struct Gen {
     const uint64_t iters = nbu > (uint64_t)RED_MAX_BLOCKS ? nbu / RED_MAX_BLOCKS : 1;
     tile_iters = iters;
     build_dag();
+    build_predbits();
     choose_warp_bits();
     std::vector<Phase> pa = plan_greedy(true), pb = plan_greedy(false);
     const std::vector<Phase>& ph = n_transitions(pb) < n_transitions(pa) ? pb : pa;
