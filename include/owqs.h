@@ -157,6 +157,12 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
  * Errors: OWQS_E_ARG (size), OWQS_E_STATE (no pattern), OWQS_E_NOMEM, OWQS_E_CUDA. */
 owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps);
 
+/* Same from a HOST buffer at `precision` (64: interleaved float pairs, 8 B per amplitude; 128:
+ * double pairs). When it equals the context's precision the bytes go straight to the state
+ * (page-locked buffers by DMA): complex64 end-to-end runs move half the PCIe bytes of
+ * owqs_set_input. Errors as owqs_set_input, OWQS_E_ARG for another precision. */
+owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precision, int64_t n_amps);
+
 /* Same from a DEVICE buffer on the context's device. precision 64: interleaved float pairs;
  * 128: interleaved double pairs. The buffer is read during the call only. NCCL multi-rank: the
  * buffer holds this rank's shard (n_amps = 2^n_in / n_ranks); loopback: the full state. */
@@ -196,6 +202,10 @@ owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const
  * bit k <-> outputs[k]. Multi-rank (collective): gathered to rank 0, filled on rank 0 only
  * (amps may be NULL elsewhere); needs 2^n_out complex128 of free device memory on rank 0. */
 owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps);
+
+/* Same into a HOST buffer at `precision` (64: float pairs, 128: double pairs); complex64 halves
+ * the PCIe bytes of owqs_get_output. Single rank and loopback only (OWQS_E_ARG otherwise). */
+owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, int64_t n_amps);
 
 /* Output into a DEVICE buffer (precision 64: float pairs, 128: double pairs), n_amps >= 2^n_out
  * (single rank). */

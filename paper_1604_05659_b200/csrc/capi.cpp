@@ -493,14 +493,15 @@ owqs_status output_to_device_full(owqs_ctx* ctx, void* dst, int dst_prec) {
   return OWQS_OK;
 }
 
-owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
+owqs_status output_to_host(owqs_ctx* ctx, void* amps, int out_prec) {
   const uint64_t n = 1ull << ctx->hp.outputs.size();
+  const size_t oe = out_prec == 1 ? 16 : 8;
   if (ctx->n_ranks > 1) {
     void* d = nullptr;
-    if (ctx->rank == 0 || ctx->loopback) CU(cudaMalloc(&d, n * 16));
-    owqs_status s = output_to_device_full(ctx, d, 1);
+    if (ctx->rank == 0 || ctx->loopback) CU(cudaMalloc(&d, n * oe));
+    owqs_status s = output_to_device_full(ctx, d, out_prec);
     if (s == OWQS_OK && d) {
-      cudaError_t e = cudaMemcpyAsync(amps, d, n * 16, cudaMemcpyDeviceToHost, ctx->stream);
+      cudaError_t e = cudaMemcpyAsync(amps, d, n * oe, cudaMemcpyDeviceToHost, ctx->stream);
       if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
       if (e != cudaSuccess) s = fail(ctx, OWQS_E_CUDA, cudaGetErrorString(e));
     } else if (s == OWQS_OK) {
@@ -511,17 +512,21 @@ owqs_status output_to_host(owqs_ctx* ctx, double* amps) {
     return s;
   }
   const Program& pr = ctx->cm[ctx->out_cm].prog;
-  const uint64_t chunk = kStagingBytes / 16;
+  const uint64_t chunk = kStagingBytes / oe;
   const bool pinned = is_pinned_host(amps);  // page-locked caller buffer: DMA straight into it
+  char* dst = (char*)amps;
   for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
     uint64_t cnt = std::min(chunk, n - j0);
-    CU(launch_permute_out(ctx->shards[0].d_state, ctx->prec, ctx->d_staging, 1, (int)pr.out_slot.size(),
+    CU(launch_permute_out(ctx->shards[0].d_state, ctx->prec, ctx->d_staging, out_prec, (int)pr.out_slot.size(),
                           pr.out_slot.data(), j0, cnt, ctx->stream));
-    CU(cudaMemcpyAsync(pinned ? (void*)(amps + 2 * j0) : ctx->h_staging, ctx->d_staging, cnt * 16,
+    CU(cudaMemcpyAsync(pinned ? (void*)(dst + j0 * oe) : ctx->h_staging, ctx->d_staging, cnt * oe,
                        cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
-    if (!pinned) memcpy(amps + 2 * j0, ctx->h_staging, cnt * 16);
+    if (!pinned) {
+      CU(cudaStreamSynchronize(ctx->stream));
+      memcpy(dst + j0 * oe, ctx->h_staging, cnt * oe);
+    }
   }
+  CU(cudaStreamSynchronize(ctx->stream));
   return OWQS_OK;
 }
 
@@ -781,26 +786,32 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
 }
 
 owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps) {
+  return owqs_set_input_host(ctx, amps, 128, n_amps);
+}
+
+owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   const uint64_t n = 1ull << ctx->hp.inputs.size();
   if (!amps || n_amps != (int64_t)n) return fail(ctx, OWQS_E_ARG, "input must hold 2^n_in amplitudes");
+  if (precision != 64 && precision != 128) return fail(ctx, OWQS_E_ARG, "precision must be 64 or 128");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
+  const int sp = precision == 64 ? 0 : 1;
+  const size_t se = precision == 64 ? 8 : 16;
   const uint64_t per = n >> ctx->n_global;  // amplitudes per shard
-  const uint64_t chunk = kStagingBytes / 16;
+  const uint64_t chunk = kStagingBytes / se;
   for (size_t r = 0; r < ctx->shards.size(); ++r) {
     const uint64_t base = (uint64_t)ctx->shard_rank((int)r) * per;
+    const char* src0 = (const char*)amps + base * se;
+    if (sp == ctx->prec) {  // same precision: straight into the state (DMA when page-locked)
+      CU(cudaMemcpyAsync(ctx->shards[r].d_state, src0, per * se, cudaMemcpyHostToDevice, ctx->stream));
+      continue;
+    }
     for (uint64_t j0 = 0; j0 < per; j0 += chunk) {
-      uint64_t cnt = std::min(chunk, per - j0);
-      const double* src = amps + 2 * (base + j0);
-      if (ctx->prec == 1) {
-        CU(cudaMemcpyAsync((char*)ctx->shards[r].d_state + j0 * 16, src, cnt * 16, cudaMemcpyHostToDevice,
-                           ctx->stream));
-      } else {
-        CU(cudaMemcpyAsync(ctx->d_staging, src, cnt * 16, cudaMemcpyHostToDevice, ctx->stream));
-        CU(launch_convert_in(ctx->d_staging, 1, ctx->shards[r].d_state, 0, j0, cnt, ctx->stream));
-      }
+      const uint64_t cnt = std::min(chunk, per - j0);
+      CU(cudaMemcpyAsync(ctx->d_staging, src0 + j0 * se, cnt * se, cudaMemcpyHostToDevice, ctx->stream));
+      CU(launch_convert_in(ctx->d_staging, sp, ctx->shards[r].d_state, ctx->prec, j0, cnt, ctx->stream));
     }
   }
   CU(cudaStreamSynchronize(ctx->stream));
@@ -922,12 +933,17 @@ owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const
 }
 
 owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps) {
+  return owqs_get_output_host(ctx, amps, 128, n_amps);
+}
+
+owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
+  if (precision != 64 && precision != 128) return fail(ctx, OWQS_E_ARG, "precision must be 64 or 128");
   const uint64_t n = 1ull << ctx->hp.outputs.size();
   const bool root = ctx->n_ranks == 1 || ctx->loopback || ctx->rank == 0;
   if (root && (!amps || n_amps < (int64_t)n)) return fail(ctx, OWQS_E_ARG, "output buffer smaller than 2^n_out");
-  return output_to_host(ctx, amps);
+  return output_to_host(ctx, amps, precision == 64 ? 0 : 1);
 }
 
 owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precision, int64_t n_amps) {
@@ -1023,7 +1039,7 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
       ctx->has_input = true;
       s = run_internal(ctx, 1, OWQS_EOWQS, 0, nullptr);
       if (s != OWQS_OK) return s;
-      s = output_to_host(ctx, U + 2 * k * rows);
+      s = output_to_host(ctx, U + 2 * k * rows, 1);
       if (s != OWQS_OK) return s;
     }
   }

@@ -115,6 +115,11 @@ class Simulator:
         self.load_pattern(pattern.inputs, pattern.outputs, pattern.cmds)
 
     def set_input(self, amps: np.ndarray):
+        """Host input; complex64 arrays are passed as is (owqs_set_input_host, precision 64: half the
+        PCIe bytes on a complex64 context), anything else as complex128."""
+        if isinstance(amps, np.ndarray) and amps.dtype == np.complex64 and amps.flags.c_contiguous:
+            self._check(self._lib.owqs_set_input_host(self._h, C.c_void_p(amps.ctypes.data), 64, amps.size))
+            return
         a = np.ascontiguousarray(amps, dtype=np.complex128)
         self._check(self._lib.owqs_set_input(self._h, a.ctypes.data_as(C.POINTER(C.c_double)), a.size))
 
@@ -170,8 +175,9 @@ class Simulator:
         if out is None and root:
             out = np.empty(2 ** self.n_out, dtype=np.complex128)
         if root:
-            assert out.dtype == np.complex128 and out.flags.c_contiguous and out.size >= 2 ** self.n_out
-            self._check(self._lib.owqs_get_output(self._h, out.ctypes.data_as(C.POINTER(C.c_double)), out.size))
+            assert out.dtype in (np.complex128, np.complex64) and out.flags.c_contiguous and out.size >= 2 ** self.n_out
+            prec = 64 if out.dtype == np.complex64 else 128
+            self._check(self._lib.owqs_get_output_host(self._h, C.c_void_p(out.ctypes.data), prec, out.size))
             return out
         self._check(self._lib.owqs_get_output(self._h, None, 0))
         return None
