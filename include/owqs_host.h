@@ -64,6 +64,18 @@ owqs_status owqs_host_jit(owqs_host_plan* h, int64_t* n_kernels, int64_t* n_jit_
  * NUL-terminated, truncated if short); returns its length in *len, 0 if the step is not generated.
  * step = -1: the common prelude every generated translation unit starts with. */
 owqs_status owqs_host_jit_source(const owqs_host_plan* h, int64_t step, char* buf, int64_t cap, int64_t* len);
+/* Measurement-calculus standardisation: rewrite the pattern
+ * given to owqs_host_compile into standard form N* E* M* C* (all N, then all E, then the M in their
+ * given order with the absorbed corrections in their s/t domains, then the outputs' X then Z
+ * corrections). Outcome labels and branch probabilities are unchanged; the output equals the
+ * original's up to a branch-dependent global phase (reading R-18). signal_shift != 0 also
+ * removes every t-domain (signal shifting): M_v's outcome label becomes s_v(new) = s_v(old) + |T_v|
+ * with T_v returned in shift_pool. Two-call protocol: pass NULL buffers to get the sizes.
+ * cmds/pool: output command list (qubit ids as in the input, domains as slices of pool);
+ * shift_slices: 2 int32 (offset, length into shift_pool) per output command (length 0 unless a
+ * shifted M); sizes[4] = {n_cmds, pool_len, shift_len, n_x_absorbed}. */
+owqs_status owqs_host_standardize(const owqs_host_plan* h, int32_t signal_shift, owqs_cmd* cmds, int32_t* pool,
+                                  int32_t* shift_slices, int32_t* shift_pool, int64_t* sizes);
 const char* owqs_host_error(const owqs_host_plan* h);
 void owqs_host_free(owqs_host_plan* h);
 

@@ -20,7 +20,7 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernels.cu"]
-CPP_SOURCES = ["scheduler.cpp", "gflow.cpp", "jit.cpp", "capi.cpp", "host_api.cpp"]
+CPP_SOURCES = ["scheduler.cpp", "gflow.cpp", "standardize.cpp", "jit.cpp", "capi.cpp", "host_api.cpp"]
 HEADERS = ["owqs_internal.h", "scheduler.h", "device_common.cuh", "jit.h"]
 PRELUDE = [("kPreludeInternal", "owqs_internal.h"), ("kPreludeCommon", "device_common.cuh")]
 

@@ -153,6 +153,54 @@ owqs_status owqs_host_jit_source(const owqs_host_plan* h, int64_t step, char* bu
   return OWQS_OK;
 }
 
+owqs_status owqs_host_standardize(const owqs_host_plan* h, int32_t signal_shift, owqs_cmd* cmds, int32_t* pool,
+                                  int32_t* shift_slices, int32_t* shift_pool, int64_t* sizes) {
+  if (!h || !sizes) return OWQS_E_ARG;
+  std::vector<HCmd> out;
+  std::vector<std::vector<int>> shift;
+  int nabs = 0, nsg = 0;
+  std::string e = standardize_pattern(h->hp, signal_shift != 0, out, shift, &nabs, &nsg);
+  if (!e.empty()) return OWQS_E_PATTERN;
+  int64_t plen = 0, slen = 0;
+  for (size_t k = 0; k < out.size(); ++k) {
+    const HCmd& c = out[k];
+    if (cmds) {
+      owqs_cmd& o = cmds[k];
+      memset(&o, 0, sizeof o);
+      o.kind = c.kind;
+      o.q0 = h->hp.ext_id[c.q0];
+      o.q1 = c.kind == H_E ? h->hp.ext_id[c.q1] : 0;
+      o.angle = c.angle;
+      o.s_off = (int32_t)plen;
+      o.s_len = (int32_t)c.sdom.size();
+      if (pool)
+        for (size_t j = 0; j < c.sdom.size(); ++j) pool[plen + j] = h->hp.ext_id[c.sdom[j]];
+      o.t_off = (int32_t)(plen + c.sdom.size());
+      o.t_len = (int32_t)c.tdom.size();
+      if (pool)
+        for (size_t j = 0; j < c.tdom.size(); ++j) pool[plen + c.sdom.size() + j] = h->hp.ext_id[c.tdom[j]];
+      if (o.s_len == 0) o.s_off = 0;
+      if (o.t_len == 0) o.t_off = 0;
+    }
+    plen += (int64_t)(c.sdom.size() + c.tdom.size());
+    const std::vector<int>* sh = (c.kind == H_M && !shift.empty()) ? &shift[c.q0] : nullptr;
+    if (shift_slices) {
+      shift_slices[2 * k] = (int32_t)slen;
+      shift_slices[2 * k + 1] = sh ? (int32_t)sh->size() : 0;
+    }
+    if (sh) {
+      if (shift_pool)
+        for (size_t j = 0; j < sh->size(); ++j) shift_pool[slen + j] = h->hp.ext_id[(*sh)[j]];
+      slen += (int64_t)sh->size();
+    }
+  }
+  sizes[0] = (int64_t)out.size();
+  sizes[1] = plen;
+  sizes[2] = slen;
+  sizes[3] = nabs;
+  return OWQS_OK;
+}
+
 const char* owqs_host_error(const owqs_host_plan* h) { return h ? h->err.c_str() : "NULL handle"; }
 
 void owqs_host_free(owqs_host_plan* h) { delete h; }

@@ -77,6 +77,11 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int s
 void plan_and_compile(const HostPattern& hp, int mode, int seg_bits, bool fuse, bool given_order,
                       const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0, int kwide = KMAX_AOT);
 
+// Standard form N* E* M* C* of a validated pattern (standardize.cpp); with
+// signal_shift, t-domains are removed and returned per measured qubit in `shift` (new labels).
+std::string standardize_pattern(const HostPattern& hp, bool signal_shift, std::vector<HCmd>& out,
+                                std::vector<std::vector<int>>& shift, int* n_x_absorbed, int* n_signs);
+
 // gflow of the pattern's open graph ([25]): "" if found, else the reason. layer[q] = 0
 // for outputs, k >= 1 for the k-th backward layer; g[q] = correction set of measured q.
 std::string find_gflow(const HostPattern& hp, std::vector<int>& layer, std::vector<std::vector<int>>& g);

@@ -87,6 +87,36 @@ def jit_host(pattern, mode: str = "sampled", precision: int = 64, flags: int = 0
         L.owqs_host_free(h)
 
 
+def standardize(pattern, signal_shift: bool = False):
+    """Standard form N* E* M* C* of a pattern (owqs_host_standardize).
+    Returns (Pattern, shifts): shifts maps a measured qubit to its removed t-domain T (signal
+    shifting: s_v(new) = s_v(old) + |T_v| over the new labels), empty without signal_shift."""
+    from workloads.patterns import Cmd, Pattern
+    L, h = _host_handle(pattern, "sampled", 128, 0, None, 1)
+    try:
+        sizes = (C.c_int64 * 4)()
+        st = L.owqs_host_standardize(h, int(signal_shift), None, None, None, None, sizes)
+        if st != 0:
+            raise OwqsError(st, L.owqs_host_error(h).decode())
+        n, plen, slen = sizes[0], sizes[1], sizes[2]
+        cmds = (_capi.owqs_cmd * max(1, n))()
+        pool = (C.c_int32 * max(1, plen))()
+        sl = (C.c_int32 * max(2, 2 * n))()
+        sp = (C.c_int32 * max(1, slen))()
+        L.owqs_host_standardize(h, int(signal_shift), cmds, pool, sl, sp, sizes)
+        out, shifts = [], {}
+        for k in range(n):
+            c = cmds[k]
+            sd = tuple(pool[c.s_off + j] for j in range(c.s_len))
+            td = tuple(pool[c.t_off + j] for j in range(c.t_len))
+            out.append(Cmd(c.kind, c.q0, c.q1 if c.kind == 1 else -1, c.angle, sd, td))
+            if sl[2 * k + 1]:
+                shifts[c.q0] = tuple(sp[sl[2 * k] + j] for j in range(sl[2 * k + 1]))
+        return Pattern(list(pattern.inputs), list(pattern.outputs), out, (pattern.name or "") + ":std"), shifts
+    finally:
+        L.owqs_host_free(h)
+
+
 def compile_host(pattern, mode: str = "sampled", precision: int = 128, flags: int = 0,
                  weights: Optional[Sequence[float]] = None, n_ranks: int = 1) -> HostProgram:
     L = lib()

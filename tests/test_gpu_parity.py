@@ -313,3 +313,22 @@ def test_config5_verification_instance(require_gpu):
     finally:
         a.close()
         b.close()
+
+
+@pytest.mark.parametrize("k", range(8))
+def test_standard_form_patterns_vs_oracle(sim, k):
+    """NEXT-2: standard-form (and signal-shifted) rewrites of wild patterns run on the GPU with exact
+    amplitude parity against the oracle on the same rewritten pattern (PROA on standard form)."""
+    from paper_1604_05659_b200.host import standardize
+    p = (W.random_general_pattern(k, n_in=2, n_total=9, n_out=2) if k < 5 else
+         [W.config_pattern("C1", seed=1), W.cluster_pattern(4, 4, seed=3), W.config_pattern("QFT:2")][k - 5])
+    for shift in (False, True):
+        std, _ = standardize(p, signal_shift=shift)
+        psi = haar_state(len(p.inputs), 60 + k)
+        rng = np.random.default_rng(k)
+        for _ in range(3):
+            try:
+                check(sim, std, psi, "forced", forced=rng.integers(0, 2, std.n_measure))
+            except (OwqsError, oracle.OracleError):
+                pass  # impossible forced branch of a non-deterministic pattern (both sides refuse)
+        check(sim, std, psi, "sampled", seed=k)
