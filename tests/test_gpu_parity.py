@@ -326,9 +326,12 @@ def test_standard_form_patterns_vs_oracle(sim, k):
         std, _ = standardize(p, signal_shift=shift)
         psi = haar_state(len(p.inputs), 60 + k)
         rng = np.random.default_rng(k)
+        # random patterns are not deterministic: PROA's order changes per-M probabilities (R-8),
+        # the joint branch probability and the amplitudes are compared
+        order = False if k < 5 else None
         for _ in range(3):
             try:
-                check(sim, std, psi, "forced", forced=rng.integers(0, 2, std.n_measure))
+                check(sim, std, psi, "forced", forced=rng.integers(0, 2, std.n_measure), same_order=order)
             except (OwqsError, oracle.OracleError):
                 pass  # impossible forced branch of a non-deterministic pattern (both sides refuse)
-        check(sim, std, psi, "sampled", seed=k)
+        check(sim, std, psi, "sampled", seed=k, same_order=order)
