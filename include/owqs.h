@@ -225,6 +225,13 @@ owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2);
  * max_unitarity_err (may be NULL): max |(U^dag U - I)_ij|. Overwrites the current input. */
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err);
 
+/* Same result from ONE run on the Choi state: the loaded pattern is
+ * extended by |I| reference qubits that no command touches (inputs I + R, outputs O + R) and run
+ * (positive EOWQS branch) on sum_k |k>_I |k>_R / sqrt(2^|I|); the output, scaled by sqrt(2^|I|), is U
+ * column-major. Runs at the pattern's width + |I| in a temporary context on the same device;
+ * |I| + |O| <= 30. Same gflow check and errors as owqs_recognize. */
+owqs_status owqs_recognize_choi(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err);
+
 /* gflow of the pattern's open graph (L372, Mhalla-Perdrix [25]; all measurements in the XY plane):
  * OWQS_OK if one exists, else OWQS_E_NO_GFLOW ("the pattern is reported as an incorrect one").
  * layers[n_measure] (may be NULL): backward layer of each measured qubit (given-order ordinal;

@@ -21,7 +21,7 @@ KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce",
 EXPORTED = ["owqs_create", "owqs_destroy", "owqs_load_pattern", "owqs_set_input", "owqs_set_input_host",
             "owqs_get_output_host", "owqs_set_input_device",
             "owqs_set_input_random", "owqs_run", "owqs_run_batch", "owqs_get_output", "owqs_get_output_device",
-            "owqs_output_inner", "owqs_output_norm", "owqs_nccl_unique_id", "owqs_recognize",
+            "owqs_output_inner", "owqs_output_norm", "owqs_nccl_unique_id", "owqs_recognize", "owqs_recognize_choi",
             "owqs_pattern_info", "owqs_plan_order", "owqs_gflow",
             "owqs_set_proa_weights", "owqs_stats", "owqs_launch_profile", "owqs_last_error", "owqs_version"]
 
@@ -75,6 +75,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "owqs_output_norm": (C.c_int, [ctx, P(C.c_double)]),
         "owqs_nccl_unique_id": (C.c_int, [C.c_void_p]),
         "owqs_recognize": (C.c_int, [ctx, P(C.c_double), C.c_int64, P(C.c_double)]),
+        "owqs_recognize_choi": (C.c_int, [ctx, P(C.c_double), C.c_int64, P(C.c_double)]),
         "owqs_pattern_info": (C.c_int, [ctx, P(C.c_int64), P(C.c_int32), P(C.c_int32), P(C.c_int32)]),
         "owqs_gflow": (C.c_int, [ctx, P(C.c_int32), P(C.c_int32)]),
         "owqs_plan_order": (C.c_int, [ctx, C.c_int, P(C.c_int32), P(C.c_int32), C.c_int64]),

@@ -1062,6 +1062,92 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
   return OWQS_OK;
 }
 
+// Recognition from the Choi state: the pattern extended by |I|
+// reference qubits that no command touches (inputs I + R, outputs O + R), run once on the maximally
+// entangled input sum_k |k>_I |k>_R / sqrt(d) (positive EOWQS branch), gives sum_k (U |k>)_O |k>_R /
+// sqrt(d): with outputs O in bits 0..|O|-1 and R above them, the output array IS U in column-major
+// order up to the factor 1/sqrt(d). One run at width + |I| instead of 2^|I| runs.
+owqs_status owqs_recognize_choi(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
+  if (!ctx) return OWQS_E_ARG;
+  if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "recognize before load_pattern");
+  if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "recognize runs on a single rank");
+  const HostPattern& hp = ctx->hp;
+  const int ni = (int)hp.inputs.size(), no = (int)hp.outputs.size();
+  if (ni + no > 30) return fail(ctx, OWQS_E_ARG, "Choi recognition is limited to |I| + |O| <= 30");
+  const uint64_t rows = 1ull << no, cols = 1ull << ni;
+  if (!U || n < (int64_t)(rows * cols)) return fail(ctx, OWQS_E_ARG, "U must hold 2^n_out * 2^n_in entries");
+  owqs_status s = gflow_gate(ctx);
+  if (s != OWQS_OK) return s;
+  // the pattern's commands with external ids, plus |I| fresh reference ids
+  std::vector<owqs_cmd> cmds;
+  std::vector<int32_t> pool;
+  int32_t maxid = 0;
+  for (int32_t e : hp.ext_id) maxid = std::max(maxid, e);
+  for (const HCmd& c : hp.cmds) {
+    owqs_cmd o{};
+    o.kind = c.kind;
+    o.q0 = hp.ext_id[c.q0];
+    o.q1 = c.kind == H_E ? hp.ext_id[c.q1] : 0;
+    o.angle = c.angle;
+    o.s_off = (int32_t)pool.size();
+    o.s_len = (int32_t)c.sdom.size();
+    for (int q : c.sdom) pool.push_back(hp.ext_id[q]);
+    o.t_off = (int32_t)pool.size();
+    o.t_len = (int32_t)c.tdom.size();
+    for (int q : c.tdom) pool.push_back(hp.ext_id[q]);
+    cmds.push_back(o);
+  }
+  std::vector<int32_t> ins, outs;
+  for (int q : hp.inputs) ins.push_back(hp.ext_id[q]);
+  for (int q : hp.outputs) outs.push_back(hp.ext_id[q]);
+  for (int r = 0; r < ni; ++r) {
+    ins.push_back(maxid + 1 + r);
+    outs.push_back(maxid + 1 + r);
+  }
+  owqs_config cfg = ctx->cfg;
+  cfg.flags |= OWQS_FLAG_NO_GFLOW;  // checked above on the same open graph
+  cfg.stream = nullptr;
+  owqs_ctx* sub = nullptr;
+  if (owqs_create(&cfg, &sub) != OWQS_OK) return fail(ctx, OWQS_E_CUDA, "Choi recognition: context creation failed");
+  auto done = [&](owqs_status st, const std::string& why) {
+    if (st != OWQS_OK) ctx->err = "Choi recognition: " + why + ": " + owqs_last_error(sub);
+    owqs_destroy(sub);
+    return st;
+  };
+  s = owqs_load_pattern(sub, ins.data(), (int32_t)ins.size(), outs.data(), (int32_t)outs.size(), cmds.data(),
+                        (int64_t)cmds.size(), pool.data(), (int64_t)pool.size());
+  if (s != OWQS_OK) return done(s, "load");
+  std::vector<double> in(2 * cols * cols, 0.0);
+  const double amp = 1.0 / std::sqrt((double)cols);
+  for (uint64_t k = 0; k < cols; ++k) in[2 * (k + (k << ni))] = amp;
+  s = owqs_set_input_host(sub, in.data(), 128, (int64_t)(cols * cols));
+  if (s != OWQS_OK) return done(s, "input");
+  s = owqs_run(sub, OWQS_EOWQS, 0, nullptr, nullptr, nullptr);
+  if (s != OWQS_OK) return done(s, "run");
+  s = owqs_get_output_host(sub, U, 128, (int64_t)(rows * cols));
+  if (s != OWQS_OK) return done(s, "output");
+  const double sc = std::sqrt((double)cols);
+  for (uint64_t i = 0; i < 2 * rows * cols; ++i) U[i] *= sc;
+  done(OWQS_OK, "");
+  if (max_unitarity_err) {
+    double worst = 0;
+    for (uint64_t i = 0; i < cols; ++i)
+      for (uint64_t j = 0; j < cols; ++j) {
+        double sr = 0, si = 0;
+        for (uint64_t r = 0; r < rows; ++r) {
+          double ar = U[2 * (i * rows + r)], ai = U[2 * (i * rows + r) + 1];
+          double br = U[2 * (j * rows + r)], bi = U[2 * (j * rows + r) + 1];
+          sr += ar * br + ai * bi;
+          si += ar * bi - ai * br;
+        }
+        if (i == j) sr -= 1.0;
+        worst = std::max(worst, std::hypot(sr, si));
+      }
+    *max_unitarity_err = worst;
+  }
+  return OWQS_OK;
+}
+
 owqs_status owqs_gflow(owqs_ctx* ctx, int32_t* layers, int32_t* depth) {
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "no pattern loaded");

@@ -195,10 +195,13 @@ class Simulator:
         self._check(self._lib.owqs_output_inner(self._h, other._h, C.byref(re), C.byref(im)))
         return complex(re.value, im.value)
 
-    def recognize(self) -> Tuple[np.ndarray, float]:
+    def recognize(self, choi: bool = False) -> Tuple[np.ndarray, float]:
+        """(U, max unitarity error). choi=True: one run on the Choi state (owqs_recognize_choi)
+        instead of one run per basis input."""
         U = np.empty((2 ** self.n_in, 2 ** self.n_out), dtype=np.complex128)  # column-major storage
         err = C.c_double()
-        self._check(self._lib.owqs_recognize(self._h, U.ctypes.data_as(C.POINTER(C.c_double)), U.size, C.byref(err)))
+        fn = self._lib.owqs_recognize_choi if choi else self._lib.owqs_recognize
+        self._check(fn(self._h, U.ctypes.data_as(C.POINTER(C.c_double)), U.size, C.byref(err)))
         return U.T.copy(), err.value
 
     def gflow(self):

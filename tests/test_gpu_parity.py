@@ -194,6 +194,21 @@ def test_recognize_cnot_and_circuits(sim):
         assert np.max(np.abs(U - oracle.recognize(p))) <= TOL[sim.precision]["amp"]
 
 
+def test_recognize_choi_matches_basis_runs(sim):
+    """NEXT-3: recognition from one Choi-state run equals the per-basis-input recognition and the
+    oracle's brute-force unitary (CNOT, random J/CZ circuits, a QFT, a flow cluster)."""
+    pats = [W.cnot_pattern_eq22(), W.config_pattern("C1", seed=4), W.config_pattern("QFT:3"),
+            W.cluster_pattern(3, 3, seed=1)]
+    for p in pats:
+        sim.load(p)
+        U, err = sim.recognize(choi=True)
+        Ub, _ = sim.recognize()
+        assert np.max(np.abs(U - Ub)) <= 2 * TOL[sim.precision]["amp"]
+        assert err < (1e-10 if sim.precision == 128 else 1e-4)
+        if len(p.inputs) <= 3:
+            assert np.max(np.abs(U - oracle.recognize(p))) <= TOL[sim.precision]["amp"]
+
+
 def test_device_haar_generator(sim):
     """owqs_set_input_random follows the documented counter generator (workloads/inputs.py)."""
     n = 12
