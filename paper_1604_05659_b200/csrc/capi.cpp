@@ -124,7 +124,8 @@ double kernels_per_run(const owqs_ctx* ctx, const CompiledMode& m) {
   for (size_t i = 0; i < m.prog.steps.size(); ++i) {
     const StepDesc& s = m.prog.steps[i];
     n += 1;
-    if (i < m.jit_name.size() && !m.jit_name[i].empty() && jit_engine(s, ctx->prec) == 2)
+    if (i < m.jit_name.size() && !m.jit_name[i].empty() && jit_engine(s, ctx->prec) == 2 &&
+        !jit_tile_small(s, ctx->prec))
       n += 1 + (s.red_kind != RED_NONE ? 1 : 0);  // decide + grid finish
   }
   return n;
@@ -395,14 +396,15 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
       } else {
         const bool jit = !m.jit_fn.empty() && m.jit_fn[i];
         const int eng = jit ? jit_engine(s, ctx->prec) : 0;
-        if (eng == 2) CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream));
+        const bool small = eng == 2 && jit_tile_small(s, ctx->prec);
+        if (eng == 2 && !small) CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream));
         for (size_t r = 0; r < ctx->shards.size(); ++r) {
           if (jit)
             CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream));
           else
             CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
         }
-        if (eng == 2 && s.red_kind != RED_NONE)  // tile passes leave block partials
+        if (eng == 2 && !small && s.red_kind != RED_NONE)  // tile passes leave block partials
           for (size_t r = 0; r < ctx->shards.size(); ++r)
             CU(launch_grid_finish(dev_ptrs(ctx, m, (int)r), jit_tile_blocks(s, ctx->prec),
                                   s.red_kind == RED_NORM ? 1 : 4, ctx->stream));

@@ -1020,6 +1020,7 @@ struct Gen {
   // deterministic two-level grid reduction ----
   std::string run_tile() {
     const int nbf = d.n_bfly;
+    const bool small = jit_tile_small(d, prec);
     const int red = d.red_kind;
     const int nred = red == RED_NONE ? 0 : (red == RED_NORM ? 1 : 4);
     const uint64_t nbu = 1ull << (d.width - TB);
@@ -1053,7 +1054,8 @@ struct Gen {
       for (int l : plays) n_trans += l != cur, cur = l;
       n_trans += l_store != cur;
     }
-    o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* pc) {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
+    o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* "
+      << (small ? "pc_global" : "pc") << ") {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
       << "  using namespace owqs;\n"
       << "  // tile engine: width " << d.width << ", tile group slots";
     for (int j = 0; j < KTILE; ++j) o << " " << gs[j];
@@ -1067,6 +1069,22 @@ struct Gen {
       o << ", " << ph[f].ops.size() << " op(s)\n";
     }
     if (n_trans) o << "  extern __shared__ __align__(16) unsigned char dsm[];\n";
+    if (small) {
+      // grid of <= 2 waves (L2-resident states): decisions by this kernel's own prologue (every CTA,
+      // warp-parallel) and the fenced last-block reduction -- one launch per pass, no decide /
+      // finish kernels
+      o << "  (void)pc_global;\n  __shared__ PassShared sh;\n  __shared__ PassCoef spc;\n"
+        << "  pass_prologue(d, p, sh);\n"
+        << "  for (int b = threadIdx.x; b < d.n_bfly; b += blockDim.x) {\n"
+        << "    const double ar = sh.ka[b][0], ai = sh.ka[b][1];\n"
+        << "    spc.ard[b] = ar; spc.aid[b] = ai; spc.ar[b] = (float)ar;\n"
+        << "    const float fai = (float)ai;\n"
+        << "    spc.B[b] = ((unsigned long long)__float_as_uint(fai) << 32) | (unsigned long long)__float_as_uint(-fai);\n"
+        << "  }\n"
+        << "  for (int i = threadIdx.x; i < d.n_ops; i += blockDim.x) spc.cond[i] = sh.cond[i];\n"
+        << "  if (threadIdx.x == 0) spc.scale = sh.scale;\n  __syncthreads();\n"
+        << "  const PassCoef* pc = &spc;\n";
+    }
     o << "  __shared__ double red_s[32][4];\n  __shared__ int flag_s;\n"
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  const unsigned rk = p.rank; (void)rk; (void)d;\n"
@@ -1104,7 +1122,7 @@ struct Gen {
           << "ull) << 5) + lane)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
     // launched right behind decide_kernel (programmatic dependent launch): the loads above overlap
     // the decisions; wait for them before the first read of PassCoef
-    o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    if (!small) o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
     if (nbf > 0 && prec == 0) o << "    const float sck = (float)pc->scale;\n    const u64 scale = bc(sck); (void)scale;\n";
     if (nbf > 0 && prec == 1) o << "    const double sck = pc->scale;\n    const double scale = sck; (void)scale;\n";
     lay = l_load;
@@ -1140,7 +1158,9 @@ struct Gen {
           << ", " << XI(q) << "));\n";
     o << "  }\n";
     if (nred > 0)
-      o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n  block_partial<" << nred << ">(acc, p, red_s);  // grid_finish_kernel sums\n";
+      o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n"
+        << (small ? "  reduce_finish_grid<" : "  block_partial<") << nred
+        << (small ? ">(acc, p, red_s, &flag_s);\n" : ">(acc, p, red_s);  // grid_finish_kernel sums\n");
     o << "}\n";
     return o.str();
   }
@@ -1207,6 +1227,17 @@ int jit_smem_carveout(int engine, int prec) {
 }
 
 int jit_block_threads(int engine, int prec) { return (engine == 2 && prec == 0) ? (32 << tile_geom().wb) : 256; }
+
+bool jit_tile_small(const StepDesc& d, int prec) {
+  if (jit_engine(d, prec) != 2) return false;
+  static const unsigned lim = [] {
+    const char* e = getenv("OWQS_TILE_SMALL_MAX");
+    // default off: measured on C2 (QFT-20, 128 CTAs per pass) the per-CTA prologue is slower than
+    // one decide_kernel overlapped by programmatic dependent launch (0.912 vs 0.869 ms per run)
+    return e ? (unsigned)atoi(e) : 0u;
+  }();
+  return jit_tile_blocks(d, prec) <= lim;
+}
 
 unsigned jit_tile_blocks(const StepDesc& d, int prec) {
   const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
@@ -1317,7 +1348,7 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = getenv("OWQS_NO_PDL") ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = (getenv("OWQS_NO_PDL") || jit_tile_small(d, prec)) ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelExC(&cfg, (const void*)k, args);

@@ -31,6 +31,9 @@ bool jit_eligible(const StepDesc& d, int prec);
 // Dynamic shared memory (bytes) and threads per block an engine's kernels are launched with.
 int jit_dyn_smem(int engine);
 int jit_block_threads(int engine, int prec);
+// A tile-engine pass small enough (<= 2 waves) to decide and reduce inside its own kernel (no
+// decide_kernel / grid_finish_kernel launches).
+bool jit_tile_small(const StepDesc& d, int prec);
 // Grid of a tile-engine pass (= its number of block partials for grid_finish_kernel).
 unsigned jit_tile_blocks(const StepDesc& d, int prec);
 // cudaFuncAttributePreferredSharedMemoryCarveout (percent) for an engine's kernels; -1 = default

@@ -40,6 +40,31 @@ __global__ void __launch_bounds__(256, 2) np_k(float4* __restrict__ a, u64 c) {
     __stcs(t + (warp * 16 + q) * 32 + lane, make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
 }
 
+// same tile, but the warp bits are segment slots t3..t5 (64 B sub-rows) and lane bits 2..4 are
+// group bits: every warp instruction reads 8 chunks of 64 B (the 8 warps of the CTA together cover
+// whole 512 B rows) -- lets phase changes keep the warp bits when slots 3..5 are untouched
+template <int K>
+__global__ void __launch_bounds__(256, 2) np64_k(float4* __restrict__ a, u64 c) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float4* t = a + (size_t)blockIdx.x * 4096;
+  // tile float4 index: row r (16 rows of 32 float4 = 512 B), within row: (warp << 2) | (lane & 3)
+  // rows: lane bits 2..4 (3 bits) + register bits (q: 1 bit... 16 loads: q bits 0..3 -> rows)
+  u64 x[32];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int row = ((lane >> 2) + (q << 3)) & 127;  // 128 rows in the 64 KB tile
+    const float4 v = __ldcs(t + row * 32 + (warp << 2) + (lane & 3));
+    x[2 * q] = pk(v.x, v.y);
+    x[2 * q + 1] = pk(v.z, v.w);
+  }
+  work<K>(x, c);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int row = ((lane >> 2) + (q << 3)) & 127;
+    __stcs(t + row * 32 + (warp << 2) + (lane & 3), make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
+  }
+}
+
 __device__ __forceinline__ void mbar_init(unsigned a, unsigned n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned tx) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(tx) : "memory"); }
 __device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) {
@@ -134,6 +159,68 @@ __global__ void __launch_bounds__(256, 2) npt_k(float4* __restrict__ a, u64 c) {
     __stcs(t + (warp * 16 + q) * 32 + lane, make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
 }
 
+template <int K, int T>
+__global__ void __launch_bounds__(256, 1) tmat_k(float4* __restrict__ a, u64 c, int ntiles) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) unsigned long long mb[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned sm_s = (unsigned)__cvta_generic_to_shared(sm), mb_s = (unsigned)__cvta_generic_to_shared(mb);
+  if (threadIdx.x == 0) {
+    mbar_init(mb_s, 1);
+    mbar_init(mb_s + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int tile, int s) {
+    if (threadIdx.x == 0) mbar_expect_tx(mb_s + 8 * s, 65536u);
+    __syncwarp();
+    if (threadIdx.x < 32)  // 32 lanes x 2 KB
+      bulk_g2s(sm_s + s * 65536 + threadIdx.x * 2048, (const char*)(a + (size_t)tile * 4096) + threadIdx.x * 2048, 2048u,
+               mb_s + 8 * s);
+  };
+  int k = 0;
+  if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++k) {
+    const int s = k & 1;
+    const int nxt = tile + gridDim.x;
+    if (nxt < ntiles) issue(nxt, s ^ 1);  // other buffer: freed by the barrier that ended tile k-1
+    mbar_wait(mb_s + 8 * s, (k >> 1) & 1);
+    float4* st = reinterpret_cast<float4*>(sm + s * 65536);
+    u64 x[32];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const float4 v = st[(warp * 16 + q) * 32 + lane];
+      x[2 * q] = pk(v.x, v.y);
+      x[2 * q + 1] = pk(v.z, v.w);
+    }
+#pragma unroll
+    for (int r = 0; r < T; ++r) {
+      work<K / (T + 1)>(x, c);
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int u = (warp * 16 + q) * 32 + lane;
+        st[u] = make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1]));
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int u = (q * 8 + warp) * 32 + lane;
+        const float4 v = st[u];
+        x[2 * q] = pk(v.x, v.y);
+        x[2 * q + 1] = pk(v.z, v.w);
+      }
+    }
+    work<K - T * (K / (T + 1))>(x, c);
+    float4* t = a + (size_t)tile * 4096;
+#pragma unroll
+    for (int q = 0; q < 16; ++q)
+      __stcs(t + (warp * 16 + q) * 32 + lane, make_float4(lo(x[2 * q]), hi(x[2 * q]), lo(x[2 * q + 1]), hi(x[2 * q + 1])));
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();  // buffer s free for the prefetch issued in iteration k + 1
+  }
+}
+
 int main() {
   const size_t bytes = 2ull << 30, n4 = bytes / 16;
   const int ntiles = (int)(n4 / 4096);
@@ -168,23 +255,25 @@ int main() {
   run("np", K, [&] { np_k<K><<<ntiles, 256>>>(a, c); });                                        \
   cudaFuncSetAttribute(tma_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 65536);       \
   run("tma", K, [&] { tma_k<K><<<sms, 256, 2 * 65536>>>(a, c, ntiles); });
-  BOTH(16)
-  // occupancy (CTAs/SM from the shared-memory request) vs L1 size (the carveout percentage)
-  for (int kb : {64, 75, 90, 110}) {
-    for (int co : {-1, 50, 67, 80, 100}) {
-      cudaFuncSetAttribute(np_k<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, kb * 1024);
-      cudaFuncSetAttribute(np_k<16>, cudaFuncAttributePreferredSharedMemoryCarveout, co);
-      int nb = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, np_k<16>, 256, kb * 1024);
-      char nm[40];
-      snprintf(nm, sizeof nm, "np%dKB/c%d/%d", kb, co, nb);
-      run(nm, 16, [&] { np_k<16><<<ntiles, 256, kb * 1024>>>(a, c); });
-    }
-  }
-  cudaFuncSetAttribute(np_k<16>, cudaFuncAttributePreferredSharedMemoryCarveout, -1);
+  // the tile engine's configuration: 2 CTAs/SM (75 KB shared each), carveout 67 % (L1 ~92 KB)
+#define NPC(K)                                                                                    \
+  cudaFuncSetAttribute(np_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);          \
+  cudaFuncSetAttribute(np_k<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 67);              \
+  run("np75/c67", K, [&] { np_k<K><<<ntiles, 256, 75 * 1024>>>(a, c); });
+  NPC(28) NPC(88)
+#define NP64(K)                                                                                   \
+  cudaFuncSetAttribute(np64_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);        \
+  cudaFuncSetAttribute(np64_k<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 67);            \
+  run("np64B/c67", K, [&] { np64_k<K><<<ntiles, 256, 75 * 1024>>>(a, c); });
+
 #define TR(K, T)                                                                                   \
   cudaFuncSetAttribute(npt_k<K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4608 * 16);        \
-  run("np+T" #T, K, [&] { npt_k<K, T><<<ntiles, 256, 4608 * 16>>>(a, c); });
-  TR(16, 0) TR(16, 1)
+  cudaFuncSetAttribute(npt_k<K, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 67);            \
+  run("np+T" #T "/c67", K, [&] { npt_k<K, T><<<ntiles, 256, 4608 * 16>>>(a, c); });
+  TR(28, 1) TR(28, 0) TR(16, 1) TR(48, 2) TR(88, 4)
+#define TT(K, T)                                                                                   \
+  cudaFuncSetAttribute(tmat_k<K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 65536);       \
+  run("tma+T" #T, K, [&] { tmat_k<K, T><<<sms, 256, 2 * 65536>>>(a, c, ntiles); });
+  TT(16, 0) TT(16, 1) TT(28, 0) TT(28, 1) TT(28, 2) TT(48, 2) TT(88, 4)
   return 0;
 }
