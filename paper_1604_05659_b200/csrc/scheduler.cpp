@@ -670,16 +670,21 @@ struct Packer {
     return d;
   }
   // the state produced by the last emitted step must carry its norm (first butterfly of a pass)
-  void need_norm_before() {
+  // false: nothing computed yet -- the state is the caller's normalised input (set_input requires
+  // ||psi||^2 = 1, the oracle checks it to 1e-9), so the first decision uses norm 1 and no
+  // read-only norm pass is spent on it
+  bool need_norm_before() {
     StepDesc* last = last_compute();
-    if (last && last->red_kind == RED_NORM) return;
-    if (last && last->red_kind == RED_NONE) {
+    if (!last) return false;
+    if (last->red_kind == RED_NORM) return true;
+    if (last->red_kind == RED_NONE) {
       last->red_kind = RED_NORM;
-      return;
+      return true;
     }
     StepDesc r = blank(ST_PASS);
     r.red_kind = RED_NORM;
     emit(r);
+    return true;
   }
   void push_sig(Op& o, const std::vector<int>& sig) {
     o.cond = sig.empty() ? 0 : 1;
@@ -932,7 +937,7 @@ struct Packer {
         at[pos[g]] = g;
         continue;
       }
-      if (cur.first_uses_red) need_norm_before();
+      if (cur.first_uses_red && !need_norm_before()) cur.first_uses_red = 0;
       absorb_and_flush(cur);
       emit(cur);
     }
