@@ -83,7 +83,7 @@ struct PassCoef {
 
 // Grid-reduction scratch sizes (per shard): block partials and group partials (deterministic
 // two-level reduction of the generated pass kernels).
-constexpr int RED_MAX_BLOCKS = 1 << 18;
+constexpr int RED_MAX_BLOCKS = 1 << 20;  // one tile per CTA up to width 33 (complex64)
 constexpr int RED_GROUP = 256;
 constexpr int RED_MAX_GROUPS = RED_MAX_BLOCKS / RED_GROUP;
 
