@@ -992,29 +992,41 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) 
     return OWQS_OK;
   }
   const uint64_t n = 1ull << a->hp.outputs.size();
-  void *ta = nullptr, *tb = nullptr;
-  CU(cudaMalloc(&ta, n * 16));
-  cudaError_t e2 = cudaMalloc(&tb, n * 16);
-  if (e2 != cudaSuccess) {
-    cudaFree(ta);
-    return fail(a, OWQS_E_NOMEM, "inner product scratch");
-  }
-  owqs_status s = output_to_device_full(a, ta, 1);
-  if (s == OWQS_OK) {
-    const Program& pb = b->cm[b->out_cm].prog;
-    cudaError_t e = launch_permute_out(b->shards[0].d_state, b->prec, tb, 1, (int)pb.out_slot.size(),
-                                       pb.out_slot.data(), 0, n, a->stream);
-    if (e == cudaSuccess) e = launch_dot(dev_ptrs(a, a->cm[0], 0), ta, tb, n, a->stream);
-    double red[4] = {0, 0, 0, 0};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(red, a->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost, a->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(a->stream);
-    if (e != cudaSuccess) s = fail(a, OWQS_E_CUDA, cudaGetErrorString(e));
+  const Program& pa = a->cm[a->out_cm].prog;
+  const Program& pb = b->cm[b->out_cm].prog;
+  if (a->prec == b->prec && pa.out_slot == pb.out_slot && pa.phys_bits == pb.phys_bits &&
+      pa.phys_bits == (int)a->hp.outputs.size()) {
+    // same final layout: dot the states in place (no scratch; any size)
+    CU(launch_dot_t(dev_ptrs(a, a->cm[0], 0), a->prec, a->shards[0].d_state, b->shards[0].d_state, n, a->stream));
+    double red[4];
+    CU(cudaMemcpyAsync(red, a->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost, a->stream));
+    CU(cudaStreamSynchronize(a->stream));
     *re = red[0];
     *im = red[1];
+    return OWQS_OK;
   }
-  cudaFree(ta);
-  cudaFree(tb);
-  return s;
+  // different layouts: permute both into the caller's output order chunk by chunk through the
+  // staging buffer (two complex128 halves) and sum the chunk dots in a fixed order
+  const uint64_t chunk = kStagingBytes / 32;
+  char* ta = (char*)a->d_staging;
+  char* tb = ta + chunk * 16;
+  double sr = 0, si = 0;
+  for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
+    const uint64_t cnt = std::min(chunk, n - j0);
+    CU(launch_permute_out(a->shards[0].d_state, a->prec, ta, 1, (int)pa.out_slot.size(), pa.out_slot.data(), j0, cnt,
+                          a->stream));
+    CU(launch_permute_out(b->shards[0].d_state, b->prec, tb, 1, (int)pb.out_slot.size(), pb.out_slot.data(), j0, cnt,
+                          a->stream));
+    CU(launch_dot(dev_ptrs(a, a->cm[0], 0), ta, tb, cnt, a->stream));
+    double red[4];
+    CU(cudaMemcpyAsync(red, a->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost, a->stream));
+    CU(cudaStreamSynchronize(a->stream));
+    sr += red[0];
+    si += red[1];
+  }
+  *re = sr;
+  *im = si;
+  return OWQS_OK;
 }
 
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
