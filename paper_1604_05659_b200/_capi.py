@@ -109,7 +109,8 @@ class StepDesc(C.Structure):
                 ("n_ops", C.c_int32), ("red_kind", C.c_int32), ("red_slot", C.c_int32), ("slot", C.c_int32),
                 ("shrink_m", C.c_int32), ("n_bfly", C.c_int32), ("first_uses_red", C.c_int32),
                 ("first_full_rho", C.c_int32), ("pad", C.c_int32), ("ops", Op * MAX_OPS),
-                ("absorb", C.c_uint64 * MAX_BFLY), ("swap_local", C.c_int32), ("swap_global", C.c_int32)]
+                ("absorb", C.c_uint64 * MAX_BFLY), ("swap_local", C.c_int32), ("swap_global", C.c_int32),
+                ("n_remap", C.c_int32), ("remap_a", C.c_int32 * 6), ("remap_b", C.c_int32 * 6)]
 
 
 class MStatic(C.Structure):

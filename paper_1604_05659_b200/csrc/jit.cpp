@@ -121,11 +121,15 @@ inline TileGeom tile_geom() {
   return g;
 }
 inline int tile_bits(int prec) { return (prec == 0 ? 6 : 5) + KTILE; }
+// 16 B unit of tile index t: v = t >> 1 (complex64 pairs) or t, XOR-swizzled in its low 3 bits by
+// the higher ones: u = v ^ ((v >> 3 ^ v >> 6 ^ v >> 9) & 7). u is a bijection, linear over GF(2)
+// (per-thread base XOR per-register constant), exactly 64 KB for both precisions, and tile bit k
+// lands in bank group 2^(class mod 3) -- the same conflict-freedom rule as a padded layout
 inline int umap_p(int t, int prec) {
   const int v = prec == 0 ? t >> 1 : t;
-  return v + (v >> 3) + (v >> 6) + (v >> 9);
+  return v ^ (((v >> 3) ^ (v >> 6) ^ (v >> 9)) & 7);
 }
-constexpr int kTileSmem = 16 * (4095 + 511 + 63 + 7 + 1);  // 16 * (u(2^TB - 1) + 1), both precisions
+constexpr int kTileSmem = 16 * 4096;
 
 struct Gen {
   const StepDesc& d;
@@ -977,13 +981,50 @@ struct Gen {
     lays.push_back(L);
     return (int)lays.size() - 1;
   }
+  // global slot of each tile bit: the pass's slots, or (store side) after the pass's qubit remap
+  int slot_of_tb(int t) const { return t < SB ? t : gs[t - SB]; }
+  int smap[16];
+  bool use_smap = false;
+  int gslot(int t) const { return use_smap ? smap[t] : slot_of_tb(t); }
   // segment offset (relative to gb) of register pair p in A-type layout l (group bits only)
   uint64_t a_seg(int l, int p) const {
     uint64_t s = 0;
     const CLayout& L = lays[l];
     for (int k = 0; k < RB; ++k)
-      if (((p >> k) & 1) && L.R[k] >= SB) s |= 1ull << (gs[L.R[k] - SB] - SB);
+      if (((p >> k) & 1) && gslot(L.R[k]) >= SB) s |= 1ull << (gslot(L.R[k]) - SB);
     return s;
+  }
+  // store layout under the remap: lanes = the tile bits that land on the segment's lane slots,
+  // registers = t0 (complex64) + the last phase's other bits where possible, warps = the rest
+  CLayout make_store_layout(const CLayout& last) const {
+    CLayout L;
+    bool used[16] = {};
+    for (int j = 0; j < 5; ++j)
+      for (int t = 0; t < TB; ++t)
+        if (smap[t] == FB + j) {
+          L.Lb[j] = t;
+          used[t] = true;
+        }
+    int k = 0;
+    if (FB) {
+      L.R[k++] = 0;
+      used[0] = true;
+    }
+    for (int q = FB; q < RB && k < RB; ++q)
+      if (!used[last.R[q]]) {
+        L.R[k++] = last.R[q];
+        used[last.R[q]] = true;
+      }
+    for (int t = 0; t < TB && k < RB; ++t)
+      if (!used[t]) {
+        L.R[k++] = t;
+        used[t] = true;
+      }
+    int w = 0;
+    for (int t = 0; t < TB; ++t)
+      if (!used[t]) L.Wb[w++] = t;
+    std::sort(L.R + FB, L.R + RB);
+    return L;
   }
   void emit_tile_transition(int to, bool last) {
     o << "    // layout " << lay << " -> " << to << " (shared-memory tile)\n";
@@ -994,20 +1035,20 @@ struct Gen {
     const char* bar = local ? "    __syncwarp();\n" : "    __syncthreads();\n";
     if (prec == 0) {
       for (int p = 0; p < P; p += 2)
-        o << "    *reinterpret_cast<float4*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_float4(lo("
+        o << "    *reinterpret_cast<float4*>(dsm + (sb" << lay << " ^ " << 16 * umap(treg(A, p)) << ")) = make_float4(lo("
           << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
       o << bar;
       for (int p = 0; p < P; p += 2)
-        o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
-          << "); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
+        o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + (sb" << to << " ^ " << 16 * umap(treg(B, p))
+          << ")); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
     } else {
       for (int p = 0; p < P; ++p)
-        o << "    *reinterpret_cast<double2*>(dsm + sb" << lay << " + " << 16 * umap(treg(A, p)) << ") = make_double2("
+        o << "    *reinterpret_cast<double2*>(dsm + (sb" << lay << " ^ " << 16 * umap(treg(A, p)) << ")) = make_double2("
           << XR(p) << ", " << XI(p) << ");\n";
       o << bar;
       for (int p = 0; p < P; ++p)
-        o << "    { const double2 w = *reinterpret_cast<const double2*>(dsm + sb" << to << " + " << 16 * umap(treg(B, p))
-          << "); xr" << p << " = w.x; xi" << p << " = w.y; }\n";
+        o << "    { const double2 w = *reinterpret_cast<const double2*>(dsm + (sb" << to << " ^ " << 16 * umap(treg(B, p))
+          << ")); xr" << p << " = w.x; xi" << p << " = w.y; }\n";
     }
     for (int p = 0; p < P; ++p) perm[p] = p;
     if (!last || tile_iters > 1) o << bar;
@@ -1047,7 +1088,19 @@ struct Gen {
         if (!((warp_pref >> b) & 1) && k < NSEL) sa[k++] = b;
     }
     const int l_load = a_type(ph.front().S) ? plays.front() : add_layout(make_layout(sa));
-    const int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(sa));
+    int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(sa));
+    if (d.n_remap > 0) {  // qubit remap at the store (packer's plan_remap)
+      for (int t = 0; t < TB; ++t) smap[t] = slot_of_tb(t);
+      for (int k = 0; k < d.n_remap; ++k) {
+        const int ta = tilebit(d.remap_a[k]), tb = tilebit(d.remap_b[k]);
+        if (ta < 0 || tb < 0 || (FB && (ta == 0 || tb == 0))) {
+          error = "remap outside the tile";
+          return "";
+        }
+        std::swap(smap[ta], smap[tb]);
+      }
+      l_store = add_layout(make_store_layout(lays[plays.back()]));
+    }
     int n_trans = 0;
     {
       int cur = l_load;
@@ -1085,7 +1138,7 @@ struct Gen {
         << "  if (threadIdx.x == 0) spc.scale = sh.scale;\n  __syncthreads();\n"
         << "  const PassCoef* pc = &spc;\n";
     }
-    o << "  __shared__ double red_s[32][4];\n  __shared__ int flag_s;\n"
+    o << "  __shared__ double red_s[" << (small ? 32 : 8) << "][4];\n  __shared__ int flag_s;\n"
       << "  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;\n"
       << "  const unsigned rk = p.rank; (void)rk; (void)d;\n"
       << "  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;\n";
@@ -1094,19 +1147,22 @@ struct Gen {
     if (n_trans)
       for (size_t l = 0; l < lays.size(); ++l) {
         o << "  const int sb" << l << " = 16 * (";
-        for (int j = 0; j < 5; ++j) o << (j ? " + " : "") << "((lane >> " << j << ") & 1) * " << umap(1 << lays[l].Lb[j]);
-        for (int j = 0; j < WB; ++j) o << " + ((warp >> " << j << ") & 1) * " << umap(1 << lays[l].Wb[j]);
+        for (int j = 0; j < 5; ++j) o << (j ? " ^ " : "") << "(((lane >> " << j << ") & 1) * " << umap(1 << lays[l].Lb[j]) << ")";
+        for (int j = 0; j < WB; ++j) o << " ^ (((warp >> " << j << ") & 1) * " << umap(1 << lays[l].Wb[j]) << ")";
         o << ");\n";
       }
     auto wseg = [&](int l) {
-      std::string e = "(";
+      std::string e = "(0ull";
       for (int j = 0; j < WB; ++j)
-        e += std::string(j ? " | " : "") + "((unsigned long long)((warp >> " + std::to_string(j) + ") & 1) << " +
-             std::to_string(gs[lays[l].Wb[j] - SB] - SB) + ")";
+        if (gslot(lays[l].Wb[j]) >= SB)
+          e += " | ((unsigned long long)((warp >> " + std::to_string(j) + ") & 1) << " +
+               std::to_string(gslot(lays[l].Wb[j]) - SB) + ")";
       return e + ")";
     };
     o << "  const unsigned long long wsl = " << wseg(l_load) << ";\n";
+    use_smap = d.n_remap > 0;
     o << "  const unsigned long long wss = " << wseg(l_store) << ";\n";
+    use_smap = false;
     o << "  " << (prec == 0 ? "float4" : "double2") << "* __restrict__ st = reinterpret_cast<"
       << (prec == 0 ? "float4" : "double2") << "*>(p.state);\n"
       << "  for (unsigned it = 0; it < " << iters << "u; ++it) {\n"
@@ -1148,6 +1204,7 @@ struct Gen {
       }
     }
     if (l_store != lay) emit_tile_transition(l_store, --left == 0);
+    use_smap = d.n_remap > 0;
     if (d.n_ops > 0 && prec == 0)
       for (int q = 0; q < P; q += 2)
         o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_float4(lo(" << X(q)
@@ -1156,6 +1213,7 @@ struct Gen {
       for (int q = 0; q < P; ++q)
         o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_double2(" << XR(q)
           << ", " << XI(q) << "));\n";
+    use_smap = false;
     o << "  }\n";
     if (nred > 0)
       o << "  double acc[4] = {acc0, acc1, acc2, acc3};\n"
@@ -1221,7 +1279,8 @@ int jit_smem_carveout(int engine, int prec) {
   if (engine != 2) return -1;  // cudaSharedmemCarveoutDefault
   if (const char* e = getenv("OWQS_CARVEOUT")) return atoi(e);
   // CTAs per SM (register-limited) x (tile + static + reserved), as a percentage of 228 KB
-  const int per = kTileSmem + 2048 + 1024;
+  // (static: red_s[8][4] + flag; reserved: 1 KB per CTA) -- 3 x 64 KB tiles fit the 196 KB split
+  const int per = kTileSmem + 288 + 1024;
   const int ctas = Gen::tile_minb_for(prec);
   return std::min(100, (ctas * per * 100 + 233471) / 233472);
 }

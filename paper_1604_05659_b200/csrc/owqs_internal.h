@@ -67,6 +67,11 @@ struct StepDesc {
   // ST_SWAP (multi-rank): exchange the qubit at global position swap_global (a rank bit) with the
   // one at local position swap_local; each rank trades half of its shard with rank ^ (1 << (g - wl))
   int32_t swap_local, swap_global;
+  // ST_PASS on the tile engine: qubit remapping applied at the pass's store -- the amplitude bit at
+  // physical position remap_a[k] is written to position remap_b[k] and vice versa (a segment slot
+  // whose qubit has no further 2x2 op traded for a group slot of a still-active qubit)
+  int32_t n_remap;
+  int32_t remap_a[6], remap_b[6];
 };
 
 // Decisions of one pass, computed once by decide_kernel and read by every CTA of the generated pass

@@ -645,6 +645,47 @@ struct Packer {
     }
   }
   int wl() const { return width - n_global; }
+  // Qubit remapping (tile engine only, programs without GROW / SHRINK): the 6 segment slots are in
+  // every pass's tile for free, so they should hold qubits that still have work. At the store of a
+  // pass, a segment slot whose qubit has no remaining 2x2 op is traded for one of the pass's group
+  // slots whose qubit has (the soonest-needed first): the next passes see up to 13 active qubits.
+  bool remap = false;
+  int remap_margin = 0;  // stream-order distance a swap must gain
+  template <typename Nodes>
+  void plan_remap(StepDesc& cur, const Nodes& nodes) {
+    if (cur.n_ops == 0) return;  // a read-only pass has no store
+    std::vector<int> next_use(64, 1 << 30);
+    for (const auto& nd : nodes)
+      if (!nd.done) {
+        const LOp& l = ops[nd.op];
+        if (l.type == 3 || l.type == 4) next_use[l.a] = std::min(next_use[l.a], nd.op);
+      }
+    // coldest segment slots (latest next 2x2 op, none = never) against the hottest group slots
+    std::vector<int> seg, grp;
+    for (int p = (SB == 6 ? 1 : 0); p < SB; ++p) seg.push_back(p);  // complex64 keeps slot 0 (float4 pairs)
+    for (int j = 0; j < cur.nb_hi; ++j)
+      if (next_use[at[cur.bhi[j]]] < (1 << 30)) grp.push_back(cur.bhi[j]);
+    std::sort(seg.begin(), seg.end(), [&](int x, int y) { return next_use[at[x]] > next_use[at[y]]; });
+    std::sort(grp.begin(), grp.end(), [&](int x, int y) { return next_use[at[x]] < next_use[at[y]]; });
+    std::vector<int> dead, live;
+    for (size_t k = 0; k < seg.size() && k < grp.size(); ++k) {
+      if (next_use[at[seg[k]]] <= next_use[at[grp[k]]] + remap_margin) break;
+      dead.push_back(seg[k]);
+      live.push_back(grp[k]);
+    }
+    cur.n_remap = 0;
+    for (size_t k = 0; k < dead.size() && k < live.size() && k < 6; ++k) {
+      const int a = live[k], b = dead[k];
+      cur.remap_a[cur.n_remap] = a;
+      cur.remap_b[cur.n_remap] = b;
+      ++cur.n_remap;
+      const int va = at[a], vb = at[b];
+      std::swap(pos[va], pos[vb]);
+      at[pos[va]] = va;
+      at[pos[vb]] = vb;
+    }
+  }
+
   // group slots allowed in a pass of (shard) width w
   int wide_at(int w) const { return (kwide > KMAX_AOT && w >= SB + KTILE) ? kwide : kmax_hi; }
   // last step that computes something (a SWAP only permutes: it preserves the norm)
@@ -939,6 +980,7 @@ struct Packer {
       }
       if (cur.first_uses_red && !need_norm_before()) cur.first_uses_red = 0;
       absorb_and_flush(cur);
+      if (remap && wide) plan_remap(cur, nodes);
       emit(cur);
     }
   }
@@ -1028,6 +1070,13 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
   Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1, n_global);
   pk.kwide = std::max(KMAX_AOT, std::min(KTILE, kwide));
   if (const char* env = getenv("OWQS_MAX_BFLY")) pk.max_bfly = std::max(1, std::min(MAX_BFLY, atoi(env)));
+  {
+    bool resize = false;
+    for (const LOp& l : em.ops) resize = resize || l.type == 10 || l.type == 11;
+    const char* env = getenv("OWQS_REMAP");
+    pk.remap = env && atoi(env) != 0 && !resize && n_global == 0 && pk.kwide > KMAX_AOT;
+    if (const char* m = getenv("OWQS_REMAP_MARGIN")) pk.remap_margin = atoi(m);
+  }
   if (const char* env = getenv("OWQS_KWIDE")) pk.kwide = std::max(KMAX_AOT, std::min(KTILE, atoi(env)));
   pk.run();
   for (int o : hp.outputs) pr.out_slot.push_back(pk.pos[em.slot_of[o]]);

@@ -155,6 +155,13 @@ class Interp:
                 if d.n_ops > 0:
                     st[:n] = v
                 self._reduce(d, v, np.arange(n))
+                for k in range(getattr(d, "n_remap", 0)):  # qubit remap at the store: swap bits a, b
+                    a, b = d.remap_a[k], d.remap_b[k]
+                    j = np.arange(n)
+                    flip = ((j >> a) ^ (j >> b)) & 1
+                    dst = j ^ (flip << a) ^ (flip << b)
+                    cur = st[:n].copy()
+                    st[dst] = cur
                 if d.red_kind != RED_NONE:
                     self._allreduce()
             elif d.kind == ST_GROW:

@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(256, 1) tma_k(float4* __restrict__ a, u64 c, i
 
 // np with T CTA-wide shared-memory transposes of the tile (write 16 B / amplitude pair, barrier,
 // read back in another order, barrier), as the tile engine's phase changes do
-template <int K, int T>
-__global__ void __launch_bounds__(256, 2) npt_k(float4* __restrict__ a, u64 c) {
+template <int K, int T, int MINB = 2>
+__global__ void __launch_bounds__(256, MINB) npt_k(float4* __restrict__ a, u64 c) {
   extern __shared__ __align__(16) unsigned char sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float4* t = a + (size_t)blockIdx.x * 4096;
@@ -260,7 +260,7 @@ int main() {
   cudaFuncSetAttribute(np_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);          \
   cudaFuncSetAttribute(np_k<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 67);              \
   run("np75/c67", K, [&] { np_k<K><<<ntiles, 256, 75 * 1024>>>(a, c); });
-  NPC(28) NPC(88)
+
 #define NP64(K)                                                                                   \
   cudaFuncSetAttribute(np64_k<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 75 * 1024);        \
   cudaFuncSetAttribute(np64_k<K>, cudaFuncAttributePreferredSharedMemoryCarveout, 67);            \
@@ -269,11 +269,17 @@ int main() {
 #define TR(K, T)                                                                                   \
   cudaFuncSetAttribute(npt_k<K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4608 * 16);        \
   cudaFuncSetAttribute(npt_k<K, T>, cudaFuncAttributePreferredSharedMemoryCarveout, 67);            \
-  run("np+T" #T "/c67", K, [&] { npt_k<K, T><<<ntiles, 256, 4608 * 16>>>(a, c); });
-  TR(28, 1) TR(28, 0) TR(16, 1) TR(48, 2) TR(88, 4)
+  run("np+T" #T "/2cta", K, [&] { npt_k<K, T><<<ntiles, 256, 4608 * 16>>>(a, c); });
+#define TR3(K, T)                                                                                  \
+  cudaFuncSetAttribute(npt_k<K, T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);         \
+  cudaFuncSetAttribute(npt_k<K, T, 3>, cudaFuncAttributePreferredSharedMemoryCarveout, 86);         \
+  { int nb = 0; cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, npt_k<K, T, 3>, 256, 65536);      \
+    printf("npt<3> occupancy %d\n", nb); }                                                           \
+  run("np+T" #T "/3cta", K, [&] { npt_k<K, T, 3><<<ntiles, 256, 65536>>>(a, c); });
+  TR(28, 1) TR3(28, 1) TR(48, 4) TR3(48, 4) TR(88, 4) TR3(88, 4) TR(28, 4) TR3(28, 4)
 #define TT(K, T)                                                                                   \
   cudaFuncSetAttribute(tmat_k<K, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 65536);       \
   run("tma+T" #T, K, [&] { tmat_k<K, T><<<sms, 256, 2 * 65536>>>(a, c, ntiles); });
-  TT(16, 0) TT(16, 1) TT(28, 0) TT(28, 1) TT(28, 2) TT(48, 2) TT(88, 4)
+
   return 0;
 }
