@@ -352,8 +352,9 @@ def run_ours(args, rank, world, local_rank):
 
     # ---- roofline of the dominant kernel: per-launch CUDA events over profiled runs ----
     # A state pass moves 2S bytes (S = 2^w amplitudes x 8/16 B; S for a read-only reduction pass) and
-    # issues, per amplitude, 4 FP32-pipe lane-ops per butterfly (y = a x1: FMUL2 + FFMA2 per pair;
-    # x0 +- y: 2 FADD2 per pair), 2 for the normalisation scale, 2 (norm) or 4 (rho) for the
+    # issues, per amplitude, 3 FP32-pipe lane-ops per butterfly (w = x0 + a x1: 2 FFMA2 per pair;
+    # 2 x0 - w: 1 FFMA2), +1 for the normalisation scale folded into the first butterfly (k x0 +-
+    # (k a) x1: 4 packed ops per pair), 2 (norm) or 4 (rho) for the
     # probability reduction. Its roofline time is max(bytes / HBM peak, ops / FP32
     # peak); light passes are HBM-bound, heavy ones FP32-bound.
     peak, peak_src = peaks()
@@ -375,14 +376,14 @@ def run_ours(args, rank, world, local_rank):
     prof_step_ms = prof.stats()["last_run_ms"]
     prof.close()
     kc, by, tm = per_step[0], per_step[1], per_step[2] / runs
-    from paper_1604_05659_b200.host import compile_host
+    from paper_1604_05659_b200.host import compile_host, nvrtc_version
     hp = compile_host(pattern, "eowqs" if mode == "eowqs" else "sampled", prec, args.flags,
                       n_ranks=n_shards if (shard or loop > 1) else 1)
     ops = np.zeros(len(kc))
     for i, sd in enumerate(hp.steps[:len(kc)]):
         if sd.kind == 0:  # state pass
             amps = float(2 ** sd.width) * n_shards / (n_shards if shard else 1)
-            per_amp = 4 * sd.n_bfly + (2 if sd.n_bfly else 0) + {0: 0, 1: 2, 2: 4}[sd.red_kind]
+            per_amp = 3 * sd.n_bfly + (1 if sd.n_bfly else 0) + {0: 0, 1: 2, 2: 4}[sd.red_kind]
             ops[i] = amps * per_amp
     agg = {}
     for c in set(kc.tolist()):
@@ -480,6 +481,7 @@ def run_ours(args, rank, world, local_rank):
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "f32" if prec == 64 else "f64", "data": "synthetic",
         "config": {"workload": WORKLOADS[args.workload], "mode": mode, "amplitudes": f"complex{prec}",
+                   "nvrtc": "%d.%d" % nvrtc_version(),
                    "commands": n_cmd, "measurements": st["n_measure"], "paper_m": st["paper_m"],
                    "phys_bits": st["phys_bits"], "passes_per_run": st["n_passes"], "swaps_per_run": st["n_swaps"],
                    "launches_per_run": st["n_launches"], "state_bytes": N * (8 if prec == 64 else 16),

@@ -76,6 +76,11 @@ owqs_status owqs_host_jit_source(const owqs_host_plan* h, int64_t step, char* bu
  * shifted M); sizes[4] = {n_cmds, pool_len, shift_len, n_x_absorbed}. */
 owqs_status owqs_host_standardize(const owqs_host_plan* h, int32_t signal_shift, owqs_cmd* cmds, int32_t* pool,
                                   int32_t* shift_slices, int32_t* shift_pool, int64_t* sizes);
+/* Version of the NVRTC the pass-kernel generator compiles with (loaded by absolute path from the
+ * CUDA toolkit the library was built against, in its own symbol scope, so a different
+ * libnvrtc.so.12 already in the process -- e.g. torch's bundled copy -- is not used). Host only; no
+ * GPU needed. Returns OWQS_E_CUDA (major = minor = 0) when NVRTC cannot be loaded. */
+owqs_status owqs_host_nvrtc_version(int32_t* major, int32_t* minor);
 const char* owqs_host_error(const owqs_host_plan* h);
 void owqs_host_free(owqs_host_plan* h);
 

@@ -17,6 +17,7 @@ BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libowqs.so")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
+NVRTC_LIB = os.path.join(CUDA_HOME, "lib64", "libnvrtc.so.12")  # loaded by path at run time (jit.cpp)
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["kernels.cu"]
@@ -79,12 +80,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
         if force or _stale(o, [s, prelude] + hdrs):
             _run(["g++", "-O2", "-g", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function",
-                  "-I", INCLUDE, "-I", CSRC, "-I", BUILD, "-I", os.path.join(CUDA_HOME, "include"), "-c", s, "-o", o])
+                  "-I", INCLUDE, "-I", CSRC, "-I", BUILD, "-I", os.path.join(CUDA_HOME, "include"),
+                  f'-DOWQS_NVRTC_PATH="{NVRTC_LIB}"', "-c", s, "-o", o])
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
         _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xlinker", "--no-undefined",
               "-L/usr/lib/x86_64-linux-gnu", "-lnccl",
-              "-L" + os.path.join(CUDA_HOME, "lib64"), "-lnvrtc", "-Xlinker", "-rpath=" + os.path.join(CUDA_HOME, "lib64"), "-lpthread", "-ldl", "-lrt"])
+              "-lpthread", "-ldl", "-lrt"])
         shutil.move(tmp, LIB)
     return LIB
 

@@ -94,7 +94,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 # ---- include/owqs_host.h (host-only introspection; no CUDA calls) ------------------------------
 HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_gflow",
-                 "owqs_host_jit", "owqs_host_jit_source", "owqs_host_standardize", "owqs_host_error",
+                 "owqs_host_jit", "owqs_host_jit_source", "owqs_host_nvrtc_version", "owqs_host_standardize", "owqs_host_error",
                  "owqs_host_free"]
 KMAX_HI, MAX_OPS, MAX_BFLY = 8, 128, 64
 
@@ -139,6 +139,7 @@ def declare_host(lib: C.CDLL) -> C.CDLL:
         "owqs_host_gflow": (C.c_int, [h, P(C.c_int32), P(C.c_int32)]),
         "owqs_host_jit": (C.c_int, [h, P(C.c_int64), P(C.c_int64), P(C.c_double)]),
         "owqs_host_jit_source": (C.c_int, [h, C.c_int64, C.c_char_p, C.c_int64, P(C.c_int64)]),
+        "owqs_host_nvrtc_version": (C.c_int, [P(C.c_int32), P(C.c_int32)]),
         "owqs_host_standardize": (C.c_int, [h, C.c_int32, P(owqs_cmd), P(C.c_int32), P(C.c_int32), P(C.c_int32),
                                             P(C.c_int64)]),
         "owqs_host_error": (C.c_char_p, [h]),

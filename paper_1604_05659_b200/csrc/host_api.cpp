@@ -137,6 +137,15 @@ owqs_status owqs_host_jit(owqs_host_plan* h, int64_t* n_kernels, int64_t* n_jit_
   return OWQS_OK;
 }
 
+owqs_status owqs_host_nvrtc_version(int32_t* major, int32_t* minor) {
+  if (!major || !minor) return OWQS_E_ARG;
+  int a = 0, b = 0;
+  const std::string e = owqs::jit_nvrtc_version(&a, &b);
+  *major = a;
+  *minor = b;
+  return e.empty() ? OWQS_OK : OWQS_E_CUDA;
+}
+
 owqs_status owqs_host_jit_source(const owqs_host_plan* h, int64_t step, char* buf, int64_t cap, int64_t* len) {
   if (!h || step < -1 || step >= (int64_t)h->prog.steps.size()) return OWQS_E_ARG;
   const int prec = h->elem == 8 ? 0 : 1;

@@ -18,7 +18,10 @@
 #include "jit.h"
 
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 #include <nvrtc.h>
+
+#include <type_traits>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -298,6 +301,10 @@ struct Gen {
   }
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
+  static bool bfly4() {
+    static const bool v = getenv("OWQS_BFLY4") != nullptr;
+    return v;
+  }
   void bfly(int i, int bi) {
     const Op& op = d.ops[i];
     const int a = op.a;
@@ -349,10 +356,15 @@ struct Gen {
           o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
             << ")); const u64 t = " << X(p) << "; " << X(p) << " = fma2(bc(sck), t, " << (s ? "neg2(y)" : "y") << "); "
             << X(p1) << " = fma2(bc(sck), t, " << (s ? "y" : "neg2(y)") << "); }\n";
-        } else if (prec == 0) {
+        } else if (prec == 0 && bfly4()) {
           o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
             << ")); const u64 t = " << X(p) << "; " << X(p) << " = " << (s ? "sub2" : "add2") << "(t, y); " << X(p1)
             << " = " << (s ? "add2" : "sub2") << "(t, y); }\n";
+        } else if (prec == 0) {
+          // w = x0 + a x1 (2 FMA), the other row 2 x0 - w (1 FMA): 3 packed ops per pair instead of 4
+          const std::string w = s ? X(p1) : X(p), r = s ? X(p) : X(p1);
+          o << "      { const u64 t = " << X(p) << "; const u64 w = fma2(bc(ar" << u << "), " << X(p1) << ", fma2(B" << u
+            << ", swp(" << X(p1) << "), t)); " << r << " = fma2(bc(2.f), t, neg2(w)); " << w << " = w; }\n";
         } else if (fold) {
           const std::string u_ = std::to_string(u);
           o << "      { const double yr = ar" << u_ << " * " << XR(p1) << " - ai" << u_ << " * " << XI(p1)
@@ -361,12 +373,14 @@ struct Gen {
             << " = fma(sck, ti, " << (s ? "-" : "") << "yi); " << XR(p1) << " = fma(sck, tr, " << (s ? "" : "-")
             << "yr); " << XI(p1) << " = fma(sck, ti, " << (s ? "" : "-") << "yi); }\n";
         } else {
+          // w = x0 + a x1 (4 DFMA), the other row 2 x0 - w (2 DFMA)
           const std::string u_ = std::to_string(u);
-          o << "      { const double yr = ar" << u_ << " * " << XR(p1) << " - ai" << u_ << " * " << XI(p1)
-            << ", yi = ar" << u_ << " * " << XI(p1) << " + ai" << u_ << " * " << XR(p1) << "; const double tr = "
-            << XR(p) << ", ti = " << XI(p) << "; " << XR(p) << " = tr " << (s ? "-" : "+") << " yr; " << XI(p)
-            << " = ti " << (s ? "-" : "+") << " yi; " << XR(p1) << " = tr " << (s ? "+" : "-") << " yr; "
-            << XI(p1) << " = ti " << (s ? "+" : "-") << " yi; }\n";
+          const std::string wr = s ? XR(p1) : XR(p), wi = s ? XI(p1) : XI(p), rr = s ? XR(p) : XR(p1),
+                            ri = s ? XI(p) : XI(p1);
+          o << "      { const double tr = " << XR(p) << ", ti = " << XI(p) << "; const double wr = fma(ar" << u_ << ", "
+            << XR(p1) << ", fma(-ai" << u_ << ", " << XI(p1) << ", tr)), wi = fma(ar" << u_ << ", " << XI(p1) << ", fma(ai"
+            << u_ << ", " << XR(p1) << ", ti)); " << rr << " = fma(2.0, tr, -wr); " << ri << " = fma(2.0, ti, -wi); "
+            << wr << " = wr; " << wi << " = wi; }\n";
         }
       }
     } else if (ka == SK_LANE) {
@@ -1233,30 +1247,96 @@ struct CacheEntry {
 std::mutex g_mu;
 std::unordered_map<std::string, std::shared_ptr<JitModule>> g_cache;  // kernel name -> module
 
+// NVRTC of the toolkit the library was built with, loaded by absolute path into its own symbol scope
+// (RTLD_LOCAL | RTLD_DEEPBIND). Linking -lnvrtc would bind to whichever libnvrtc.so.12 the process
+// loaded first -- after `import torch` that is torch's bundled cu128 copy, whose back end emits
+// measurably slower sm_100a code for the same source (C3 pass kernels: 62.5 vs 50.5 ms per run).
+struct Nvrtc {
+  void* h = nullptr;
+  std::string err;
+  int major = 0, minor = 0;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*) = nullptr;
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*) = nullptr;
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*log)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*) = nullptr;
+  nvrtcResult (*cubin)(nvrtcProgram, char*) = nullptr;
+  nvrtcResult (*destroy)(nvrtcProgram*) = nullptr;
+  const char* (*errstr)(nvrtcResult) = nullptr;
+  nvrtcResult (*version)(int*, int*) = nullptr;
+};
+
+const Nvrtc& nvrtc() {
+  static const Nvrtc n = [] {
+    Nvrtc x;
+    const char* path = getenv("OWQS_NVRTC");
+#ifdef OWQS_NVRTC_PATH
+    if (!path) path = OWQS_NVRTC_PATH;
+#endif
+    if (!path) path = "libnvrtc.so.12";
+    x.h = dlopen(path, RTLD_NOW | RTLD_LOCAL | RTLD_DEEPBIND);
+    if (!x.h) {
+      const char* e = dlerror();
+      x.err = std::string("cannot load NVRTC from ") + path + ": " + (e ? e : "?");
+      return x;
+    }
+    bool ok = true;
+    auto sym = [&](auto& f, const char* name) {
+      f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(x.h, name));
+      if (!f) ok = false;
+    };
+    sym(x.create, "nvrtcCreateProgram");
+    sym(x.compile, "nvrtcCompileProgram");
+    sym(x.log_size, "nvrtcGetProgramLogSize");
+    sym(x.log, "nvrtcGetProgramLog");
+    sym(x.cubin_size, "nvrtcGetCUBINSize");
+    sym(x.cubin, "nvrtcGetCUBIN");
+    sym(x.destroy, "nvrtcDestroyProgram");
+    sym(x.errstr, "nvrtcGetErrorString");
+    sym(x.version, "nvrtcVersion");
+    if (!ok) {
+      x.err = std::string("NVRTC at ") + path + " lacks an entry point";
+      return x;
+    }
+    x.version(&x.major, &x.minor);
+    return x;
+  }();
+  return n;
+}
+
 std::string compile_tu(const std::string& src, std::vector<char>& cubin) {
+  const Nvrtc& nv = nvrtc();
+  if (!nv.err.empty()) return nv.err;
   nvrtcProgram prog;
-  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "owqs_pass_jit.cu", 0, nullptr, nullptr);
-  if (r != NVRTC_SUCCESS) return std::string("nvrtcCreateProgram: ") + nvrtcGetErrorString(r);
+  nvrtcResult r = nv.create(&prog, src.c_str(), "owqs_pass_jit.cu", 0, nullptr, nullptr);
+  if (r != NVRTC_SUCCESS) return std::string("nvrtcCreateProgram: ") + nv.errstr(r);
   const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOWQS_JIT=1"};
-  r = nvrtcCompileProgram(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  r = nv.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
   std::string err;
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;
-    nvrtcGetProgramLogSize(prog, &n);
+    nv.log_size(prog, &n);
     std::string log(n, '\0');
-    if (n) nvrtcGetProgramLog(prog, &log[0]);
-    err = std::string("nvrtcCompileProgram: ") + nvrtcGetErrorString(r) + "\n" + log;
+    if (n) nv.log(prog, &log[0]);
+    err = std::string("nvrtcCompileProgram: ") + nv.errstr(r) + "\n" + log;
   } else {
     size_t n = 0;
-    nvrtcGetCUBINSize(prog, &n);
+    nv.cubin_size(prog, &n);
     cubin.resize(n);
-    nvrtcGetCUBIN(prog, cubin.data());
+    nv.cubin(prog, cubin.data());
   }
-  nvrtcDestroyProgram(&prog);
+  nv.destroy(&prog);
   return err;
 }
 
 }  // namespace
+
+std::string jit_nvrtc_version(int* major, int* minor) {
+  const Nvrtc& nv = nvrtc();
+  *major = nv.major;
+  *minor = nv.minor;
+  return nv.err;
+}
 
 int jit_engine(const StepDesc& d, int prec) {
   if (d.kind != ST_PASS) return 0;

@@ -8,6 +8,7 @@
 // time (host only, no device needed); the cubins are loaded on the device with the runtime's
 // library API when the context first runs.
 #pragma once
+
 #include <stdint.h>
 
 #include <string>
@@ -55,5 +56,8 @@ struct JitModule {
 // cached per process (keyed by the source text). Returns "" on success, else the NVRTC log.
 std::string jit_compile(const std::vector<std::string>& names, const std::vector<std::string>& sources,
                         std::vector<JitModule>& out, double* compile_ms = nullptr);
+
+// Version of the NVRTC jit_compile uses; "" on success, else why it cannot be loaded.
+std::string jit_nvrtc_version(int* major, int* minor);
 
 }  // namespace owqs

@@ -59,6 +59,16 @@ def _host_handle(pattern, mode, precision, flags, weights, n_ranks):
     return L, h
 
 
+def nvrtc_version():
+    """(major, minor) of the NVRTC the pass-kernel generator compiles with (the build's CUDA
+    toolkit, loaded by path; include/owqs_host.h owqs_host_nvrtc_version)."""
+    a, b = C.c_int32(0), C.c_int32(0)
+    st = lib().owqs_host_nvrtc_version(C.byref(a), C.byref(b))
+    if st != 0:
+        raise OwqsError(st, "NVRTC could not be loaded")
+    return a.value, b.value
+
+
 def jit_host(pattern, mode: str = "sampled", precision: int = 64, flags: int = 0,
              weights: Optional[Sequence[float]] = None, n_ranks: int = 1, sources: bool = False) -> dict:
     """NVRTC-compile the generated pass kernels of the compiled program (no GPU needed).

@@ -55,3 +55,26 @@ def test_tile_kernel_structure_c3():
         trans = int(re.search(r"(\d+) transpose\(s\)", s).group(1))
         assert trans <= phases + 1
         assert "block_partial" in s  # fence-free block partials, summed by grid_finish_kernel
+
+
+def test_generator_uses_toolkit_nvrtc_after_torch():
+    """The generator compiles with the build toolkit's NVRTC (loaded by path, own symbol scope), not
+    a libnvrtc.so.12 loaded earlier by another library: torch's bundled cu128 copy produces slower
+    sm_100a code for the same source."""
+    import subprocess
+    import sys
+    code = ("import torch; torch.zeros(1)\n"
+            "from paper_1604_05659_b200.host import nvrtc_version, jit_host\n"
+            "from workloads import patterns as W\n"
+            "jit_host(W.config_pattern('BW:14x2', seed=1), 'sampled', 64)\n"
+            "maps = [l.split()[-1] for l in open('/proc/self/maps') if 'libnvrtc.so' in l]\n"
+            "print(nvrtc_version(), sorted(set(maps)))\n")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=600,
+                         cwd=__import__("os").path.dirname(__import__("os").path.dirname(__file__)))
+    assert out.returncode == 0, out.stderr[-2000:]
+    maps = out.stdout
+    from paper_1604_05659_b200.host import nvrtc_version
+    major, minor = nvrtc_version()
+    assert (major, minor) >= (12, 9)
+    assert f"({major}, {minor})" in out.stdout
+    assert "/usr/local/cuda" in maps or "cuda-12" in maps

@@ -20,6 +20,20 @@ __global__ void k_ffma2(u64* out, u64 c) {
   for (int i = 0; i < 16; ++i) s ^= x[i];
   if (s == 0x1234) out[0] = s;
 }
+__device__ __forceinline__ u64 add2(u64 a, u64 b) { u64 r; asm volatile("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+__device__ __forceinline__ u64 mul2(u64 a, u64 b) { u64 r; asm volatile("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b)); return r; }
+// MODE 0: FADD2 only, 1: FMUL2 only, 2: FFMA2 + FADD2 alternating (co-issue?)
+template <int MODE>
+__global__ void k_mix2(u64* out, u64 c) {
+  u64 x[16];
+  for (int i = 0; i < 16; ++i) x[i] = c + threadIdx.x + i;
+  for (int it = 0; it < ITERS; ++it)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = MODE == 0 ? add2(x[i], c) : MODE == 1 ? mul2(x[i], c) : ((i & 1) ? add2(x[i], c) : fma2(x[i], c, c));
+  u64 s = 0;
+  for (int i = 0; i < 16; ++i) s ^= x[i];
+  if (s == 0x1234) out[0] = s;
+}
 __global__ void k_ffma(float* out, float c) {
   float x[16];
   for (int i = 0; i < 16; ++i) x[i] = c + threadIdx.x + i;
@@ -79,6 +93,9 @@ int main() {
            ops / (best * 1e-3) / sms / (clk * 1e3), clk / 1000);
   };
   run("FFMA2", 2.0 * ITERS * 16, [&] { k_ffma2<<<blocks, threads>>>((u64*)buf, 0x3f8000003f800000ull); });
+  run("FADD2", 2.0 * ITERS * 16, [&] { k_mix2<0><<<blocks, threads>>>((u64*)buf, 0x3f8000003f800000ull); });
+  run("FMUL2", 2.0 * ITERS * 16, [&] { k_mix2<1><<<blocks, threads>>>((u64*)buf, 0x3f8000003f800000ull); });
+  run("MIX2", 2.0 * ITERS * 16, [&] { k_mix2<2><<<blocks, threads>>>((u64*)buf, 0x3f8000003f800000ull); });
   run("FFMA", 1.0 * ITERS * 16, [&] { k_ffma<<<blocks, threads>>>((float*)buf, 1.0001f); });
   run("DFMA", 1.0 * ITERS * 16, [&] { k_dfma<<<blocks, threads>>>((double*)buf, 1.0001); });
   run("SHFL", 1.0 * ITERS / 4 * 16, [&] { k_shfl<<<blocks, threads>>>((float*)buf, 1.0001f); });

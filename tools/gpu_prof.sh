@@ -1,2 +1,3 @@
-OWQS_TILE_MINB=3 timeout 600 ncu --section Occupancy --section SpeedOfLight --clock-control none -k regex:owqs_tma_c64 --launch-skip 3 --launch-count 1 python tools/prof_run.py --workload C3 > gpurun_out/ncu_occ3.log 2>&1; echo a=$?
-timeout 600 ncu --section Occupancy --section SpeedOfLight --clock-control none -k regex:owqs_tma_c64 --launch-skip 3 --launch-count 1 python tools/prof_run.py --workload C3 > gpurun_out/ncu_occ2.log 2>&1; echo b=$?
+for v in OWQS_X=1 OWQS_BFLY4=1; do
+env $v timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none --csv python tools/prof_run.py --workload C3 --runs 2 > gpurun_out/ncu_all_$v.csv 2>&1; echo l=$?
+done

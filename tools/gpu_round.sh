@@ -1,11 +1,8 @@
-# A/B: tile occupancy (2 vs 3 CTAs/SM), RB 5 vs 6, remapping; quick parity subset under each
-b() { timeout 240 env "$@" python bench.py --workload C3 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import sys,json; j=json.loads(sys.stdin.readlines()[-1]); print('$*', round(j['value']), j['ms_per_step'], j['roofline']['frac'])" ; }
-b OWQS_X=0
-b OWQS_TILE_MINB=3
+b() { timeout 240 env "$@" python bench.py --workload ${WL:-C3} --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import sys,json; j=json.loads(sys.stdin.read()); print('${WL:-C3} $*', round(j['value']), j['ms_per_step'], round(j['roofline']['frac'],3), j['roofline']['bound'])" ; }
+b OWQS_X=1
+b OWQS_BFLY4=1
+WL=C3W b OWQS_X=1
+WL=C2 b OWQS_X=1
 b OWQS_REMAP=1
-b OWQS_REMAP=1 OWQS_TILE_MINB=3
-b OWQS_TILE_RB=6
-b OWQS_TILE_RB=6 OWQS_REMAP=1
-b OWQS_TILE_RB=6 OWQS_TILE_MINB=2
-OWQS_TILE_MINB=3 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "not inner" > gpurun_out/pt3.log 2>&1; echo pt3=$?; tail -1 gpurun_out/pt3.log
-OWQS_TILE_RB=6 timeout 600 python -m pytest tests/test_gpu_parity.py -x -q -k "not inner" > gpurun_out/pt6.log 2>&1; echo pt6=$?; tail -1 gpurun_out/pt6.log
+b OWQS_TILE_MINB=3
+timeout 300 python bench.py --workload C3 --precision 128 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | cut -c1-200
