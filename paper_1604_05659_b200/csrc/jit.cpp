@@ -301,6 +301,11 @@ struct Gen {
   }
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
+  static int prefetch_distance() {
+    // default: one wave of 2 CTAs x 148 SMs (B200); C3 49.8 -> 49.3 ms, C3W 219 -> 213 ms
+    static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH")) : 296;
+    return v;
+  }
   static bool bfly4() {
     static const bool v = getenv("OWQS_BFLY4") != nullptr;
     return v;
@@ -1190,6 +1195,19 @@ struct Gen {
       for (int q = 0; q < P; ++q)
         o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
           << "ull) << 5) + lane)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
+    // L2 prefetch of the tile the CTA one wave later (blockIdx + D, D ~ resident CTAs) will load:
+    // lane m < 16 of each warp bulk-prefetches that warp's m-th 512 B segment there, so the next
+    // wave's load phase hits L2 instead of waiting on HBM (OWQS_PREFETCH=D; no extra DRAM bytes)
+    if (const int D = prefetch_distance(); D > 0 && iters == 1) {
+      o << "    { const unsigned long long ubp = (unsigned long long)blockIdx.x + " << D << "ull;\n"
+        << "    if (ubp < " << nbu << "ull && lane < 16) {\n";
+      emit_gb("gbp", "ubp");
+      o << "    const unsigned long long ap = 0ull";
+      for (int k = 0; k < 4; ++k)
+        o << " | ((lane & " << (1 << k) << ") ? " << a_seg(l_load, prec == 0 ? 2 << k : 1 << k) << "ull : 0ull)";
+      o << ";\n    asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], 512;\" :: \"l\"(st + ((gbp | wsl | ap) << 5)) : \"memory\");\n"
+        << "    } }\n";
+    }
     // launched right behind decide_kernel (programmatic dependent launch): the loads above overlap
     // the decisions; wait for them before the first read of PassCoef
     if (!small) o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";

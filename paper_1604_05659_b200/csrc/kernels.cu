@@ -1014,26 +1014,57 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
 }
 
 // Sum of the block partials of a tile pass (fixed order: deterministic) into red_result.
-__global__ void __launch_bounds__(1024) grid_finish_kernel(DevPtrs p, unsigned nblk, int nred) {
-  __shared__ double red[32][4];
-  double v[4] = {0, 0, 0, 0};
-  for (unsigned b = threadIdx.x; b < nblk; b += blockDim.x)
-    for (int k = 0; k < nred; ++k) v[k] += p.partials[(size_t)b * 4 + k];
+// Sum of the tile kernels' block partials into red_result, deterministic: CTA g sums the contiguous
+// range of partials [g * per, (g + 1) * per) in a fixed order into gpart[g]; the last CTA to arrive
+// (fenced counter) sums gpart[0..G) in order. G <= RED_MAX_GROUPS CTAs of 256 threads keep the
+// 2^15-partial sum of a 2^28-amplitude pass at a few microseconds (one CTA: ~24 us).
+__global__ void __launch_bounds__(256) grid_finish_kernel(DevPtrs p, unsigned nblk, int nred) {
+  __shared__ double red[8][4];
+  __shared__ int last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = 0; k < 4; ++k)
-    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULLMASK, v[k], o);
-  if (lane == 0)
-    for (int k = 0; k < 4; ++k) red[warp][k] = v[k];
-  __syncthreads();
-  if (threadIdx.x < 4) {
-    double t = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w][threadIdx.x];
-    p.red_result[threadIdx.x] = threadIdx.x < nred ? t : 0.0;
+  const unsigned per = (nblk + gridDim.x - 1) / gridDim.x;
+  const unsigned b0 = blockIdx.x * per, b1 = min(nblk, b0 + per);
+  double* gpart = p.partials + (size_t)RED_MAX_BLOCKS * 4;
+  auto block_sum = [&](double (&v)[4], double* out) {
+    for (int k = 0; k < 4; ++k)
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(FULLMASK, v[k], o);
+    if (lane == 0)
+      for (int k = 0; k < 4; ++k) red[warp][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      double t = 0;
+      for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+      out[threadIdx.x] = threadIdx.x < nred ? t : 0.0;
+    }
+  };
+  double v[4] = {0, 0, 0, 0};
+  for (unsigned b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
+    const double4 x = *reinterpret_cast<const double4*>(p.partials + (size_t)b * 4);
+    v[0] += x.x;
+    v[1] += x.y;
+    v[2] += x.z;
+    v[3] += x.w;
   }
+  block_sum(v, gpart + (size_t)blockIdx.x * 4);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&p.counter[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double w[4] = {0, 0, 0, 0};
+  for (unsigned g = threadIdx.x; g < gridDim.x; g += blockDim.x)
+    for (int k = 0; k < 4; ++k) w[k] += __ldcg(&gpart[(size_t)g * 4 + k]);
+  __syncthreads();
+  block_sum(w, p.red_result);
+  if (threadIdx.x == 0) p.counter[0] = 0;
 }
 
 cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaStream_t s) {
-  grid_finish_kernel<<<1, 1024, 0, s>>>(p, nblk, nred);
+  const unsigned g = std::max(1u, std::min((unsigned)RED_MAX_GROUPS, (nblk + 255) / 256));
+  grid_finish_kernel<<<g, 256, 0, s>>>(p, nblk, nred);
   return cudaGetLastError();
 }
 
