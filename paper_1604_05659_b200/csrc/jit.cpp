@@ -21,6 +21,7 @@
 #include <dlfcn.h>
 #include <nvrtc.h>
 
+#include <functional>
 #include <type_traits>
 #include <stdio.h>
 #include <stdlib.h>
@@ -301,6 +302,10 @@ struct Gen {
   }
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
+  static int stagger_ns() {
+    static const int v = getenv("OWQS_STAGGER") ? atoi(getenv("OWQS_STAGGER")) : 0;
+    return v;
+  }
   static int prefetch_distance() {
     // default: one wave of 2 CTAs x 148 SMs (B200); C3 49.8 -> 49.3 ms, C3W 219 -> 213 ms
     static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH")) : 296;
@@ -739,7 +744,7 @@ struct Gen {
     return e ? std::max(1, std::min(4, atoi(e))) : ((prec == 0 && tile_geom().rb == 6) ? 3 : 2);
   }
   int tile_minb() const { return tile_minb_for(prec); }
-  int n_local_ = 0, n_cta_ = 0;
+  int n_local_ = 0, n_cta_ = 0, n_group_ = 0, next_bar_ = 1;
 
   void build_dag() {
     const int n = d.n_ops;
@@ -1051,7 +1056,51 @@ struct Gen {
     const CLayout& B = lays[to];
     // warp bits unchanged: every warp exchanges only its own amplitudes (warp-local barrier)
     const bool local = !memcmp(A.Wb, B.Wb, sizeof(int) * WB);
-    const char* bar = local ? "    __syncwarp();\n" : "    __syncthreads();\n";
+    // otherwise only the warps that exchange amplitudes synchronise: the connected components of
+    // {writer warp of t (layout A), reader warp of t (layout B)} over the tile's indices t -- cosets of
+    // the warp-index bits both layouts assign to the same tile bit -- each on its own named barrier
+    std::string bar = local ? "    __syncwarp();\n" : "    __syncthreads();\n";
+    if (!local && !getenv("OWQS_NO_GROUPBAR")) {
+      const int NW = 1 << WB;
+      int comp[8];
+      for (int w = 0; w < NW; ++w) comp[w] = w;
+      std::function<int(int)> find = [&](int x) { return comp[x] == x ? x : comp[x] = find(comp[x]); };
+      for (int t = 0; t < (1 << TB); ++t) {
+        int wa = 0, wb = 0;
+        for (int j = 0; j < WB; ++j) {
+          wa |= ((t >> A.Wb[j]) & 1) << j;
+          wb |= ((t >> B.Wb[j]) & 1) << j;
+        }
+        const int ra = find(wa), rb = find(wb);
+        if (ra != rb) comp[std::max(ra, rb)] = std::min(ra, rb);
+      }
+      int size[8] = {}, id[8], nid = 0, rep_id[8];
+      for (int w = 0; w < NW; ++w) ++size[find(w)];
+      for (int w = 0; w < NW; ++w)
+        if (find(w) == w) rep_id[w] = nid++;
+      bool uniform = true;
+      for (int w = 0; w < NW; ++w) {
+        id[w] = rep_id[find(w)];
+        uniform = uniform && size[find(w)] == size[find(0)];
+      }
+      if (uniform && nid > 1) {
+        // fresh barrier ids for every grouped transpose: a warp may run ahead into the next
+        // transpose while others still wait on this one's barrier, so an id is reused only after a
+        // CTA-wide barrier (bar 0) has been passed by all warps
+        std::string pre;
+        if (next_bar_ + nid > 16) {
+          pre = "    __syncthreads();\n";
+          next_bar_ = 1;
+        }
+        uint32_t table = 0;
+        for (int w = 0; w < NW; ++w) table |= (uint32_t)(next_bar_ + id[w]) << (4 * w);
+        next_bar_ += nid;
+        bar = pre + "    asm volatile(\"bar.sync %0, %1;\" :: \"r\"((" + std::to_string(table) +
+              "u >> (4 * warp)) & 15), \"r\"(" + std::to_string(32 * size[find(0)]) + ") : \"memory\");\n";
+        ++n_group_;
+      }
+    }
+    if (bar == "    __syncthreads();\n") next_bar_ = 1;
     if (prec == 0) {
       for (int p = 0; p < P; p += 2)
         o << "    *reinterpret_cast<float4*>(dsm + (sb" << lay << " ^ " << 16 * umap(treg(A, p)) << ")) = make_float4(lo("
@@ -1070,7 +1119,10 @@ struct Gen {
           << ")); xr" << p << " = w.x; xi" << p << " = w.y; }\n";
     }
     for (int p = 0; p < P; ++p) perm[p] = p;
-    if (!last || tile_iters > 1) o << bar;
+    // no write-after-read barrier between transposes: location u(t) depends only on the tile index
+    // t, and the thread that writes it in the next transpose is the one that read it in this one.
+    // Only a next tile of the same CTA (other writers) needs one.
+    if ((last && tile_iters > 1) || (!last && getenv("OWQS_TRANS_WAR"))) o << "    __syncthreads();\n";
     ++(local ? n_local_ : n_cta_);
     lay = to;
   }
@@ -1186,6 +1238,8 @@ struct Gen {
       << (prec == 0 ? "float4" : "double2") << "*>(p.state);\n"
       << "  for (unsigned it = 0; it < " << iters << "u; ++it) {\n"
       << "    const unsigned long long ub = (unsigned long long)blockIdx.x * " << iters << "ull + it;\n";
+    if (stagger_ns() > 0)
+      o << "    if (blockIdx.x >= 148u && blockIdx.x < 296u) __nanosleep(" << stagger_ns() << ");\n";
     emit_gb("gb0", "ub");
     if (prec == 0)
       for (int q = 0; q < P; q += 2)

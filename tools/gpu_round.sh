@@ -1,3 +1,6 @@
-timeout 2400 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -1 gpurun_out/pytest_gpu.log; grep -E "^E " gpurun_out/pytest_gpu.log | head -5
-timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench_default.log | cut -c1-200
-for w in C3W C2 C4 C3E; do timeout 600 python bench.py --workload $w --steps 3 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_$w.log 2>&1; tail -1 gpurun_out/bench_$w.log | python -c "import sys,json; j=json.loads(sys.stdin.read()); print('$w', round(j['value']), j['ms_per_step'], round(j['roofline']['frac'],3), j['roofline']['bound'])"; done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py -x -q -k "not config4" > gpurun_out/pt.log 2>&1; echo pt=$?; tail -1 gpurun_out/pt.log; grep -E "^E " gpurun_out/pt.log | head -5
+b() { timeout 240 env "$@" python bench.py --workload ${WL:-C3} --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import sys,json; j=json.loads(sys.stdin.read()); print('${WL:-C3} $*', round(j['value']), j['ms_per_step'], round(j['roofline']['frac'],3), j['roofline']['bound'])" ; }
+b OWQS_X=1
+b OWQS_NO_GROUPBAR=1
+WL=C3W b OWQS_X=1
+WL=C3W b OWQS_NO_GROUPBAR=1
