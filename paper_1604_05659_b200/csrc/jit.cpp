@@ -1172,6 +1172,38 @@ struct Gen {
       }
       l_store = add_layout(make_store_layout(lays[plays.back()]));
     }
+    // warp-position alignment along the layout sequence: a warp bit the previous layout also has
+    // keeps its warp position (a relabelling of warp indices), so a transpose synchronises only the
+    // warps that exchange amplitudes -- groups of 2^(changed positions) -- and a transpose that only
+    // reorders warp bits becomes warp-local
+    if (!getenv("OWQS_NO_WALIGN")) {
+      auto align = [&](CLayout B, const CLayout& A) {
+        int nw[8];
+        bool placed[8] = {}, taken[16] = {};
+        for (int j = 0; j < WB; ++j) nw[j] = -1;
+        for (int j = 0; j < WB; ++j)
+          for (int i = 0; i < WB; ++i)
+            if (B.Wb[i] == A.Wb[j]) {
+              nw[j] = B.Wb[i];
+              placed[j] = true;
+              taken[B.Wb[i]] = true;
+            }
+        int k = 0;
+        for (int i = 0; i < WB; ++i)
+          if (!taken[B.Wb[i]]) {
+            while (placed[k]) ++k;
+            nw[k++] = B.Wb[i];
+          }
+        for (int j = 0; j < WB; ++j) B.Wb[j] = nw[j];
+        return B;
+      };
+      int prev = l_load;
+      for (int& l : plays) {
+        if (l != prev) l = add_layout(align(lays[l], lays[prev]));
+        prev = l;
+      }
+      if (l_store != prev) l_store = add_layout(align(lays[l_store], lays[prev]));
+    }
     int n_trans = 0;
     {
       int cur = l_load;
