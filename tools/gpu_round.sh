@@ -1,6 +1,7 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edge.py -x -q -k "not config4" > gpurun_out/pt.log 2>&1; echo pt=$?; tail -1 gpurun_out/pt.log; grep -E "^E " gpurun_out/pt.log | head -5
-b() { timeout 240 env "$@" python bench.py --workload ${WL:-C3} --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import sys,json; j=json.loads(sys.stdin.read()); print('${WL:-C3} $*', round(j['value']), j['ms_per_step'], round(j['roofline']['frac'],3), j['roofline']['bound'])" ; }
+b() { timeout 240 env "$@" python bench.py --workload ${WL:-C3} --steps 5 --warmup 3 --no-cpu-baseline --no-e2e 2>/dev/null | tail -1 | python -c "import sys,json; j=json.loads(sys.stdin.read()); print('${WL:-C3} $*', round(j['value']), j['ms_per_step'], j['config']['passes_per_run'])" ; }
 b OWQS_X=1
-b OWQS_NO_GROUPBAR=1
-WL=C3W b OWQS_X=1
-WL=C3W b OWQS_NO_GROUPBAR=1
+b OWQS_KWIDE=6
+b OWQS_KWIDE=5
+b OWQS_REMAP_MARGIN=0
+b OWQS_REMAP_MARGIN=2
+b OWQS_REMAP_MARGIN=4
