@@ -185,6 +185,23 @@ owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed);
 owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced,
                      uint8_t* outcomes_out, double* prob0_out);
 
+/* Asynchronous host-to-host run (serving path; the problem statement of L153 -- input state in,
+ * output state out -- as one call that returns before the work is done). Enqueues on the
+ * context's stream: the host->device copy of in_amps (2^n_in amplitudes at in_precision, caller
+ * order), owqs_run(mode, seed, forced), and the device->host copy of the output (2^n_out amplitudes
+ * at out_precision, bit k <-> outputs[k]) into out_amps; returns without waiting. Both host buffers
+ * must be page-locked (cudaHostAlloc / cudaHostRegister: OWQS_E_ARG otherwise) and stay untouched
+ * until owqs_wait. Two contexts on different streams pipeline: one run's PCIe copies overlap the
+ * other's kernels. Single rank only (OWQS_E_ARG). Any other call on the context before owqs_wait
+ * returns OWQS_E_STATE. Errors found while enqueueing are returned here; errors of the run itself
+ * (OWQS_E_BRANCH, OWQS_E_NOT_DETERMINISTIC, CUDA faults) are returned by owqs_wait. */
+owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced,
+                             const void* in_amps, int32_t in_precision, int64_t n_in, void* out_amps,
+                             int32_t out_precision, int64_t n_out);
+/* Wait for the submitted run; outcomes_out / prob0_out as for owqs_run (may be NULL). The output
+ * buffer is complete when this returns OWQS_OK. OWQS_E_STATE if nothing is pending. */
+owqs_status owqs_wait(owqs_ctx* ctx, uint8_t* outcomes_out, double* prob0_out);
+
 /* Batched replicas: run the loaded pattern on n_batch independent inputs in
  * one launch (one CTA per state, the state in shared memory; single rank, physical width <= 12).
  * inputs  : HOST [n_batch][2^n_in] complex128 interleaved (input k of state b at b*2^n_in + k)

@@ -104,6 +104,8 @@ struct owqs_ctx {
   void* h_staging = nullptr;  // pinned
   bool has_input = false, has_output = false;
   int out_cm = -1;
+  int pending = 0;  // owqs_submit_host: 1 + compiled mode of the enqueued run, until owqs_wait
+  int pending_mode = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   owqs_stats_t stats{};
   int last_cm = 0;
@@ -359,14 +361,22 @@ owqs_status do_swap(owqs_ctx* ctx, const StepDesc& d) {
   return OWQS_OK;
 }
 
-owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const uint8_t* forced) {
+// Enqueue one run on ctx->stream without synchronising the host (run parameters and forced
+// outcomes go through the page-locked staging buffer, so the copies are truly asynchronous; no
+// earlier copy from it is pending because every call ends synchronised or with owqs_wait).
+owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const uint8_t* forced) {
   CompiledMode& m = ctx->cm[cmi];
-  RunParams rp{};
-  rp.mode = mode;
-  rp.seed = seed;
-  CU(cudaMemcpyAsync(ctx->d_run, &rp, sizeof(rp), cudaMemcpyHostToDevice, ctx->stream));
-  if (mode == OWQS_FORCED && ctx->hp.n_measure > 0)
-    CU(cudaMemcpyAsync(ctx->d_forced, forced, ctx->hp.n_measure, cudaMemcpyHostToDevice, ctx->stream));
+  RunParams* rp = reinterpret_cast<RunParams*>(ctx->h_staging);
+  *rp = RunParams{};
+  rp->mode = mode;
+  rp->seed = seed;
+  CU(cudaMemcpyAsync(ctx->d_run, rp, sizeof(RunParams), cudaMemcpyHostToDevice, ctx->stream));
+  if (mode == OWQS_FORCED && ctx->hp.n_measure > 0) {
+    if ((size_t)ctx->hp.n_measure + 4096 > kStagingBytes) return fail(ctx, OWQS_E_ARG, "too many measurements");
+    uint8_t* hf = static_cast<uint8_t*>(ctx->h_staging) + 4096;
+    memcpy(hf, forced, ctx->hp.n_measure);
+    CU(cudaMemcpyAsync(ctx->d_forced, hf, ctx->hp.n_measure, cudaMemcpyHostToDevice, ctx->stream));
+  }
   for (auto& s : ctx->shards) CU(cudaMemsetAsync(s.d_err, 0, sizeof(int32_t), ctx->stream));
   const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH);
   const bool prof = (ctx->cfg.flags & OWQS_FLAG_PROFILE) != 0;
@@ -438,6 +448,13 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
     if (st != OWQS_OK) return st;
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  ctx->has_input = false;
+  ctx->out_cm = cmi;
+  return OWQS_OK;
+}
+
+// Wait for the enqueued run (and whatever follows it on the stream), then its time and error flag.
+owqs_status run_complete(owqs_ctx* ctx, int cmi) {
   CU(cudaStreamSynchronize(ctx->stream));
   float ms = 0;
   CU(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1));
@@ -449,11 +466,15 @@ owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const 
     CU(cudaMemcpy(&e, s.d_err, sizeof(e), cudaMemcpyDeviceToHost));
     herr |= e;
   }
-  ctx->has_input = false;
   ctx->has_output = true;
-  ctx->out_cm = cmi;
   if (herr) return fail(ctx, OWQS_E_BRANCH, "forced outcome on a branch with probability < 1e-12");
   return OWQS_OK;
+}
+
+owqs_status run_internal(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const uint8_t* forced) {
+  owqs_status s = run_enqueue(ctx, cmi, mode, seed, forced);
+  if (s != OWQS_OK) return s;
+  return run_complete(ctx, cmi);
 }
 
 bool is_pinned_host(const void* p) {
@@ -495,6 +516,8 @@ owqs_status output_to_device_full(owqs_ctx* ctx, void* dst, int dst_prec) {
   return OWQS_OK;
 }
 
+owqs_status output_to_host_enqueue(owqs_ctx* ctx, void* amps, int out_prec, bool pinned, bool sync);
+
 owqs_status output_to_host(owqs_ctx* ctx, void* amps, int out_prec) {
   const uint64_t n = 1ull << ctx->hp.outputs.size();
   const size_t oe = out_prec == 1 ? 16 : 8;
@@ -513,9 +536,17 @@ owqs_status output_to_host(owqs_ctx* ctx, void* amps, int out_prec) {
     cudaFree(d);
     return s;
   }
+  return output_to_host_enqueue(ctx, amps, out_prec, is_pinned_host(amps), true);
+}
+
+// Single-rank output in the caller's order into host memory: permute into the device staging buffer
+// chunk by chunk and DMA each chunk out. A page-locked destination is written directly (fully
+// asynchronous when sync = false); a pageable one goes through the pinned host staging buffer.
+owqs_status output_to_host_enqueue(owqs_ctx* ctx, void* amps, int out_prec, bool pinned, bool sync) {
+  const uint64_t n = 1ull << ctx->hp.outputs.size();
+  const size_t oe = out_prec == 1 ? 16 : 8;
   const Program& pr = ctx->cm[ctx->out_cm].prog;
   const uint64_t chunk = kStagingBytes / oe;
-  const bool pinned = is_pinned_host(amps);  // page-locked caller buffer: DMA straight into it
   char* dst = (char*)amps;
   for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
     uint64_t cnt = std::min(chunk, n - j0);
@@ -528,7 +559,7 @@ owqs_status output_to_host(owqs_ctx* ctx, void* amps, int out_prec) {
       memcpy(dst + j0 * oe, ctx->h_staging, cnt * oe);
     }
   }
-  CU(cudaStreamSynchronize(ctx->stream));
+  if (sync) CU(cudaStreamSynchronize(ctx->stream));
   return OWQS_OK;
 }
 
@@ -757,6 +788,7 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
                               int32_t n_out, const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool,
                               int64_t pool_len) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   ctx->loaded = false;
   ctx->has_input = ctx->has_output = false;
   ctx->gflow_state = 0;
@@ -791,14 +823,28 @@ owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps) {
   return owqs_set_input_host(ctx, amps, 128, n_amps);
 }
 
+owqs_status input_from_host_enqueue(owqs_ctx* ctx, const void* amps, int32_t precision);
+
 owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   const uint64_t n = 1ull << ctx->hp.inputs.size();
   if (!amps || n_amps != (int64_t)n) return fail(ctx, OWQS_E_ARG, "input must hold 2^n_in amplitudes");
   if (precision != 64 && precision != 128) return fail(ctx, OWQS_E_ARG, "precision must be 64 or 128");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
+  s = input_from_host_enqueue(ctx, amps, precision);
+  if (s != OWQS_OK) return s;
+  CU(cudaStreamSynchronize(ctx->stream));
+  ctx->has_input = true;
+  ctx->has_output = false;
+  return OWQS_OK;
+}
+
+// host input (caller order, either precision) into every local shard's state, on ctx->stream
+owqs_status input_from_host_enqueue(owqs_ctx* ctx, const void* amps, int32_t precision) {
+  const uint64_t n = 1ull << ctx->hp.inputs.size();
   const int sp = precision == 64 ? 0 : 1;
   const size_t se = precision == 64 ? 8 : 16;
   const uint64_t per = n >> ctx->n_global;  // amplitudes per shard
@@ -816,14 +862,12 @@ owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precisi
       CU(launch_convert_in(ctx->d_staging, sp, ctx->shards[r].d_state, ctx->prec, j0, cnt, ctx->stream));
     }
   }
-  CU(cudaStreamSynchronize(ctx->stream));
-  ctx->has_input = true;
-  ctx->has_output = false;
   return OWQS_OK;
 }
 
 owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   const uint64_t n = 1ull << ctx->hp.inputs.size();
   const uint64_t per = n >> ctx->n_global;
@@ -849,6 +893,7 @@ owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t p
 
 owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
@@ -866,9 +911,12 @@ owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed) {
   return OWQS_OK;
 }
 
+owqs_status finish_run(owqs_ctx* ctx, int cmi, int mode, owqs_status s, uint8_t* outcomes_out, double* prob0_out);
+
 owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, uint8_t* outcomes_out,
                      double* prob0_out) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "run before load_pattern");
   if (!ctx->has_input) return fail(ctx, OWQS_E_STATE, "run without a fresh input (set_input consumes per run)");
   if (mode != OWQS_SAMPLED && mode != OWQS_FORCED && mode != OWQS_EOWQS) return fail(ctx, OWQS_E_ARG, "bad mode");
@@ -879,6 +927,11 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   }
   const int cmi = mode == OWQS_EOWQS ? 1 : 0;
   owqs_status s = run_internal(ctx, cmi, mode, seed, forced);
+  return finish_run(ctx, cmi, mode, s, outcomes_out, prob0_out);
+}
+
+// After a completed run: outcomes / prob0 to the caller, stats, the EOWQS norm check.
+owqs_status finish_run(owqs_ctx* ctx, int cmi, int mode, owqs_status s, uint8_t* outcomes_out, double* prob0_out) {
   const int64_t K = ctx->hp.n_measure;
   if (K > 0 && (s == OWQS_OK || s == OWQS_E_BRANCH)) {
     if (outcomes_out) {
@@ -919,6 +972,52 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
   return OWQS_OK;
 }
 
+owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, const void* in_amps,
+                             int32_t in_precision, int64_t n_in, void* out_amps, int32_t out_precision,
+                             int64_t n_out) {
+  if (!ctx) return OWQS_E_ARG;
+  if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "submit before load_pattern");
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
+  if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "owqs_submit_host is single-rank");
+  if (mode != OWQS_SAMPLED && mode != OWQS_FORCED && mode != OWQS_EOWQS) return fail(ctx, OWQS_E_ARG, "bad mode");
+  if (mode == OWQS_FORCED && ctx->hp.n_measure > 0 && !forced) return fail(ctx, OWQS_E_ARG, "forced outcomes missing");
+  if ((in_precision != 64 && in_precision != 128) || (out_precision != 64 && out_precision != 128))
+    return fail(ctx, OWQS_E_ARG, "precision must be 64 or 128");
+  if (!in_amps || n_in != (int64_t)(1ull << ctx->hp.inputs.size()))
+    return fail(ctx, OWQS_E_ARG, "input must hold 2^n_in amplitudes");
+  if (!out_amps || n_out < (int64_t)(1ull << ctx->hp.outputs.size()))
+    return fail(ctx, OWQS_E_ARG, "output buffer smaller than 2^n_out");
+  if (!is_pinned_host(in_amps) || !is_pinned_host(out_amps))
+    return fail(ctx, OWQS_E_ARG, "owqs_submit_host needs page-locked host buffers (cudaHostAlloc)");
+  if (mode == OWQS_EOWQS) {
+    owqs_status g = gflow_gate(ctx);
+    if (g != OWQS_OK) return g;
+  }
+  owqs_status s = ensure_device(ctx);
+  if (s != OWQS_OK) return s;
+  s = input_from_host_enqueue(ctx, in_amps, in_precision);
+  if (s != OWQS_OK) return s;
+  ctx->has_input = true;
+  ctx->has_output = false;
+  const int cmi = mode == OWQS_EOWQS ? 1 : 0;
+  s = run_enqueue(ctx, cmi, mode, seed, forced);
+  if (s != OWQS_OK) return s;
+  s = output_to_host_enqueue(ctx, out_amps, out_precision == 64 ? 0 : 1, true, false);
+  if (s != OWQS_OK) return s;
+  ctx->pending = 1 + cmi;
+  ctx->pending_mode = mode;
+  return OWQS_OK;
+}
+
+owqs_status owqs_wait(owqs_ctx* ctx, uint8_t* outcomes_out, double* prob0_out) {
+  if (!ctx) return OWQS_E_ARG;
+  if (!ctx->pending) return fail(ctx, OWQS_E_STATE, "nothing submitted");
+  const int cmi = ctx->pending - 1;
+  ctx->pending = 0;
+  owqs_status s = run_complete(ctx, cmi);
+  return finish_run(ctx, cmi, ctx->pending_mode, s, outcomes_out, prob0_out);
+}
+
 owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const double* inputs,
                            const uint64_t* seeds, const uint8_t* forced, double* outputs, uint8_t* outcomes,
                            double* prob0) {
@@ -940,6 +1039,7 @@ owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps) {
 
 owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
   if (precision != 64 && precision != 128) return fail(ctx, OWQS_E_ARG, "precision must be 64 or 128");
   const uint64_t n = 1ull << ctx->hp.outputs.size();
@@ -950,6 +1050,7 @@ owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, i
 
 owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
   const uint64_t n = 1ull << ctx->hp.outputs.size();
   const bool root = ctx->n_ranks == 1 || ctx->loopback || ctx->rank == 0;

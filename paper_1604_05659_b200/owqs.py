@@ -146,6 +146,34 @@ class Simulator:
         self._check(st)
         return (out[:K], p0[:K]) if want else (None, None)
 
+    def submit_host(self, in_ptr: int, in_precision: int, out_ptr: int, out_precision: int,
+                    mode: str = "sampled", seed: int = 0, forced: Optional[Sequence[int]] = None):
+        """owqs_submit_host: enqueue input copy + run + output copy between PAGE-LOCKED host buffers
+        (raw addresses, e.g. torch.empty(..., pin_memory=True).data_ptr()) and return at once;
+        complete with wait(). in/out hold 2^n_in / 2^n_out amplitudes at precision 64 or 128."""
+        f = None
+        self._forced_keep = None
+        if forced is not None:
+            fa = np.ascontiguousarray(np.asarray(forced, dtype=np.uint8))
+            if fa.size != self.n_measure:
+                raise ValueError("forced must have one entry per M")
+            self._forced_keep = fa
+            f = fa.ctypes.data_as(C.POINTER(C.c_uint8))
+        self._check(self._lib.owqs_submit_host(self._h, MODES[mode], C.c_uint64(seed & (2 ** 64 - 1)), f,
+                                               C.c_void_p(in_ptr), in_precision, 2 ** self.n_in,
+                                               C.c_void_p(out_ptr), out_precision, 2 ** self.n_out))
+
+    def wait(self, want: bool = False) -> Tuple[Optional[np.ndarray], Optional[np.ndarray]]:
+        """owqs_wait: complete the submitted run; (outcomes, prob0) when want."""
+        K = self.n_measure
+        out = np.zeros(max(K, 1), dtype=np.uint8) if want else None
+        p0 = np.zeros(max(K, 1), dtype=np.float64) if want else None
+        st = self._lib.owqs_wait(self._h, out.ctypes.data_as(C.POINTER(C.c_uint8)) if want else None,
+                                 p0.ctypes.data_as(C.POINTER(C.c_double)) if want else None)
+        self._forced_keep = None
+        self._check(st)
+        return (out[:K], p0[:K]) if want else (None, None)
+
     def run_batch(self, inputs: np.ndarray, mode: str = "sampled", seeds: Optional[Sequence[int]] = None,
                   forced: Optional[np.ndarray] = None):
         """Batched replicas: inputs [B, 2^n_in] -> (outputs [B, 2^n_out], outcomes [B, K], prob0 [B, K])."""
