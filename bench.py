@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--loopback", type=int, default=1,
                     help="N = 1: shard the problem over this many virtual ranks on the one GPU")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-contexts", type=int, default=3,
+                    help="e2e serving pipeline depth: contexts (own state + stream) submitted round-robin")
     ap.add_argument("--ref-cmds", type=int, default=None,
                     help="oracle sample: first k commands at full width (default 4 for cpu_baseline, "
                          "2 per step for --impl reference so K+W steps finish in minutes)")
@@ -428,16 +430,16 @@ def run_ours(args, rank, world, local_rank):
         h_in.copy_(x.to(hdt))
         a_in = h_in.numpy()
         assert 2 ** len(pattern.outputs) == N
-        k_e2e = max(4, args.steps)
-        # serving pipeline over two contexts on two streams (owqs_submit_host / owqs_wait): every
+        k_e2e = max(2 * args.e2e_contexts, args.steps)
+        # serving pipeline over --e2e-contexts contexts on their own streams (owqs_submit_host / owqs_wait): every
         # step still does its own H2D copy, run and D2H copy, but one context's PCIe copies overlap
         # the other's kernels
-        stream2 = torch.cuda.Stream(device=dev)
-        sim2 = None if loop > 1 else Simulator(precision=prec, device=local_rank, flags=args.flags,
-                                               stream=stream2.cuda_stream)
-        ctxs = [sim] + ([sim2] if sim2 is not None else [])
-        if sim2 is not None:
-            sim2.load(pattern)
+        extra_streams = [torch.cuda.Stream(device=dev) for _ in range(max(0, args.e2e_contexts - 1))]
+        extra = [] if loop > 1 else [Simulator(precision=prec, device=local_rank, flags=args.flags,
+                                               stream=st.cuda_stream) for st in extra_streams]
+        ctxs = [sim] + extra
+        for x in extra:
+            x.load(pattern)
         h_outs = [torch.empty(N, dtype=hdt, pin_memory=True) for _ in ctxs]
         busy = [False] * len(ctxs)
 
@@ -481,8 +483,8 @@ def run_ours(args, rank, world, local_rank):
                "host_buffers": f"page-locked complex{prec}",
                "pipeline": (f"{len(ctxs)} contexts on separate streams (owqs_submit_host / owqs_wait)"
                             if loop <= 1 else "synchronous set_input / run / get_output")}
-        if sim2 is not None:
-            sim2.close()
+        for x in extra:
+            x.close()
         psi_host = a_in.astype(np.complex128)
     elif shard or big:
         e2e = {"value": None, "unit": "commands/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
