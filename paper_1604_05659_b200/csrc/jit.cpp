@@ -145,8 +145,93 @@ struct Gen {
   int TB = 13;         // tile bits
   int FB = 1;          // first register-selectable tile bit (complex64: t0 is fixed in R[0])
   int NSEL = 4;        // register tile bits a phase selects
-  int umap(int t) const { return umap_p(t, prec); }
-  int bclass(int k) const { return prec == 0 ? (k - 1) % 3 : k % 3; }
+  // per-kernel shared-memory map (choose_bank_classes): uval[k] = 16 B unit of tile bit k alone
+  bool ucustom = false;
+  int uval[16] = {}, ucls[16] = {};
+  int umap(int t) const {
+    if (!ucustom) return umap_p(t, prec);
+    int u = 0;
+    for (int k = 0; k < 16; ++k)
+      if ((t >> k) & 1) u ^= uval[k];
+    return u;
+  }
+  int bclass(int k) const { return ucustom ? ucls[k] : (prec == 0 ? (k - 1) % 3 : k % 3); }
+  // Bank classes chosen for this kernel: a 3-colouring of the tile bits (t1.. for complex64, t0..
+  // for complex128) such that every used layout's 5 lane bits hold all three classes, so its lane
+  // bits 0..2 can take one each (quarter-warp 16 B accesses conflict-free). Branch and bound over
+  // 3^12 colourings (fewest non-rainbow lane sets; the default colouring first). Then the map:
+  // u bit c (c < 3) = XOR of the v-bits of class c, u bits 3.. = the non-pivot v-bits in order --
+  // a GF(2) bijection of the 12 v-bits (v = t >> 1 complex64, t complex128) onto 64 KB.
+  void choose_bank_classes(const std::vector<int>& used) {
+    const int lo = FB, nb = TB - FB;
+    std::vector<uint32_t> edges;
+    for (int l : used) {
+      uint32_t m = 0;
+      for (int j = 0; j < 5; ++j) m |= 1u << lays[l].Lb[j];
+      if (std::find(edges.begin(), edges.end(), m) == edges.end()) edges.push_back(m);
+    }
+    int cls[16], best[16], best_bad = 1 << 30;
+    for (int k = 0; k < 16; ++k) cls[k] = best[k] = -1;
+    auto bad_edges = [&](int upto) {  // edges fully coloured among bits < upto that miss a class
+      int bad = 0;
+      for (uint32_t m : edges) {
+        if (m >> upto) continue;
+        int seen = 0;
+        for (int k = lo; k < upto; ++k)
+          if ((m >> k) & 1) seen |= 1 << cls[k];
+        bad += seen != 7;
+      }
+      return bad;
+    };
+    long long budget = 2000000;
+    std::function<void(int)> dfs = [&](int k) {
+      if (--budget < 0) return;
+      const int bad = bad_edges(k);
+      if (bad >= best_bad) return;
+      if (k == TB) {
+        best_bad = bad;
+        std::copy(cls, cls + 16, best);
+        return;
+      }
+      const int def = (k - lo) % 3;  // default colouring tried first
+      for (int c0 = 0; c0 < 3 && best_bad > 0; ++c0) {
+        cls[k] = (def + c0) % 3;
+        dfs(k + 1);
+      }
+      cls[k] = -1;
+    };
+    dfs(lo);
+    if (best_bad == 1 << 30) return;
+    int pivot[3] = {-1, -1, -1};
+    for (int k = lo; k < TB; ++k)
+      if (pivot[best[k]] < 0) pivot[best[k]] = k;
+    if (pivot[0] < 0 || pivot[1] < 0 || pivot[2] < 0) return;
+    ucustom = true;
+    int hi = 3;
+    for (int k = 0; k < 16; ++k) uval[k] = 0, ucls[k] = 0;
+    for (int k = lo; k < TB; ++k) {
+      ucls[k] = best[k];
+      uval[k] = 1 << best[k];
+      if (k != pivot[best[k]]) uval[k] |= 1 << hi++;
+    }
+    (void)nb;
+    // lane order: one bit of each class on lane bits 0..2 where the set allows
+    for (int l : used) {
+      CLayout& L = lays[l];
+      int order[5], n = 0;
+      bool taken[5] = {};
+      for (int c = 0; c < 3; ++c)
+        for (int j = 0; j < 5; ++j)
+          if (!taken[j] && ucls[L.Lb[j]] == c) {
+            taken[j] = true;
+            order[n++] = L.Lb[j];
+            break;
+          }
+      for (int j = 0; j < 5; ++j)
+        if (!taken[j]) order[n++] = L.Lb[j];
+      for (int j = 0; j < 5; ++j) L.Lb[j] = order[j];
+    }
+  }
   int gs[KMAX_HI];  // group slots (engine 2: padded to KTILE)
   std::vector<CLayout> lays;  // engine 2 layouts used by this kernel
   int lay = 0;                // engine 2: current layout index
@@ -1018,17 +1103,41 @@ struct Gen {
       if (((p >> k) & 1) && gslot(L.R[k]) >= SB) s |= 1ull << (gslot(L.R[k]) - SB);
     return s;
   }
+  // global float4/double2 offset of a lane in the store layout: lane bit i -> segment slot smap[Lb[i]]
+  std::string lane_expr(const CLayout& L, bool remapped) const {
+    std::string e = "(0";
+    bool ident = true;
+    for (int i = 0; i < 5; ++i) {
+      const int j = (remapped ? smap[L.Lb[i]] : slot_of_tb(L.Lb[i])) - FB;
+      ident = ident && j == i;
+      e += " | (((lane >> " + std::to_string(i) + ") & 1) << " + std::to_string(j) + ")";
+    }
+    return ident ? "lane" : e + ")";
+  }
   // store layout under the remap: lanes = the tile bits that land on the segment's lane slots,
   // registers = t0 (complex64) + the last phase's other bits where possible, warps = the rest
   CLayout make_store_layout(const CLayout& last) const {
     CLayout L;
     bool used[16] = {};
+    // lanes = the tile bits stored to the segment's 5 lane slots, ordered so that lane bits 0..2
+    // carry one bank class each where possible (a quarter-warp's 16 B accesses conflict-free); any
+    // order covers the same 512 B, the store offset follows the permutation (store_lane_expr)
+    int seg[5];
     for (int j = 0; j < 5; ++j)
       for (int t = 0; t < TB; ++t)
-        if (smap[t] == FB + j) {
-          L.Lb[j] = t;
-          used[t] = true;
+        if (smap[t] == FB + j) seg[j] = t;
+    bool taken[5] = {};
+    int li = 0;
+    for (int c = 0; c < 3; ++c)
+      for (int j = 0; j < 5; ++j)
+        if (!taken[j] && bclass(seg[j]) == c) {
+          taken[j] = true;
+          L.Lb[li++] = seg[j];
+          break;
         }
+    for (int j = 0; j < 5; ++j)
+      if (!taken[j]) L.Lb[li++] = seg[j];
+    for (int j = 0; j < 5; ++j) used[L.Lb[j]] = true;
     int k = 0;
     if (FB) {
       L.R[k++] = 0;
@@ -1210,6 +1319,14 @@ struct Gen {
       for (int l : plays) n_trans += l != cur, cur = l;
       n_trans += l_store != cur;
     }
+    if (!getenv("OWQS_NO_BANKCLS")) {
+      std::vector<int> used{l_load};
+      for (int l : plays) used.push_back(l);
+      used.push_back(l_store);
+      std::sort(used.begin(), used.end());
+      used.erase(std::unique(used.begin(), used.end()), used.end());
+      choose_bank_classes(used);
+    }
     o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* "
       << (small ? "pc_global" : "pc") << ") {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
       << "  using namespace owqs;\n"
@@ -1265,6 +1382,8 @@ struct Gen {
     o << "  const unsigned long long wsl = " << wseg(l_load) << ";\n";
     use_smap = d.n_remap > 0;
     o << "  const unsigned long long wss = " << wseg(l_store) << ";\n";
+    o << "  const int lane_st = " << lane_expr(lays[l_store], d.n_remap > 0) << ";\n";
+    o << "  const int lane_ld = " << lane_expr(lays[l_load], false) << ";\n";
     use_smap = false;
     o << "  " << (prec == 0 ? "float4" : "double2") << "* __restrict__ st = reinterpret_cast<"
       << (prec == 0 ? "float4" : "double2") << "*>(p.state);\n"
@@ -1276,11 +1395,11 @@ struct Gen {
     if (prec == 0)
       for (int q = 0; q < P; q += 2)
         o << "    u64 x" << q << ", x" << q + 1 << "; { const float4 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
-          << "ull) << 5) + lane)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
+          << "ull) << 5) + lane_ld)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
     else
       for (int q = 0; q < P; ++q)
         o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
-          << "ull) << 5) + lane)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
+          << "ull) << 5) + lane_ld)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
     // L2 prefetch of the tile the CTA one wave later (blockIdx + D, D ~ resident CTAs) will load:
     // lane m < 16 of each warp bulk-prefetches that warp's m-th 512 B segment there, so the next
     // wave's load phase hits L2 instead of waiting on HBM (OWQS_PREFETCH=D; no extra DRAM bytes)
@@ -1325,11 +1444,11 @@ struct Gen {
     use_smap = d.n_remap > 0;
     if (d.n_ops > 0 && prec == 0)
       for (int q = 0; q < P; q += 2)
-        o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_float4(lo(" << X(q)
+        o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane_st), make_float4(lo(" << X(q)
           << "), hi(" << X(q) << "), lo(" << X(q + 1) << "), hi(" << X(q + 1) << ")));\n";
     if (d.n_ops > 0 && prec == 1)
       for (int q = 0; q < P; ++q)
-        o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane), make_double2(" << XR(q)
+        o << "    __stcs(st + (((gb0 | wss | " << a_seg(l_store, q) << "ull) << 5) + lane_st), make_double2(" << XR(q)
           << ", " << XI(q) << "));\n";
     use_smap = false;
     o << "  }\n";

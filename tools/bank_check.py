@@ -1,0 +1,43 @@
+"""Static bank-conflict check of generated tile kernels: for every layout's shared-memory base
+`sb<l> = 16 * (XOR over lane/warp bits of coefficient)`, a quarter-warp (lanes 0..7) of 16 B
+accesses is conflict-free iff the 16 B-unit coefficients of lane bits 0..2 have linearly independent
+low 3 bits (bank groups). Counts conflicted layouts (weighted by their accesses) per kernel."""
+import re
+import sys
+
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+from paper_1604_05659_b200.host import jit_host  # noqa: E402
+from workloads.patterns import config_pattern  # noqa: E402
+
+
+def rank3(vals):
+    rows = [v & 7 for v in vals]
+    r = 0
+    for bit in (4, 2, 1):
+        piv = next((i for i in range(r, len(rows)) if rows[i] & bit), None)
+        if piv is None:
+            continue
+        rows[r], rows[piv] = rows[piv], rows[r]
+        for i in range(len(rows)):
+            if i != r and rows[i] & bit:
+                rows[i] ^= rows[r]
+        r += 1
+    return r
+
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "C3"
+src = jit_host(config_pattern(wl, seed=1), "sampled", 64, sources=True)["sources"]
+tot = bad = 0
+for k, s in sorted(src.items()):
+    if k < 0:
+        continue
+    bases = {}
+    for m in re.finditer(r"const int sb(\d+) = 16 \* \((.*)\);", s):
+        coef = {int(a): int(b) for a, b in re.findall(r"\(\(lane >> (\d)\) & 1\) \* (\d+)\)", m.group(2))}
+        bases[m.group(1)] = coef
+    for m in re.finditer(r"dsm \+ \(sb(\d+) \^", s):
+        c = bases[m.group(1)]
+        tot += 1
+        if rank3([c.get(0, 0), c.get(1, 0), c.get(2, 0)]) < 3:
+            bad += 1
+print(f"{wl}: {bad} of {tot} shared-memory accesses from layouts with a conflicted quarter-warp")
