@@ -78,3 +78,17 @@ def test_generator_uses_toolkit_nvrtc_after_torch():
     assert (major, minor) >= (12, 9)
     assert f"({major}, {minor})" in out.stdout
     assert "/usr/local/cuda" in maps or "cuda-12" in maps
+
+
+@pytest.mark.parametrize("shape", ["BW:16x8", "BW:18x6"])
+def test_tile_transposes_bank_conflict_free(shape):
+    """Every shared-memory access of the generated tile kernels is quarter-warp conflict-free: the
+    per-kernel bank classes give each layout's lane bits 0..2 independent bank-group bits
+    (tools/bank_check.py)."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from bank_check import conflicted_accesses
+    src = jit_host(W.config_pattern(shape, seed=1), "sampled", 64, sources=True)["sources"]
+    bad, tot = conflicted_accesses(src)
+    assert tot > 0 and bad == 0, (bad, tot)

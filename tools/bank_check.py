@@ -25,19 +25,26 @@ def rank3(vals):
     return r
 
 
-wl = sys.argv[1] if len(sys.argv) > 1 else "C3"
-src = jit_host(config_pattern(wl, seed=1), "sampled", 64, sources=True)["sources"]
-tot = bad = 0
-for k, s in sorted(src.items()):
-    if k < 0:
-        continue
-    bases = {}
-    for m in re.finditer(r"const int sb(\d+) = 16 \* \((.*)\);", s):
-        coef = {int(a): int(b) for a, b in re.findall(r"\(\(lane >> (\d)\) & 1\) \* (\d+)\)", m.group(2))}
-        bases[m.group(1)] = coef
-    for m in re.finditer(r"dsm \+ \(sb(\d+) \^", s):
-        c = bases[m.group(1)]
-        tot += 1
-        if rank3([c.get(0, 0), c.get(1, 0), c.get(2, 0)]) < 3:
-            bad += 1
-print(f"{wl}: {bad} of {tot} shared-memory accesses from layouts with a conflicted quarter-warp")
+def conflicted_accesses(sources):
+    """(conflicted, total) shared-memory accesses over the generated kernel sources."""
+    tot = bad = 0
+    for k, s in sorted(sources.items()):
+        if k < 0:
+            continue
+        bases = {}
+        for m in re.finditer(r"const int sb(\d+) = 16 \* \((.*)\);", s):
+            coef = {int(a): int(b) for a, b in re.findall(r"\(\(lane >> (\d)\) & 1\) \* (\d+)\)", m.group(2))}
+            bases[m.group(1)] = coef
+        for m in re.finditer(r"dsm \+ \(sb(\d+) \^", s):
+            c = bases[m.group(1)]
+            tot += 1
+            if rank3([c.get(0, 0), c.get(1, 0), c.get(2, 0)]) < 3:
+                bad += 1
+    return bad, tot
+
+
+if __name__ == "__main__":
+    wl = sys.argv[1] if len(sys.argv) > 1 else "C3"
+    src = jit_host(config_pattern(wl, seed=1), "sampled", 64, sources=True)["sources"]
+    bad, tot = conflicted_accesses(src)
+    print(f"{wl}: {bad} of {tot} shared-memory accesses from layouts with a conflicted quarter-warp")
