@@ -93,6 +93,10 @@ typedef struct {
 #define OWQS_FLAG_NO_JIT      0x80u /* run every pass with the ahead-of-time (op-interpreting) pass
                                        kernel instead of the kernels generated for the pattern at
                                        owqs_load_pattern (NVRTC, sm_100a)          */
+#define OWQS_FLAG_ONE_STATE   0x100u /* keep the whole pattern in one state vector even when its
+                                        entanglement graph has several components (default: each
+                                        component is its own sub-state, PAPER §4.1; see
+                                        owqs_load_pattern)                                        */
 #define OWQS_FLAG_LOOPBACK    0x20u /* n_ranks > 1 on ONE device: the context holds every rank's
                                        shard and runs them one after the other (swaps and
                                        all-reduces by device copies); for testing the sharded path
@@ -127,7 +131,8 @@ typedef struct {
   double n_jit_steps;        /* steps of the last mode's program run by generated kernels    */
   double n_kernels;          /* kernel launches per owqs_run of the last mode (steps + the
                                 decision kernels of tile-engine passes), per shard            */
-  double reserved[1];
+  double n_substates;        /* sub-states (PAPER §4.1) the pattern runs as: 1, or the number
+                                of components of its entanglement graph (owqs_load_pattern)   */
 } owqs_stats_t;
 
 /* Create / destroy a context on cfg->device.

@@ -81,6 +81,13 @@ owqs_status owqs_host_standardize(const owqs_host_plan* h, int32_t signal_shift,
  * libnvrtc.so.12 already in the process -- e.g. torch's bundled copy -- is not used). Host only; no
  * GPU needed. Returns OWQS_E_CUDA (major = minor = 0) when NVRTC cannot be loaded. */
 owqs_status owqs_host_nvrtc_version(int32_t* major, int32_t* minor);
+/* Sub-states of the compiled pattern (PAPER §4.1; owqs_load_pattern): *n = the number of
+ * components of its entanglement graph it runs as (1 when it stays one state vector: connected,
+ * a signal crossing components, or more than 32 components). If n > 1 and the arrays are not NULL
+ * (capacity cap >= n): masks[c] = the caller-order output bits sub-state c owns, phys_bits[c] =
+ * the physical width of its compiled program (same mode, precision, flags as the plan). */
+owqs_status owqs_host_substates(const owqs_host_plan* h, int32_t* n, uint64_t* masks, int32_t* phys_bits,
+                                int32_t cap);
 const char* owqs_host_error(const owqs_host_plan* h);
 void owqs_host_free(owqs_host_plan* h);
 

@@ -15,6 +15,7 @@ MODES = {"sampled": 0, "forced": 1, "eowqs": 2}
 FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE, FLAG_LOOPBACK = 1, 2, 4, 8, 16, 32
 FLAG_NO_GFLOW = 64
 FLAG_NO_JIT = 128
+FLAG_ONE_STATE = 256  # keep a disconnected pattern in one state vector (no sub-states)
 KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
@@ -43,7 +44,7 @@ class owqs_stats_t(C.Structure):
                 ("n_shrink", C.c_int32), ("n_reduce", C.c_int32), ("n_launches", C.c_int32),
                 ("n_swaps", C.c_int32), ("bytes_per_run", C.c_double), ("last_run_ms", C.c_double),
                 ("schedule_ms", C.c_double), ("jit_ms", C.c_double), ("n_jit_steps", C.c_double),
-                ("n_kernels", C.c_double), ("reserved", C.c_double * 1)]
+                ("n_kernels", C.c_double), ("n_substates", C.c_double)]
 
 
 assert C.sizeof(owqs_cmd) == 40
@@ -97,7 +98,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
 
 # ---- include/owqs_host.h (host-only introspection; no CUDA calls) ------------------------------
 HOST_EXPORTED = ["owqs_host_compile", "owqs_host_info_get", "owqs_host_program", "owqs_host_gflow",
-                 "owqs_host_jit", "owqs_host_jit_source", "owqs_host_nvrtc_version", "owqs_host_standardize", "owqs_host_error",
+                 "owqs_host_jit", "owqs_host_jit_source", "owqs_host_nvrtc_version", "owqs_host_substates", "owqs_host_standardize", "owqs_host_error",
                  "owqs_host_free"]
 KMAX_HI, MAX_OPS, MAX_BFLY = 8, 128, 64
 
@@ -118,7 +119,8 @@ class StepDesc(C.Structure):
 
 class MStatic(C.Structure):
     _fields_ = [("alpha", C.c_double), ("ord", C.c_int32), ("s_off", C.c_int32), ("s_len", C.c_int32),
-                ("t_off", C.c_int32), ("t_len", C.c_int32), ("reuse", C.c_int32), ("structural", C.c_int32)]
+                ("t_off", C.c_int32), ("t_len", C.c_int32), ("reuse", C.c_int32), ("structural", C.c_int32),
+                ("key", C.c_int32)]
 
 
 class owqs_host_info(C.Structure):
@@ -143,6 +145,7 @@ def declare_host(lib: C.CDLL) -> C.CDLL:
         "owqs_host_jit": (C.c_int, [h, P(C.c_int64), P(C.c_int64), P(C.c_double)]),
         "owqs_host_jit_source": (C.c_int, [h, C.c_int64, C.c_char_p, C.c_int64, P(C.c_int64)]),
         "owqs_host_nvrtc_version": (C.c_int, [P(C.c_int32), P(C.c_int32)]),
+        "owqs_host_substates": (C.c_int, [h, P(C.c_int32), P(C.c_uint64), P(C.c_int32), C.c_int32]),
         "owqs_host_standardize": (C.c_int, [h, C.c_int32, P(owqs_cmd), P(C.c_int32), P(C.c_int32), P(C.c_int32),
                                             P(C.c_int64)]),
         "owqs_host_error": (C.c_char_p, [h]),

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <functional>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -24,6 +25,8 @@ cudaError_t launch_scatter_out(const void* shard, int prec, void* out, int out_p
                                uint64_t rank, int wl, cudaStream_t s);
 cudaError_t launch_convert_in(const void* src, int src_prec, void* state, int prec, uint64_t j0, uint64_t count,
                               cudaStream_t s);
+cudaError_t launch_kron_merge(void* out, int prec, const void* const* factors, const uint64_t* masks, int n,
+                              uint64_t count, cudaStream_t s);
 cudaError_t launch_basis(void* state, int prec, uint64_t n, uint64_t k, cudaStream_t s);
 cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, uint64_t j0, cudaStream_t s);
 cudaError_t launch_scale(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
@@ -105,6 +108,10 @@ struct owqs_ctx {
   bool has_input = false, has_output = false;
   int out_cm = -1;
   int pending = 0;  // owqs_submit_host: 1 + compiled mode of the enqueued run, until owqs_wait
+  // PAPER §4.1 sub-states: one child context per component of the entanglement graph (subs[0]
+  // holds the inputs when there are any); sub_mask[c] = the caller-order output bits it owns
+  std::vector<owqs_ctx*> subs;
+  std::vector<uint64_t> sub_mask;
   int pending_mode = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   owqs_stats_t stats{};
@@ -759,6 +766,8 @@ owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
 
 void owqs_destroy(owqs_ctx* ctx) {
   if (!ctx) return;
+  for (owqs_ctx* c : ctx->subs) owqs_destroy(c);  // children use the parent's stream
+  ctx->subs.clear();
   cudaSetDevice(ctx->cfg.device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   for (int i = 0; i < 2; ++i) free_mode(ctx->cm[i]);
@@ -784,6 +793,52 @@ void owqs_destroy(owqs_ctx* ctx) {
   delete ctx;
 }
 
+owqs_status substates_unsupported(owqs_ctx* ctx, const char* what) {
+  return fail(ctx, OWQS_E_STATE,
+              std::string(what) + " is not available for a pattern run as " + std::to_string(ctx->subs.size()) +
+                  " sub-states (disconnected entanglement graph); create the context with OWQS_FLAG_ONE_STATE");
+}
+
+owqs_status load_compiled(owqs_ctx* ctx);
+
+// one child context per sub-state, on the parent's stream; the gflow pre-check of EOWQS stays with
+// the parent (the whole pattern's graph), the children keep their final-norm check
+owqs_status load_substates(owqs_ctx* ctx, std::vector<HostPattern>& parts) {
+  owqs_config cc = ctx->cfg;
+  cc.flags |= OWQS_FLAG_ONE_STATE | OWQS_FLAG_NO_GFLOW;
+  cc.stream = ctx->stream;
+  owqs_stats_t agg{};
+  for (HostPattern& p : parts) {
+    owqs_ctx* ch = nullptr;
+    owqs_status s = owqs_create(&cc, &ch);
+    if (s != OWQS_OK) return fail(ctx, s, "sub-state context: " + std::string(owqs_last_error(nullptr)));
+    ctx->subs.push_back(ch);
+    ch->weights = ctx->weights;
+    ch->hp = std::move(p);
+    s = load_compiled(ch);
+    if (s != OWQS_OK) return fail(ctx, s, "sub-state: " + std::string(owqs_last_error(ch)));
+    const owqs_stats_t& cs = ch->stats;
+    agg.paper_m = std::max(agg.paper_m, cs.paper_m);
+    agg.phys_bits = std::max(agg.phys_bits, cs.phys_bits);
+    agg.n_passes += cs.n_passes;
+    agg.n_grow += cs.n_grow;
+    agg.n_shrink += cs.n_shrink;
+    agg.n_reduce += cs.n_reduce;
+    agg.n_launches += cs.n_launches;
+    agg.bytes_per_run += cs.bytes_per_run;
+    agg.schedule_ms += cs.schedule_ms;
+    agg.jit_ms += cs.jit_ms;
+    agg.n_jit_steps += cs.n_jit_steps;
+    agg.n_kernels += cs.n_kernels;
+  }
+  agg.n_commands = (int64_t)ctx->hp.cmds.size();
+  agg.n_measure = ctx->hp.n_measure;
+  agg.n_substates = (double)ctx->subs.size();
+  ctx->stats = agg;
+  ctx->loaded = true;
+  return OWQS_OK;
+}
+
 owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in, const int32_t* outputs,
                               int32_t n_out, const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool,
                               int64_t pool_len) {
@@ -792,13 +847,25 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
   ctx->loaded = false;
   ctx->has_input = ctx->has_output = false;
   ctx->gflow_state = 0;
+  for (owqs_ctx* c : ctx->subs) owqs_destroy(c);
+  ctx->subs.clear();
+  ctx->sub_mask.clear();
   std::string e = validate_pattern(inputs, n_in, outputs, n_out, cmds, n_cmds, domain_pool, pool_len, ctx->hp);
   if (!e.empty()) return fail(ctx, OWQS_E_PATTERN, e);
   if (n_in > 40 || n_out > 40) return fail(ctx, OWQS_E_ARG, "more than 40 input/output qubits");
+  std::vector<HostPattern> parts;
+  if (!(ctx->cfg.flags & OWQS_FLAG_ONE_STATE) && ctx->n_ranks == 1 && split_substates(ctx->hp, parts, ctx->sub_mask, KRON_MAX))
+    return load_substates(ctx, parts);
+  return load_compiled(ctx);
+}
+
+// compile the context's validated pattern (both modes) and fill the load-time stats
+owqs_status load_compiled(owqs_ctx* ctx) {
   owqs_status s = compile_modes(ctx);
   if (s != OWQS_OK) return s;
   const Program& pr = ctx->cm[0].prog;
   ctx->stats = owqs_stats_t{};
+  ctx->stats.n_substates = 1;
   ctx->stats.n_commands = (int64_t)ctx->hp.cmds.size();
   ctx->stats.n_measure = ctx->hp.n_measure;
   ctx->stats.paper_m = ctx->cm[0].plan.paper_m;
@@ -828,6 +895,13 @@ owqs_status input_from_host_enqueue(owqs_ctx* ctx, const void* amps, int32_t pre
 owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
+  if (!ctx->subs.empty()) {  // the caller's input is the inputs' sub-state (PAPER §4.1)
+    owqs_status st = owqs_set_input_host(ctx->subs[0], amps, precision, n_amps);
+    if (st != OWQS_OK) return fail(ctx, st, owqs_last_error(ctx->subs[0]));
+    ctx->has_input = true;
+    ctx->has_output = false;
+    return OWQS_OK;
+  }
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   const uint64_t n = 1ull << ctx->hp.inputs.size();
   if (!amps || n_amps != (int64_t)n) return fail(ctx, OWQS_E_ARG, "input must hold 2^n_in amplitudes");
@@ -868,6 +942,13 @@ owqs_status input_from_host_enqueue(owqs_ctx* ctx, const void* amps, int32_t pre
 owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
+  if (!ctx->subs.empty()) {  // the caller's input is the inputs' sub-state (PAPER §4.1)
+    owqs_status st = owqs_set_input_device(ctx->subs[0], dev_amps, precision, n_amps);
+    if (st != OWQS_OK) return fail(ctx, st, owqs_last_error(ctx->subs[0]));
+    ctx->has_input = true;
+    ctx->has_output = false;
+    return OWQS_OK;
+  }
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   const uint64_t n = 1ull << ctx->hp.inputs.size();
   const uint64_t per = n >> ctx->n_global;
@@ -894,6 +975,13 @@ owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t p
 owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed) {
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
+  if (!ctx->subs.empty()) {  // the caller's input is the inputs' sub-state (PAPER §4.1)
+    owqs_status st = owqs_set_input_random(ctx->subs[0], seed);
+    if (st != OWQS_OK) return fail(ctx, st, owqs_last_error(ctx->subs[0]));
+    ctx->has_input = true;
+    ctx->has_output = false;
+    return OWQS_OK;
+  }
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "set_input before load_pattern");
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
@@ -912,6 +1000,8 @@ owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed) {
 }
 
 owqs_status finish_run(owqs_ctx* ctx, int cmi, int mode, owqs_status s, uint8_t* outcomes_out, double* prob0_out);
+owqs_status run_substates(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, uint8_t* outcomes_out,
+                          double* prob0_out);
 
 owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, uint8_t* outcomes_out,
                      double* prob0_out) {
@@ -925,9 +1015,50 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
     owqs_status g = gflow_gate(ctx);
     if (g != OWQS_OK) return g;
   }
+  if (!ctx->subs.empty()) return run_substates(ctx, mode, seed, forced, outcomes_out, prob0_out);
   const int cmi = mode == OWQS_EOWQS ? 1 : 0;
   owqs_status s = run_internal(ctx, cmi, mode, seed, forced);
   return finish_run(ctx, cmi, mode, s, outcomes_out, prob0_out);
+}
+
+// every sub-state in turn (independent: no signal crosses them); the others start from the
+// 0-qubit state 1. Outcomes and prob0 gathered at the caller's ordinals.
+owqs_status run_substates(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, uint8_t* outcomes_out,
+                          double* prob0_out) {
+  const int64_t K = ctx->hp.n_measure;
+  std::vector<uint8_t> oc(std::max<int64_t>(K, 1)), ao(std::max<int64_t>(K, 1));
+  std::vector<double> p0(std::max<int64_t>(K, 1)), ap(std::max<int64_t>(K, 1));
+  double ms = 0;
+  ctx->has_input = false;
+  owqs_status worst = OWQS_OK;
+  std::vector<uint8_t> fc;
+  for (size_t c = 0; c < ctx->subs.size(); ++c) {
+    owqs_ctx* ch = ctx->subs[c];
+    const std::vector<int>& key = ch->hp.draw_key;  // sub-state ordinal -> the caller's
+    if (forced) {
+      fc.assign(std::max<size_t>(key.size(), 1), 0);
+      for (size_t k = 0; k < key.size(); ++k) fc[k] = forced[key[k]];
+    }
+    if (c > 0) {
+      const double one[2] = {1.0, 0.0};
+      owqs_status st = owqs_set_input_host(ch, one, 128, 1);
+      if (st != OWQS_OK) return fail(ctx, st, owqs_last_error(ch));
+    }
+    owqs_status st = owqs_run(ch, mode, seed, forced ? fc.data() : nullptr, oc.data(), p0.data());
+    if (st != OWQS_OK && st != OWQS_E_BRANCH) return fail(ctx, st, owqs_last_error(ch));
+    if (st == OWQS_E_BRANCH) worst = st;
+    for (size_t k = 0; k < key.size(); ++k) {
+      ao[key[k]] = oc[k];
+      ap[key[k]] = p0[k];
+    }
+    ms += ch->stats.last_run_ms;
+  }
+  if (K > 0 && outcomes_out) memcpy(outcomes_out, ao.data(), K);
+  if (K > 0 && prob0_out) memcpy(prob0_out, ap.data(), K * sizeof(double));
+  ctx->stats.last_run_ms = ms;
+  if (worst != OWQS_OK) return fail(ctx, worst, "forced outcome on a branch with probability < 1e-12");
+  ctx->has_output = true;
+  return OWQS_OK;
 }
 
 // After a completed run: outcomes / prob0 to the caller, stats, the EOWQS norm check.
@@ -976,6 +1107,7 @@ owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const
                              int32_t in_precision, int64_t n_in, void* out_amps, int32_t out_precision,
                              int64_t n_out) {
   if (!ctx) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_submit_host");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "submit before load_pattern");
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "owqs_submit_host is single-rank");
@@ -1022,6 +1154,7 @@ owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const
                            const uint64_t* seeds, const uint8_t* forced, double* outputs, uint8_t* outcomes,
                            double* prob0) {
   if (!ctx) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_run_batch");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "run_batch before load_pattern");
   if (n_batch <= 0 || !inputs || !outputs) return fail(ctx, OWQS_E_ARG, "empty batch or NULL buffers");
   if (mode != OWQS_SAMPLED && mode != OWQS_FORCED && mode != OWQS_EOWQS) return fail(ctx, OWQS_E_ARG, "bad mode");
@@ -1037,6 +1170,45 @@ owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps) {
   return owqs_get_output_host(ctx, amps, 128, n_amps);
 }
 
+// Output of a pattern run as sub-states: each sub-state's output (its outputs in caller order) into
+// a device factor, then one kron_merge launch scatters their tensor product into the caller's
+// output order (bit k <-> outputs[k]); into dst on the device, or through a device buffer to host.
+owqs_status output_merged(owqs_ctx* ctx, void* dst, int out_prec, bool dst_device) {
+  const size_t oe = out_prec == 1 ? 16 : 8;
+  const int nc = (int)ctx->subs.size();
+  std::vector<void*> f(nc, nullptr);
+  void* tmp = nullptr;
+  auto cleanup = [&]() {
+    for (void* x : f) cudaFree(x);
+    cudaFree(tmp);
+  };
+  for (int c = 0; c < nc; ++c) {
+    const uint64_t nf = 1ull << ctx->subs[c]->hp.outputs.size();
+    if (cudaMalloc(&f[c], nf * oe) != cudaSuccess) {
+      cleanup();
+      return fail(ctx, OWQS_E_NOMEM, "sub-state output factor");
+    }
+    owqs_status st = owqs_get_output_device(ctx->subs[c], f[c], out_prec == 1 ? 128 : 64, (int64_t)nf);
+    if (st != OWQS_OK) {
+      cleanup();
+      return fail(ctx, st, owqs_last_error(ctx->subs[c]));
+    }
+  }
+  const uint64_t n = 1ull << ctx->hp.outputs.size();
+  void* d = dst;
+  if (!dst_device && cudaMalloc(&tmp, n * oe) != cudaSuccess) {
+    cleanup();
+    return fail(ctx, OWQS_E_NOMEM, "merged output buffer");
+  }
+  if (!dst_device) d = tmp;
+  cudaError_t e = launch_kron_merge(d, out_prec, f.data(), ctx->sub_mask.data(), nc, n, ctx->stream);
+  if (e == cudaSuccess && !dst_device) e = cudaMemcpyAsync(dst, d, n * oe, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  cleanup();
+  if (e != cudaSuccess) return fail(ctx, OWQS_E_CUDA, cudaGetErrorString(e));
+  return OWQS_OK;
+}
+
 owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, int64_t n_amps) {
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
@@ -1045,6 +1217,7 @@ owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, i
   const uint64_t n = 1ull << ctx->hp.outputs.size();
   const bool root = ctx->n_ranks == 1 || ctx->loopback || ctx->rank == 0;
   if (root && (!amps || n_amps < (int64_t)n)) return fail(ctx, OWQS_E_ARG, "output buffer smaller than 2^n_out");
+  if (!ctx->subs.empty()) return output_merged(ctx, amps, precision == 64 ? 0 : 1, false);
   return output_to_host(ctx, amps, precision == 64 ? 0 : 1);
 }
 
@@ -1056,6 +1229,7 @@ owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precis
   const bool root = ctx->n_ranks == 1 || ctx->loopback || ctx->rank == 0;
   if ((root && (!dev_amps || n_amps < (int64_t)n)) || (precision != 64 && precision != 128))
     return fail(ctx, OWQS_E_ARG, "bad output buffer");
+  if (!ctx->subs.empty()) return output_merged(ctx, dev_amps, precision == 64 ? 0 : 1, true);
   owqs_status s = output_to_device_full(ctx, dev_amps, precision == 64 ? 0 : 1);
   if (s != OWQS_OK) return s;
   CU(cudaStreamSynchronize(ctx->stream));
@@ -1064,6 +1238,7 @@ owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precis
 
 owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2) {
   if (!ctx || !norm2) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_output_norm");
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
   return norm_all(ctx, norm2);
 }
@@ -1071,6 +1246,7 @@ owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2) {
 owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) {
   owqs_ctx* ctx = a;
   if (!a || !b || !re || !im) return OWQS_E_ARG;
+  if (!a->subs.empty() || !b->subs.empty()) return substates_unsupported(a, "owqs_output_inner");
   if (!a->has_output || !b->has_output) return fail(a, OWQS_E_STATE, "no output: run first");
   if (a->hp.outputs.size() != b->hp.outputs.size()) return fail(a, OWQS_E_ARG, "output widths differ");
   if (a->n_ranks > 1 || b->n_ranks > 1) {
@@ -1132,6 +1308,7 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) 
 
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
   if (!ctx) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_recognize");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "recognize before load_pattern");
   if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "recognize runs on a single rank");
   const int ni = (int)ctx->hp.inputs.size(), no = (int)ctx->hp.outputs.size();
@@ -1184,6 +1361,7 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
 // order up to the factor 1/sqrt(d). One run at width + |I| instead of 2^|I| runs.
 owqs_status owqs_recognize_choi(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
   if (!ctx) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_recognize_choi");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "recognize before load_pattern");
   if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "recognize runs on a single rank");
   const HostPattern& hp = ctx->hp;
@@ -1285,6 +1463,12 @@ owqs_status owqs_pattern_info(owqs_ctx* ctx, int64_t* n_measure, int32_t* paper_
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "no pattern loaded");
   if (n_measure) *n_measure = ctx->hp.n_measure;
+  if (!ctx->subs.empty()) {  // largest sub-state (PAPER §4.1: memory O(2^m), m = largest), passes summed
+    if (paper_m) *paper_m = ctx->stats.paper_m;
+    if (phys_bits) *phys_bits = ctx->stats.phys_bits;
+    if (n_passes) *n_passes = ctx->stats.n_passes;
+    return OWQS_OK;
+  }
   if (paper_m) *paper_m = ctx->cm[0].plan.paper_m;
   if (phys_bits) *phys_bits = ctx->cm[0].prog.phys_bits;
   if (n_passes) *n_passes = ctx->cm[0].prog.n_passes;
@@ -1293,6 +1477,7 @@ owqs_status owqs_pattern_info(owqs_ctx* ctx, int64_t* n_measure, int32_t* paper_
 
 owqs_status owqs_plan_order(owqs_ctx* ctx, owqs_mode mode, int32_t* qubits, int32_t* ms, int64_t n) {
   if (!ctx || !qubits) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_plan_order");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "no pattern loaded");
   if (n < ctx->hp.n_measure) return fail(ctx, OWQS_E_ARG, "array smaller than n_measure");
   const CompiledMode& m = ctx->cm[mode == OWQS_EOWQS ? 1 : 0];
@@ -1311,7 +1496,15 @@ owqs_status owqs_set_proa_weights(owqs_ctx* ctx, double a, double b, double g, d
   ctx->weights.g = g;
   ctx->weights.d = d;
   ctx->weights.tune = tune != 0;
-  if (ctx->loaded) {
+  if (ctx->loaded && !ctx->subs.empty()) {  // recompile every sub-state
+    for (owqs_ctx* c : ctx->subs) {
+      c->weights = ctx->weights;
+      owqs_status s = load_compiled(c);
+      if (s != OWQS_OK) return fail(ctx, s, owqs_last_error(c));
+      c->has_input = c->has_output = false;
+    }
+    ctx->has_input = ctx->has_output = false;
+  } else if (ctx->loaded) {
     owqs_status s = compile_modes(ctx);
     if (s != OWQS_OK) return s;
     ctx->has_input = ctx->has_output = false;
@@ -1321,6 +1514,7 @@ owqs_status owqs_set_proa_weights(owqs_ctx* ctx, double a, double b, double g, d
 
 owqs_status owqs_launch_profile(owqs_ctx* ctx, int32_t* kclass, double* bytes, float* ms, int64_t n) {
   if (!ctx) return OWQS_E_ARG;
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_launch_profile");
   if (!(ctx->cfg.flags & OWQS_FLAG_PROFILE) || ctx->prof_cm < 0 || !ctx->has_output)
     return fail(ctx, OWQS_E_STATE, "no profiled run (create the context with OWQS_FLAG_PROFILE)");
   const Program& pr = ctx->cm[ctx->prof_cm].prog;

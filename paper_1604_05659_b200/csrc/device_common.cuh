@@ -78,7 +78,7 @@ __device__ void decide(const DevPtrs& p, int m, bool use_red, bool full, bool re
       P1 = 0.5 * nrm;
     }
     if (mode == 0) {
-      outc = draw_uniform(p.run->seed, ms.ord) <= P0 ? 0 : 1;
+      outc = draw_uniform(p.run->seed, ms.key) <= P0 ? 0 : 1;
     } else {
       outc = p.forced[ms.ord] & 1;
     }
@@ -179,7 +179,7 @@ __device__ void pass_prologue(const StepDesc& d, const DevPtrs& p, PassShared& s
         const double nrm = (b == 0 && d.first_uses_red) ? p.red_result[0] : 1.0;
         P0[h] = 0.5 * nrm;
         const double P1 = 0.5 * nrm;
-        outc[h] = mode == 0 ? (draw_uniform(p.run->seed, ms[h].ord) <= P0[h] ? 0 : 1) : (p.forced[ms[h].ord] & 1);
+        outc[h] = mode == 0 ? (draw_uniform(p.run->seed, ms[h].key) <= P0[h] ? 0 : 1) : (p.forced[ms[h].ord] & 1);
         pS[h] = outc[h] ? P1 : P0[h];
         if (pS[h] < 1e-12) {
           if (record) atomicExch(p.err, 1);

@@ -16,6 +16,9 @@ struct owqs_host_plan {
   Plan plan;
   Program prog;
   int elem = 16;
+  int mode = 0, precision = 128;
+  uint32_t flags = 0;
+  ProaWeights w;
 };
 
 extern "C" {
@@ -49,9 +52,40 @@ owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t
                    (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w, h->plan, h->prog, n_global,
                    jit_max_group(precision == 64 ? 0 : 1, (flags & OWQS_FLAG_NO_JIT) != 0));
   h->elem = precision == 64 ? 8 : 16;
+  h->mode = mode;
+  h->precision = precision;
+  h->flags = flags;
+  h->w = w;
   if (!h->prog.error.empty()) {
     h->err = h->prog.error;
     return OWQS_E_ARG;
+  }
+  return OWQS_OK;
+}
+
+owqs_status owqs_host_substates(const owqs_host_plan* h, int32_t* n, uint64_t* masks, int32_t* phys_bits,
+                                int32_t cap) {
+  if (!h || !n) return OWQS_E_ARG;
+  std::vector<HostPattern> parts;
+  std::vector<uint64_t> mk;
+  if (!split_substates(h->hp, parts, mk, KRON_MAX)) {
+    *n = 1;
+    return OWQS_OK;
+  }
+  *n = (int32_t)parts.size();
+  if (!masks && !phys_bits) return OWQS_OK;
+  if (cap < *n) return OWQS_E_ARG;
+  for (size_t c = 0; c < parts.size(); ++c) {
+    if (masks) masks[c] = mk[c];
+    if (phys_bits) {
+      Plan pl;
+      Program pr;
+      plan_and_compile(parts[c], h->mode, h->precision == 64 ? 6 : 5, !(h->flags & OWQS_FLAG_NO_FUSE),
+                       (h->flags & OWQS_FLAG_GIVEN_ORDER) != 0, h->w, pl, pr, 0,
+                       jit_max_group(h->precision == 64 ? 0 : 1, (h->flags & OWQS_FLAG_NO_JIT) != 0));
+      if (!pr.error.empty()) return OWQS_E_ARG;
+      phys_bits[c] = pr.phys_bits;
+    }
   }
   return OWQS_OK;
 }

@@ -1229,6 +1229,54 @@ cudaError_t launch_permute_out(const void* state, int prec, void* out, int out_p
   return cudaGetLastError();
 }
 
+// Tensor merge of sub-states (PAPER §4.1: "two different sub-states are combined only
+// when ..."; the reported output is their tensor product): out[i] = prod_c f_c[pext(i, mask_c)],
+// where factor c holds the amplitudes of the output bits set in mask_c (bit k of its index <-> the
+// k-th set bit of mask_c, increasing). Factors are complex at the output precision. HBM-bound
+// (one write per amplitude; the factors are read through L2).
+struct KronArgs {
+  const void* f[KRON_MAX];
+  uint64_t mask[KRON_MAX];
+  int n;
+};
+
+template <typename T>
+__global__ void kron_merge_kernel(void* out, KronArgs a, uint64_t count) {
+  typedef typename VT<T>::C C;
+  C* o = reinterpret_cast<C*>(out);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (uint64_t)gridDim.x * blockDim.x) {
+    T re = 1, im = 0;
+    for (int c = 0; c < a.n; ++c) {
+      uint64_t m = a.mask[c], j = 0;
+      for (int k = 0; m; ++k) {
+        const int b = __ffsll((long long)m) - 1;
+        j |= ((i >> b) & 1ull) << k;
+        m &= m - 1;
+      }
+      const C v = reinterpret_cast<const C*>(a.f[c])[j];
+      const T r = re * v.x - im * v.y;
+      im = re * v.y + im * v.x;
+      re = r;
+    }
+    o[i] = make_c<T>(re, im);
+  }
+}
+
+cudaError_t launch_kron_merge(void* out, int prec, const void* const* factors, const uint64_t* masks, int n,
+                              uint64_t count, cudaStream_t s) {
+  if (n > KRON_MAX) return cudaErrorInvalidValue;
+  KronArgs a{};
+  for (int c = 0; c < n; ++c) {
+    a.f[c] = factors[c];
+    a.mask[c] = masks[c];
+  }
+  a.n = n;
+  const unsigned b = elem_blocks(count);
+  if (prec == 0) kron_merge_kernel<float><<<b, 256, 0, s>>>(out, a, count);
+  else kron_merge_kernel<double><<<b, 256, 0, s>>>(out, a, count);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_convert_in(const void* src, int src_prec, void* state, int prec, uint64_t j0, uint64_t count, cudaStream_t s) {
   unsigned b = elem_blocks(count);
   if (src_prec == 0 && prec == 0) convert_in_kernel<float, float><<<b, 256, 0, s>>>(src, state, j0, count);

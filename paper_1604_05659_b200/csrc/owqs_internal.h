@@ -89,6 +89,7 @@ struct PassCoef {
 // Grid-reduction scratch sizes (per shard): block partials and group partials (deterministic
 // two-level reduction of the generated pass kernels).
 constexpr int RED_MAX_BLOCKS = 1 << 20;  // one tile per CTA up to width 33 (complex64)
+constexpr int KRON_MAX = 32;  // sub-states merged by one kron_merge launch
 constexpr int RED_GROUP = 256;
 constexpr int RED_MAX_GROUPS = RED_MAX_BLOCKS / RED_GROUP;
 
@@ -99,6 +100,8 @@ struct MStatic {
   int32_t s_off, s_len, t_off, t_len;  // domains as given-order ordinals in sig_pool
   int32_t reuse;      // 1: slot-reuse butterfly (fresh |+> neighbour folded), 0: elimination
   int32_t structural; // 1: prob0 = ||psi||^2 / 2 exactly (a fresh |+> neighbour dephases it)
+  int32_t key;        // keyed sampling draw index (reading R-5): the caller's given-order ordinal
+                      // (differs from ord only in a sub-state of a split pattern, PAPER §4.1)
 };
 
 // Run parameters in device memory (written by the host before each run).

@@ -3,6 +3,7 @@
 #include "scheduler.h"
 
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <sstream>
@@ -495,6 +496,7 @@ struct Emitter {
     MStatic ms{};
     ms.alpha = h.angle;
     ms.ord = hp.m_ord_of_qubit[v];
+    ms.key = hp.draw_key.empty() ? ms.ord : hp.draw_key[ms.ord];
     std::vector<int> s = eowqs ? std::vector<int>() : sig_of(h.sdom);
     std::vector<int> t = eowqs ? std::vector<int>() : sig_of(h.tdom);
     ms.s_off = (int)pool.size();
@@ -1107,6 +1109,78 @@ void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool g
     plan = std::move(filt);
     prog = std::move(ap);
   }
+}
+
+// PAPER §4.1 (L155): "Initially, all of the qubit states are separate (except the input qubits
+// which can be entangled) ... Two different sub-states are combined only when the entanglement
+// operation is applied". The sub-states that are never combined are the connected components of
+// the pattern's E graph, with all inputs in one. Each component becomes its own pattern over the
+// same dense qubit ids and the same given-order M ordinals (so keyed outcome draws, forced strings
+// and the outcome / prob0 arrays keep the caller's indexing); it is split only when no signal
+// domain crosses components (execution order between sub-states is then free) and there are at
+// most KRON_MAX components. Returns false when the pattern stays one state.
+bool split_substates(const HostPattern& hp, std::vector<HostPattern>& parts, std::vector<uint64_t>& masks,
+                     int max_parts) {
+  const int nq = hp.nq;
+  std::vector<int> par(nq);
+  for (int q = 0; q < nq; ++q) par[q] = q;
+  std::function<int(int)> find = [&](int x) { return par[x] == x ? x : par[x] = find(par[x]); };
+  auto unite = [&](int a, int b) { par[find(a)] = find(b); };
+  for (size_t i = 1; i < hp.inputs.size(); ++i) unite(hp.inputs[0], hp.inputs[i]);
+  for (const HCmd& c : hp.cmds)
+    if (c.kind == H_E) unite(c.q0, c.q1);
+  for (const HCmd& c : hp.cmds) {
+    for (int q : c.sdom)
+      if (find(q) != find(c.q0)) return false;
+    for (int q : c.tdom)
+      if (find(q) != find(c.q0)) return false;
+  }
+  std::vector<int> roots;
+  auto add = [&](int q) {
+    const int r = find(q);
+    if (std::find(roots.begin(), roots.end(), r) == roots.end()) roots.push_back(r);
+  };
+  if (!hp.inputs.empty()) add(hp.inputs[0]);
+  for (const HCmd& c : hp.cmds) add(c.q0);
+  for (int q : hp.outputs) add(q);
+  if (roots.size() < 2 || roots.size() > (size_t)max_parts || hp.outputs.size() > 63) return false;
+  parts.clear();
+  masks.clear();
+  for (int r : roots) {
+    HostPattern p;
+    p.nq = nq;
+    p.ext_id = hp.ext_id;
+    p.n_measure = 0;  // dense ordinals per sub-state; draw_key keeps the caller's for sampling
+    p.m_ord_of_qubit.assign(nq, -1);
+    p.is_output.assign(nq, 0);
+    p.is_input.assign(nq, 0);
+    if (!hp.inputs.empty() && find(hp.inputs[0]) == r)
+      for (int q : hp.inputs) {
+        p.inputs.push_back(q);
+        p.is_input[q] = 1;
+      }
+    uint64_t mask = 0;
+    for (size_t k = 0; k < hp.outputs.size(); ++k)
+      if (find(hp.outputs[k]) == r) {
+        p.outputs.push_back(hp.outputs[k]);
+        p.is_output[hp.outputs[k]] = 1;
+        mask |= 1ull << k;
+      }
+    for (size_t i = 0; i < hp.cmds.size(); ++i)
+      if (find(hp.cmds[i].q0) == r) {
+        p.cmds.push_back(hp.cmds[i]);
+        int o = -1;
+        if (hp.m_ord_of_cmd[i] >= 0) {
+          o = p.n_measure++;
+          p.m_ord_of_qubit[hp.cmds[i].q0] = o;
+          p.draw_key.push_back(hp.m_ord_of_cmd[i]);
+        }
+        p.m_ord_of_cmd.push_back(o);
+      }
+    parts.push_back(std::move(p));
+    masks.push_back(mask);
+  }
+  return true;
 }
 
 }  // namespace owqs

@@ -28,12 +28,19 @@ struct HostPattern {
   std::vector<int> m_ord_of_cmd;        // given-order M ordinal of each cmd (-1 if not M)
   std::vector<int> m_ord_of_qubit;      // given-order M ordinal measuring each qubit (-1)
   std::vector<char> is_output, is_input;
+  std::vector<int> draw_key;            // keyed-draw index per M ordinal (empty: the ordinal itself)
 };
 
 // Validate rules D0-D3 and normalise. Returns "" on success, else a message.
 std::string validate_pattern(const int32_t* inputs, int n_in, const int32_t* outputs, int n_out,
                              const void* cmds /* owqs_cmd[] */, int64_t n_cmds,
                              const int32_t* pool, int64_t pool_len, HostPattern& out);
+
+// PAPER §4.1 sub-states: the components of the E graph (all inputs in one), each as its own
+// pattern over the same qubit ids and given-order M ordinals; masks[c] = its caller-order output
+// bits. False (one state) when a signal domain crosses components or there are < 2 or > max_parts.
+bool split_substates(const HostPattern& hp, std::vector<HostPattern>& parts, std::vector<uint64_t>& masks,
+                     int max_parts);
 
 struct ProaWeights {
   double a = -1, b = -1, g = 0.5, d = -1;  // alpha, beta, gamma, delta of Eq. 18 (-1: |O|)

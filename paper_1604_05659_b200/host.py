@@ -59,6 +59,26 @@ def _host_handle(pattern, mode, precision, flags, weights, n_ranks):
     return L, h
 
 
+def substates(pattern, mode: str = "sampled", precision: int = 64, flags: int = 0):
+    """Sub-states the pattern runs as (PAPER §4.1; owqs_host_substates): a list of
+    (output_mask, phys_bits) per component, or [] when it stays one state vector."""
+    L, h = _host_handle(pattern, mode, precision, flags, None, 1)
+    try:
+        n = C.c_int32(0)
+        if L.owqs_host_substates(h, C.byref(n), None, None, 0) != 0:
+            raise OwqsError(1, "owqs_host_substates")
+        if n.value <= 1:
+            return []
+        masks = (C.c_uint64 * n.value)()
+        bits = (C.c_int32 * n.value)()
+        st = L.owqs_host_substates(h, C.byref(n), masks, bits, n.value)
+        if st != 0:
+            raise OwqsError(st, "owqs_host_substates")
+        return [(int(masks[c]), int(bits[c])) for c in range(n.value)]
+    finally:
+        L.owqs_host_free(h)
+
+
 def nvrtc_version():
     """(major, minor) of the NVRTC the pass-kernel generator compiles with (the build's CUDA
     toolkit, loaded by path; include/owqs_host.h owqs_host_nvrtc_version)."""

@@ -69,7 +69,7 @@ class Interp:
             else:
                 nrm = self.red[0] if use_red else 1.0
                 P0 = P1 = 0.5 * nrm
-            outc = (0 if _draw(self.seed, ms.ord) <= P0 else 1) if self.mode == 0 else int(self.forced[ms.ord]) & 1
+            outc = (0 if _draw(self.seed, ms.key) <= P0 else 1) if self.mode == 0 else int(self.forced[ms.ord]) & 1
             pS = P1 if outc else P0
             if pS < 1e-12:
                 self.err = 1

@@ -175,3 +175,27 @@ def test_random_patterns_cover_grow_and_shrink():
         grow += info["n_grow"]
         shrink += info["n_shrink"]
     assert grow > 0 and shrink > 0
+
+
+def test_substate_split_host():
+    """PAPER §4.1 sub-states (owqs_host_substates): a pattern whose E graph has separate components
+    runs as one state per component (inputs together), each compiled at its own width; the output
+    masks partition the caller's output bits; a signal that crosses components keeps one state."""
+    import sys
+    import os
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_gpu_substates import disconnected, fragment
+    from paper_1604_05659_b200.host import substates
+    p = disconnected()
+    parts = substates(p)
+    assert len(parts) == 3
+    masks = [m for m, _ in parts]
+    assert sum(masks) == (1 << len(p.outputs)) - 1 and all(a & b == 0 for a in masks for b in masks if a is not b)
+    # the inputs' circuit (4 wires) is sub-state 0; the cluster (3 rows) and the lone |+> follow
+    assert masks[0] == 0b10100101 and masks[2] == 0b00001000
+    assert [b for _, b in parts] == [4, 3, 1] or max(b for _, b in parts) <= 4
+    assert max(b for _, b in parts) < compile_host(p, "sampled", 64).info["phys_bits"]
+    ci, co, cc = fragment(W.config_pattern("BW:3x2", seed=2), 0, True)
+    cross = W.Pattern(ci, co + [501], cc + [W.N(500), W.N(501), W.E(500, 501), W.M(500, 0.4, sdom=(ci[0],))])
+    assert substates(cross) == []
+    assert substates(W.config_pattern("C1", seed=1)) == []
