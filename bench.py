@@ -508,7 +508,7 @@ def run_ours(args, rank, world, local_rank):
     else:
         par = "single" if world == 1 else f"replicas{world}"
     line = {
-        "metric": "pattern commands/s (state-update HBM GB/s in hbm_gbs / roofline)",
+        "metric": "pattern commands/s",
         "value": value, "unit": "commands/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong" if shard else "weak",
         "vs_baseline": None, "dtype": "f32" if prec == 64 else "f64", "data": "synthetic",
