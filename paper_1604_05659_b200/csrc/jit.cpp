@@ -915,7 +915,8 @@ struct Gen {
   // first depth where a state has run every op; ties go to fewer transposes (non-A first/last
   // phases cost one each). first_group_only: the first phase must be loadable (A-type).
   std::vector<Phase> plan_greedy(bool first_group_only) const {
-    const int kBeam = 8, kExpand = 6;
+    static const int kBeam = getenv("OWQS_BEAM") ? atoi(getenv("OWQS_BEAM")) : 8;
+    static const int kExpand = getenv("OWQS_EXPAND") ? atoi(getenv("OWQS_EXPAND")) : 6;
     struct St {
       Bits done;
       std::vector<Phase> ph;
@@ -925,7 +926,8 @@ struct Gen {
     for (unsigned m = 0; m < (1u << (TB - FB)); ++m) {
       if (__builtin_popcount(m) != NSEL) continue;
       const unsigned regs = (FB ? 1u : 0u) | (m << FB);
-      if (regs & warp_pref) continue;  // keep the pass's warp bits out of registers
+      static const bool wregs = getenv("OWQS_WARP_IN_REGS") != nullptr;
+      if (!wregs && (regs & warp_pref)) continue;  // keep the pass's warp bits out of registers
       std::array<int, 5> S{};
       int n = 0;
       for (int b = FB; b < TB; ++b)
