@@ -387,17 +387,9 @@ struct Gen {
   }
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
-  static int stagger_ns() {
-    static const int v = getenv("OWQS_STAGGER") ? atoi(getenv("OWQS_STAGGER")) : 0;
-    return v;
-  }
   static int prefetch_distance() {
     // default: one wave of 2 CTAs x 148 SMs (B200); C3 49.8 -> 49.3 ms, C3W 219 -> 213 ms
     static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH")) : 296;
-    return v;
-  }
-  static bool bfly4() {
-    static const bool v = getenv("OWQS_BFLY4") != nullptr;
     return v;
   }
   void bfly(int i, int bi) {
@@ -451,10 +443,6 @@ struct Gen {
           o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
             << ")); const u64 t = " << X(p) << "; " << X(p) << " = fma2(bc(sck), t, " << (s ? "neg2(y)" : "y") << "); "
             << X(p1) << " = fma2(bc(sck), t, " << (s ? "y" : "neg2(y)") << "); }\n";
-        } else if (prec == 0 && bfly4()) {
-          o << "      { const u64 y = fma2(B" << u << ", swp(" << X(p1) << "), mul2(bc(ar" << u << "), " << X(p1)
-            << ")); const u64 t = " << X(p) << "; " << X(p) << " = " << (s ? "sub2" : "add2") << "(t, y); " << X(p1)
-            << " = " << (s ? "add2" : "sub2") << "(t, y); }\n";
         } else if (prec == 0) {
           // w = x0 + a x1 (2 FMA), the other row 2 x0 - w (1 FMA): 3 packed ops per pair instead of 4
           const std::string w = s ? X(p1) : X(p), r = s ? X(p) : X(p1);
@@ -1391,8 +1379,6 @@ struct Gen {
       << (prec == 0 ? "float4" : "double2") << "*>(p.state);\n"
       << "  for (unsigned it = 0; it < " << iters << "u; ++it) {\n"
       << "    const unsigned long long ub = (unsigned long long)blockIdx.x * " << iters << "ull + it;\n";
-    if (stagger_ns() > 0)
-      o << "    if (blockIdx.x >= 148u && blockIdx.x < 296u) __nanosleep(" << stagger_ns() << ");\n";
     emit_gb("gb0", "ub");
     if (prec == 0)
       for (int q = 0; q < P; q += 2)
