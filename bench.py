@@ -34,6 +34,8 @@ WORKLOADS = {
     "C3W": "config 3 at width 30: brickwork 30 wires x 40 layers, sampled OWQS",
     "C2": "config 2: QFT-20 (H = J(0), CP = 8 J + 2 CZ), sampled OWQS",
     "C3E": "config 3 in EOWQS mode (positive branch, no probabilities)",
+    "C5E32": "config 5's per-rank shard on one GPU: 32 x 8 flow cluster (2^32 complex64 = 32 GiB, the width "
+             "each of 8 ranks holds for config 5), EOWQS",
 }
 
 
@@ -67,6 +69,8 @@ def pattern_for(workload):
         return W.config_pattern("C3", seed=1), ("eowqs" if workload == "C3E" else "sampled")
     if workload == "C5E":
         return W.config_pattern("C5", seed=1), "eowqs"
+    if workload == "C5E32":
+        return W.config_pattern("CL:32x8", seed=1), "eowqs"
     return W.config_pattern(workload, seed=1), "sampled"
 
 
