@@ -144,10 +144,14 @@ struct Gen {
   int RB = 5, WB = 3;  // tile engine geometry
   int TB = 13;         // tile bits
   int FB = 1;          // first register-selectable tile bit (complex64: t0 is fixed in R[0])
+  int LS = 1;          // first segment lane slot of global IO layouts (complex64: t1, t0 pairs float4)
+  bool t0free = false; // complex64, OWQS_T0_FREE: phases may leave t0 out of the registers
   int NSEL = 4;        // register tile bits a phase selects
   // per-kernel shared-memory map (choose_bank_classes): uval[k] = 16 B unit of tile bit k alone
   bool ucustom = false;
   int uval[16] = {}, ucls[16] = {};
+  // byte offset of tile index t in the shared-memory tile: 16 B unit, plus 8 B for t0 (complex64)
+  int addrb(int t) const { return 16 * umap(t) ^ ((prec == 0 && (t & 1)) ? 8 : 0); }
   int umap(int t) const {
     if (!ucustom) return umap_p(t, prec);
     int u = 0;
@@ -163,11 +167,12 @@ struct Gen {
   // u bit c (c < 3) = XOR of the v-bits of class c, u bits 3.. = the non-pivot v-bits in order --
   // a GF(2) bijection of the 12 v-bits (v = t >> 1 complex64, t complex128) onto 64 KB.
   void choose_bank_classes(const std::vector<int>& used) {
-    const int lo = FB, nb = TB - FB;
+    const int lo = LS, nb = TB - LS;  // complex64: t0 is the 8 B half of a unit, not a bank bit
     std::vector<uint32_t> edges;
     for (int l : used) {
       uint32_t m = 0;
       for (int j = 0; j < 5; ++j) m |= 1u << lays[l].Lb[j];
+      if (prec == 0) m &= ~1u;
       if (std::find(edges.begin(), edges.end(), m) == edges.end()) edges.push_back(m);
     }
     int cls[16], best[16], best_bad = 1 << 30;
@@ -215,17 +220,31 @@ struct Gen {
       if (k != pivot[best[k]]) uval[k] |= 1 << hi++;
     }
     (void)nb;
-    // lane order: one bit of each class on lane bits 0..2 where the set allows
+    // lane order: one bit of each class on lane bits 0..2 where the set allows; t0 (complex64, not
+    // a register bit: 8 B accesses, half-warp wavefronts) on lane bit 3
     for (int l : used) {
       CLayout& L = lays[l];
       int order[5], n = 0;
       bool taken[5] = {};
       for (int c = 0; c < 3; ++c)
         for (int j = 0; j < 5; ++j)
-          if (!taken[j] && ucls[L.Lb[j]] == c) {
+          if (!taken[j] && L.Lb[j] >= lo && ucls[L.Lb[j]] == c) {
             taken[j] = true;
             order[n++] = L.Lb[j];
             break;
+          }
+      if (prec == 0)
+        for (int j = 0; j < 5; ++j)
+          if (!taken[j] && L.Lb[j] == 0) {
+            while (n < 3) {  // fewer than 3 classes: fill before t0 (conflicts, still correct)
+              int k = 0;
+              while (k < 5 && (taken[k] || L.Lb[k] == 0)) ++k;
+              if (k == 5) break;
+              taken[k] = true;
+              order[n++] = L.Lb[k];
+            }
+            taken[j] = true;
+            order[n++] = 0;
           }
       for (int j = 0; j < 5; ++j)
         if (!taken[j]) order[n++] = L.Lb[j];
@@ -262,12 +281,15 @@ struct Gen {
       if (prec == 0) {
         RB = tile_geom().rb;
         WB = tile_geom().wb;
-        FB = 1;
-        NSEL = RB - 1;
+        t0free = getenv("OWQS_T0_FREE") != nullptr;
+        FB = t0free ? 0 : 1;
+        LS = 1;
+        NSEL = t0free ? RB : RB - 1;
       } else {
         RB = 4;
         WB = 3;
         FB = 0;
+        LS = 0;
         NSEL = 4;
       }
       P = 1 << RB;
@@ -994,6 +1016,14 @@ struct Gen {
       if (use[cand[k]] > 0) warp_pref &= ~(1u << cand[k]);
   }
   bool a_type(const int* S) const {
+    if (t0free) {  // t0 + 4 group bits (global IO pairs t0 neighbours in float4)
+      bool has0 = false;
+      for (int k = 0; k < NSEL; ++k) {
+        if (S[k] == 0) has0 = true;
+        else if (S[k] < SB) return false;
+      }
+      return has0;
+    }
     for (int k = 0; k < NSEL; ++k)
       if (S[k] < SB) return false;
     return true;
@@ -1025,7 +1055,7 @@ struct Gen {
       if (!taken) L.Wb[w++] = b;
     }
     if (w < WB)  // S holds group bits and the preferred set overlaps: any remaining bits
-      for (int b = TB - 1; b >= 0 && w < WB; --b) {
+      for (int b = TB - 1; b >= (prec == 0 ? 1 : 0) && w < WB; --b) {
         bool taken = in_s(b);
         for (int j = 0; j < w; ++j) taken = taken || L.Wb[j] == b;
         if (!taken) L.Wb[w++] = b;
@@ -1037,13 +1067,13 @@ struct Gen {
       return false;
     };
     bool seg_lanes = a_type(S);
-    for (int j = 0; j < 5; ++j) seg_lanes = seg_lanes && !in_w(FB + j);
+    for (int j = 0; j < 5; ++j) seg_lanes = seg_lanes && !in_w(LS + j);
     if (seg_lanes) {  // A-type: lanes = the segment's lane slots (global IO layout)
-      for (int j = 0; j < 5; ++j) L.Lb[j] = FB + j;
+      for (int j = 0; j < 5; ++j) L.Lb[j] = LS + j;
       return L;
     }
     std::vector<int> rest;
-    for (int b = 0; b < TB; ++b)
+    for (int b = (t0free ? 1 : 0); b < TB; ++b)  // t0 (when not a register bit) goes to lane bit 3
       if (!in_s(b) && !in_w(b)) rest.push_back(b);
     // lane bits 0..2: one tile bit of each bank class, lowest first
     std::vector<char> used(rest.size(), 0);
@@ -1064,6 +1094,7 @@ struct Gen {
       L.Lb[c] = rest[pick];
     }
     int j = 3;
+    if (t0free && !in_s(0)) L.Lb[j++] = 0;
     for (size_t i = 0; i < rest.size(); ++i)
       if (!used[i] && j < 5) L.Lb[j++] = rest[i];
     return L;
@@ -1098,7 +1129,7 @@ struct Gen {
     std::string e = "(0";
     bool ident = true;
     for (int i = 0; i < 5; ++i) {
-      const int j = (remapped ? smap[L.Lb[i]] : slot_of_tb(L.Lb[i])) - FB;
+      const int j = (remapped ? smap[L.Lb[i]] : slot_of_tb(L.Lb[i])) - LS;
       ident = ident && j == i;
       e += " | (((lane >> " + std::to_string(i) + ") & 1) << " + std::to_string(j) + ")";
     }
@@ -1115,7 +1146,7 @@ struct Gen {
     int seg[5];
     for (int j = 0; j < 5; ++j)
       for (int t = 0; t < TB; ++t)
-        if (smap[t] == FB + j) seg[j] = t;
+        if (smap[t] == LS + j) seg[j] = t;
     bool taken[5] = {};
     int li = 0;
     for (int c = 0; c < 3; ++c)
@@ -1129,11 +1160,12 @@ struct Gen {
       if (!taken[j]) L.Lb[li++] = seg[j];
     for (int j = 0; j < 5; ++j) used[L.Lb[j]] = true;
     int k = 0;
-    if (FB) {
+    const int fb = prec == 0 ? 1 : 0;  // global stores pair t0 neighbours (float4)
+    if (fb) {
       L.R[k++] = 0;
       used[0] = true;
     }
-    for (int q = FB; q < RB && k < RB; ++q)
+    for (int q = 0; q < RB && k < RB; ++q)
       if (!used[last.R[q]]) {
         L.R[k++] = last.R[q];
         used[last.R[q]] = true;
@@ -1146,7 +1178,7 @@ struct Gen {
     int w = 0;
     for (int t = 0; t < TB; ++t)
       if (!used[t]) L.Wb[w++] = t;
-    std::sort(L.R + FB, L.R + RB);
+    std::sort(L.R + fb, L.R + RB);
     return L;
   }
   void emit_tile_transition(int to, bool last) {
@@ -1201,20 +1233,31 @@ struct Gen {
     }
     if (bar == "    __syncthreads();\n") next_bar_ = 1;
     if (prec == 0) {
-      for (int p = 0; p < P; p += 2)
-        o << "    *reinterpret_cast<float4*>(dsm + (sb" << lay << " ^ " << 16 * umap(treg(A, p)) << ")) = make_float4(lo("
-          << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
+      // t0 in register position 0: 16 B accesses of t0 neighbours; else 8 B per amplitude
+      if (A.R[0] == 0)
+        for (int p = 0; p < P; p += 2)
+          o << "    *reinterpret_cast<float4*>(dsm + (sb" << lay << " ^ " << addrb(treg(A, p)) << ")) = make_float4(lo("
+            << X(p) << "), hi(" << X(p) << "), lo(" << X(p + 1) << "), hi(" << X(p + 1) << "));\n";
+      else
+        for (int p = 0; p < P; ++p)
+          o << "    *reinterpret_cast<float2*>(dsm + (sb" << lay << " ^ " << addrb(treg(A, p)) << ")) = make_float2(lo("
+            << X(p) << "), hi(" << X(p) << "));\n";
       o << bar;
-      for (int p = 0; p < P; p += 2)
-        o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + (sb" << to << " ^ " << 16 * umap(treg(B, p))
-          << ")); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
+      if (B.R[0] == 0)
+        for (int p = 0; p < P; p += 2)
+          o << "    { const float4 w = *reinterpret_cast<const float4*>(dsm + (sb" << to << " ^ " << addrb(treg(B, p))
+            << ")); x" << p << " = pk(w.x, w.y); x" << p + 1 << " = pk(w.z, w.w); }\n";
+      else
+        for (int p = 0; p < P; ++p)
+          o << "    { const float2 w = *reinterpret_cast<const float2*>(dsm + (sb" << to << " ^ " << addrb(treg(B, p))
+            << ")); x" << p << " = pk(w.x, w.y); }\n";
     } else {
       for (int p = 0; p < P; ++p)
-        o << "    *reinterpret_cast<double2*>(dsm + (sb" << lay << " ^ " << 16 * umap(treg(A, p)) << ")) = make_double2("
+        o << "    *reinterpret_cast<double2*>(dsm + (sb" << lay << " ^ " << addrb(treg(A, p)) << ")) = make_double2("
           << XR(p) << ", " << XI(p) << ");\n";
       o << bar;
       for (int p = 0; p < P; ++p)
-        o << "    { const double2 w = *reinterpret_cast<const double2*>(dsm + (sb" << to << " ^ " << 16 * umap(treg(B, p))
+        o << "    { const double2 w = *reinterpret_cast<const double2*>(dsm + (sb" << to << " ^ " << addrb(treg(B, p))
           << ")); xr" << p << " = w.x; xi" << p << " = w.y; }\n";
     }
     for (int p = 0; p < P; ++p) perm[p] = p;
@@ -1257,13 +1300,17 @@ struct Gen {
       for (int b = SB; b < TB; ++b)
         if (!((warp_pref >> b) & 1) && k < NSEL) sa[k++] = b;
     }
+    if (t0free) {  // t0 + 4 group bits
+      for (int k = 4; k > 0; --k) sa[k] = sa[k - 1];
+      sa[0] = 0;
+    }
     const int l_load = a_type(ph.front().S) ? plays.front() : add_layout(make_layout(sa));
     int l_store = a_type(ph.back().S) ? plays.back() : add_layout(make_layout(sa));
     if (d.n_remap > 0) {  // qubit remap at the store (packer's plan_remap)
       for (int t = 0; t < TB; ++t) smap[t] = slot_of_tb(t);
       for (int k = 0; k < d.n_remap; ++k) {
         const int ta = tilebit(d.remap_a[k]), tb = tilebit(d.remap_b[k]);
-        if (ta < 0 || tb < 0 || (FB && (ta == 0 || tb == 0))) {
+        if (ta < 0 || tb < 0 || (prec == 0 && (ta == 0 || tb == 0))) {
           error = "remap outside the tile";
           return "";
         }
@@ -1356,9 +1403,9 @@ struct Gen {
     scale_pending = nbf > 0;
     if (n_trans)
       for (size_t l = 0; l < lays.size(); ++l) {
-        o << "  const int sb" << l << " = 16 * (";
-        for (int j = 0; j < 5; ++j) o << (j ? " ^ " : "") << "(((lane >> " << j << ") & 1) * " << umap(1 << lays[l].Lb[j]) << ")";
-        for (int j = 0; j < WB; ++j) o << " ^ (((warp >> " << j << ") & 1) * " << umap(1 << lays[l].Wb[j]) << ")";
+        o << "  const int sb" << l << " = (";  // byte offset
+        for (int j = 0; j < 5; ++j) o << (j ? " ^ " : "") << "(((lane >> " << j << ") & 1) * " << addrb(1 << lays[l].Lb[j]) << ")";
+        for (int j = 0; j < WB; ++j) o << " ^ (((warp >> " << j << ") & 1) * " << addrb(1 << lays[l].Wb[j]) << ")";
         o << ");\n";
       }
     auto wseg = [&](int l) {

@@ -92,3 +92,28 @@ def test_tile_transposes_bank_conflict_free(shape):
     src = jit_host(W.config_pattern(shape, seed=1), "sampled", 64, sources=True)["sources"]
     bad, tot = conflicted_accesses(src)
     assert tot > 0 and bad == 0, (bad, tot)
+
+
+def test_t0_free_option_conflict_free_and_fewer_transposes(monkeypatch):
+    """OWQS_T0_FREE (complex64 phases may leave t0 out of the registers; off by default, not faster
+    on B200 -- profiles/r01c/README.md): still bank-conflict free, fewer transposes."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(__file__)), "tools"))
+    from bank_check import conflicted_accesses
+
+    def count(src):
+        n = 0
+        for k, s in src.items():
+            m = re.search(r"(\d+) transpose\(s\)", s)
+            n += int(m.group(1)) if m else 0
+        return n
+
+    p = W.config_pattern("BW:18x8", seed=2)
+    base = jit_host(p, "sampled", 64, sources=True)["sources"]
+    monkeypatch.setenv("OWQS_T0_FREE", "1")
+    free = jit_host(p, "sampled", 64, sources=True)["sources"]
+    bad, tot = conflicted_accesses(free)
+    assert tot > 0 and bad == 0
+    assert count(free) <= count(base)
+    assert any("reinterpret_cast<float2*>" in s for s in free.values())

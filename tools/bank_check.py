@@ -10,10 +10,11 @@ from paper_1604_05659_b200.host import jit_host  # noqa: E402
 from workloads.patterns import config_pattern  # noqa: E402
 
 
-def rank3(vals):
-    rows = [v & 7 for v in vals]
+def rank_bits(vals, nbits):
+    rows = list(vals)
     r = 0
-    for bit in (4, 2, 1):
+    for b in reversed(range(nbits)):
+        bit = 1 << b
         piv = next((i for i in range(r, len(rows)) if rows[i] & bit), None)
         if piv is None:
             continue
@@ -26,20 +27,26 @@ def rank3(vals):
 
 
 def conflicted_accesses(sources):
-    """(conflicted, total) shared-memory accesses over the generated kernel sources."""
+    """(conflicted, total) shared-memory accesses over the generated kernel sources. Bases are byte
+    offsets; a 16 B access (float4 / double2) is conflict-free when lane bits 0..2 give independent
+    bank groups (bits 4..6 of the address), an 8 B access (float2) when lane bits 0..3 give
+    independent 8 B slots of a 128 B wavefront (bits 3..6)."""
     tot = bad = 0
     for k, s in sorted(sources.items()):
         if k < 0:
             continue
         bases = {}
-        for m in re.finditer(r"const int sb(\d+) = 16 \* \((.*)\);", s):
+        for m in re.finditer(r"const int sb(\d+) = \((.*)\);", s):
             coef = {int(a): int(b) for a, b in re.findall(r"\(\(lane >> (\d)\) & 1\) \* (\d+)\)", m.group(2))}
             bases[m.group(1)] = coef
-        for m in re.finditer(r"dsm \+ \(sb(\d+) \^", s):
-            c = bases[m.group(1)]
+        for m in re.finditer(r"reinterpret_cast<(?:const )?(float4|double2|float2)\*>\(dsm \+ \(sb(\d+) \^", s):
+            c = bases[m.group(2)]
             tot += 1
-            if rank3([c.get(0, 0), c.get(1, 0), c.get(2, 0)]) < 3:
-                bad += 1
+            if m.group(1) == "float2":
+                ok = rank_bits([(c.get(j, 0) >> 3) & 15 for j in range(4)], 4) == 4
+            else:
+                ok = rank_bits([(c.get(j, 0) >> 4) & 7 for j in range(3)], 3) == 3
+            bad += not ok
     return bad, tot
 
 
