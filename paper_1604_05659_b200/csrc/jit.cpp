@@ -28,6 +28,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cctype>
 #include <array>
 #include <chrono>
 #include <map>
@@ -263,7 +264,7 @@ struct Gen {
   std::vector<Pend> pend;
   std::string error;
 
-  Gen(const StepDesc& dd, int pr, bool use_tile)
+  Gen(const StepDesc& dd, int pr, bool use_tile, bool free_t0 = false)
       : d(dd), prec(pr), tile(use_tile), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1) {
     if (tile) {
       KHI = KTILE;
@@ -281,7 +282,7 @@ struct Gen {
       if (prec == 0) {
         RB = tile_geom().rb;
         WB = tile_geom().wb;
-        t0free = getenv("OWQS_T0_FREE") != nullptr;
+        t0free = free_t0;
         FB = t0free ? 0 : 1;
         LS = 1;
         NSEL = t0free ? RB : RB - 1;
@@ -1648,6 +1649,21 @@ const std::string& jit_prelude() {
   return s;
 }
 
+namespace {
+int count_of(const std::string& s, const char* what) {
+  int n = 0;
+  for (size_t i = s.find(what); i != std::string::npos; i = s.find(what, i + 1)) ++n;
+  return n;
+}
+int transposes_of(const std::string& s) {
+  const size_t i = s.find(" transpose(s)");
+  if (i == std::string::npos) return 0;
+  size_t j = i;
+  while (j > 0 && isdigit((unsigned char)s[j - 1])) --j;
+  return atoi(s.c_str() + j);
+}
+}  // namespace
+
 std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
   const int eng = jit_engine(d, prec);
   if (!eng) return "";
@@ -1655,6 +1671,18 @@ std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
   if (!g.error.empty()) return "";
   std::string body = g.run();
   if (!g.error.empty()) return "";
+  // complex64 tile passes: the t0-free plan (phases over any 5 of the 13 tile bits) where it needs
+  // fewer transposes and no more shared-memory instructions (8 B accesses when t0 is a lane bit);
+  // OWQS_T0_FREE=0 / 1 forces it off / on for every pass
+  const char* tf = getenv("OWQS_T0_FREE");
+  if (eng == 2 && prec == 0 && !(tf && atoi(tf) == 0)) {
+    Gen g2(d, prec, true, true);
+    std::string b2 = g2.error.empty() ? g2.run() : std::string();
+    if (g2.error.empty() && !b2.empty()) {
+      const int smem1 = count_of(body, "reinterpret_cast<"), smem2 = count_of(b2, "reinterpret_cast<");
+      if ((tf && atoi(tf) == 1) || (transposes_of(b2) < transposes_of(body) && smem2 <= smem1)) body = b2;
+    }
+  }
   const std::string nm = std::string(eng == 2 ? "owqs_tma_" : "owqs_pass_") + (prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
   const std::string key = "OWQS_KNAME";
   body.replace(body.find(key), key.size(), nm);
