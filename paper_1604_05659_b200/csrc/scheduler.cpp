@@ -1077,7 +1077,9 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
     for (const LOp& l : em.ops) resize = resize || l.type == 10 || l.type == 11;
     const char* env = getenv("OWQS_REMAP");
     // default on (OWQS_REMAP=0 turns it off): C3 51 -> 35 passes, 51.0 -> 49.8 ms
-    pk.remap = (!env || atoi(env) != 0) && !resize && n_global == 0 && pk.kwide > KMAX_AOT;
+    // (sharded programs too: a remap permutes local positions only; rank bits and the swap plan
+    // follow the same pos / at maps)
+    pk.remap = (!env || atoi(env) != 0) && !resize && pk.kwide > KMAX_AOT;
     if (const char* m = getenv("OWQS_REMAP_MARGIN")) pk.remap_margin = atoi(m);
   }
   if (const char* env = getenv("OWQS_KWIDE")) pk.kwide = std::max(KMAX_AOT, std::min(KTILE, atoi(env)));
