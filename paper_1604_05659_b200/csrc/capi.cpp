@@ -76,6 +76,7 @@ struct Shard {
   double* d_red = nullptr;  // -> ctx->d_red_all + 4 * index
 };
 constexpr size_t kStagingBytes = 64ull << 20;
+constexpr size_t kFullOutMaxBytes = 8ull << 30;
 }  // namespace
 
 struct owqs_ctx {
@@ -104,6 +105,8 @@ struct owqs_ctx {
   uint8_t* d_forced = nullptr;
   size_t k_cap = 0;
   void* d_staging = nullptr;
+  void* d_out_full = nullptr;  // owqs_submit_host: whole permuted output (<= kFullOutMaxBytes)
+  size_t out_full_bytes = 0;
   void* h_staging = nullptr;  // pinned
   bool has_input = false, has_output = false;
   int out_cm = -1;
@@ -555,6 +558,34 @@ owqs_status output_to_host_enqueue(owqs_ctx* ctx, void* amps, int out_prec, bool
   const Program& pr = ctx->cm[ctx->out_cm].prog;
   const uint64_t chunk = kStagingBytes / oe;
   char* dst = (char*)amps;
+  if (pinned) {
+    // outputs already in the caller's order at the state's precision: one DMA from the state
+    bool ident = out_prec == ctx->prec && pr.out_slot.size() == ctx->hp.outputs.size();
+    for (size_t k = 0; ident && k < pr.out_slot.size(); ++k) ident = pr.out_slot[k] == (int)k;
+    if (ident) {
+      CU(cudaMemcpyAsync(dst, ctx->shards[0].d_state, n * oe, cudaMemcpyDeviceToHost, ctx->stream));
+      if (sync) CU(cudaStreamSynchronize(ctx->stream));
+      return OWQS_OK;
+    }
+    // asynchronous (owqs_submit_host): one permute kernel into a full-size device buffer and one
+    // DMA, instead of 64 MB chunks alternating kernel / copy -- each small permute kernel would wait
+    // for SM slots behind other contexts' pass kernels and stall this context's copy stream
+    if (!sync && n * oe <= kFullOutMaxBytes) {
+      if (ctx->out_full_bytes < n * oe) {
+        cudaFree(ctx->d_out_full);
+        ctx->d_out_full = nullptr;
+        ctx->out_full_bytes = 0;
+        if (cudaMalloc(&ctx->d_out_full, n * oe) == cudaSuccess) ctx->out_full_bytes = n * oe;
+        else cudaGetLastError();
+      }
+      if (ctx->d_out_full) {
+        CU(launch_permute_out(ctx->shards[0].d_state, ctx->prec, ctx->d_out_full, out_prec, (int)pr.out_slot.size(),
+                              pr.out_slot.data(), 0, n, ctx->stream));
+        CU(cudaMemcpyAsync(dst, ctx->d_out_full, n * oe, cudaMemcpyDeviceToHost, ctx->stream));
+        return OWQS_OK;
+      }
+    }
+  }
   for (uint64_t j0 = 0; j0 < n; j0 += chunk) {
     uint64_t cnt = std::min(chunk, n - j0);
     CU(launch_permute_out(ctx->shards[0].d_state, ctx->prec, ctx->d_staging, out_prec, (int)pr.out_slot.size(),
@@ -784,6 +815,7 @@ void owqs_destroy(owqs_ctx* ctx) {
   cudaFree(ctx->d_prob0);
   cudaFree(ctx->d_forced);
   cudaFree(ctx->d_staging);
+  cudaFree(ctx->d_out_full);
   if (ctx->h_staging) cudaFreeHost(ctx->h_staging);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
