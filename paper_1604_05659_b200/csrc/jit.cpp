@@ -1279,7 +1279,7 @@ struct Gen {
     const int red = d.red_kind;
     const int nred = red == RED_NONE ? 0 : (red == RED_NORM ? 1 : 4);
     const uint64_t nbu = 1ull << (d.width - TB);
-    const uint64_t iters = nbu > (uint64_t)RED_MAX_BLOCKS ? nbu / RED_MAX_BLOCKS : 1;
+    const uint64_t iters = nbu / jit_tile_blocks(d, prec);
     tile_iters = iters;
     build_dag();
     build_predbits();
@@ -1639,7 +1639,14 @@ bool jit_tile_small(const StepDesc& d, int prec) {
 
 unsigned jit_tile_blocks(const StepDesc& d, int prec) {
   const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
-  return (unsigned)(nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu);
+  // test hook OWQS_TILE_MAX_BLOCKS (power of two): cap the grid lower than RED_MAX_BLOCKS so that
+  // small states exercise the several-tiles-per-CTA path of states above 2^20 tiles
+  static const uint64_t cap = [] {
+    const char* e = getenv("OWQS_TILE_MAX_BLOCKS");
+    const uint64_t v = e ? (uint64_t)atoll(e) : 0;
+    return (v && !(v & (v - 1)) && v < (uint64_t)RED_MAX_BLOCKS) ? v : (uint64_t)RED_MAX_BLOCKS;
+  }();
+  return (unsigned)(nbu > cap ? cap : nbu);
 }
 
 int jit_dyn_smem(int engine) { return engine == 2 ? kTileSmem : 0; }
@@ -1764,7 +1771,8 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
   const PassCoef* pcc = pc;
   if (eng == 2) {  // non-persistent: one CTA per 13-bit tile (or iters tiles above RED_MAX_BLOCKS)
     const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
-    const uint64_t blocks = nbu > (uint64_t)RED_MAX_BLOCKS ? (uint64_t)RED_MAX_BLOCKS : nbu;
+    const uint64_t blocks = jit_tile_blocks(d, prec);  // the generator's tiles-per-CTA use the same count
+    (void)nbu;
     void* args[] = {&dd, &pp, &pcc};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
