@@ -309,7 +309,7 @@ owqs_status ensure_device(owqs_ctx* ctx) {
           if (std::find(jm.names.begin(), jm.names.end(), m.jit_name[k]) == jm.names.end()) continue;
           CU(cudaLibraryGetKernel(&fn[k], lib, m.jit_name[k].c_str()));
           const int eng = jit_engine(m.prog.steps[k], ctx->prec);
-          const int dyn = jit_dyn_smem(eng);
+          const int dyn = jit_dyn_smem(eng, ctx->prec);
           if (dyn > 0) {
             CU(cudaFuncSetAttribute((const void*)fn[k], cudaFuncAttributeMaxDynamicSharedMemorySize, dyn));
             // shared-memory carveout just large enough for the CTAs the registers allow: the rest

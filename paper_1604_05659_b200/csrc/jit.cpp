@@ -117,15 +117,26 @@ struct CLayout {
 struct TileGeom {
   int rb, wb;
 };
+// group slots of a complex64 tile: 6 (default: 12-bit tiles, 4-warp CTAs, 4 CTAs per SM) or
+// OWQS_TILE_G = 7 (13-bit tiles, 8-warp CTAs, 2 per SM) / 5 (2-warp CTAs, 8 per SM). Measured on C3:
+// 43.5 / 44.6 / 47.1 ms -- 6 needs 38 passes instead of 35 but four independent CTAs per SM overlap
+// their load / compute / transpose phases better. complex128 keeps KTILE.
+inline int tile_g(int prec) {
+  static const int g = [] {
+    const char* e = getenv("OWQS_TILE_G");
+    return (e && atoi(e) >= 5 && atoi(e) <= KTILE) ? atoi(e) : 6;
+  }();
+  return prec == 0 ? g : KTILE;
+}
 inline TileGeom tile_geom() {
   static const TileGeom g = [] {
     const char* e = getenv("OWQS_TILE_RB");
     const int rb = (e && atoi(e) == 6) ? 6 : 5;
-    return TileGeom{rb, 8 - rb};
+    return TileGeom{rb, 1 + tile_g(0) - rb};  // 6 + G tile bits = RB + 5 lane bits + WB
   }();
   return g;
 }
-inline int tile_bits(int prec) { return (prec == 0 ? 6 : 5) + KTILE; }
+inline int tile_bits(int prec) { return (prec == 0 ? 6 : 5) + tile_g(prec); }
 // 16 B unit of tile index t: v = t >> 1 (complex64 pairs) or t, XOR-swizzled in its low 3 bits by
 // the higher ones: u = v ^ ((v >> 3 ^ v >> 6 ^ v >> 9) & 7). u is a bijection, linear over GF(2)
 // (per-thread base XOR per-register constant), exactly 64 KB for both precisions, and tile bit k
@@ -267,17 +278,17 @@ struct Gen {
   Gen(const StepDesc& dd, int pr, bool use_tile, bool free_t0 = false)
       : d(dd), prec(pr), tile(use_tile), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1) {
     if (tile) {
-      KHI = KTILE;
+      KHI = tile_g(pr);
       UNR = 1;
       int n = 0;
       for (int j = 0; j < d.nb_hi; ++j) gs[n++] = d.bhi[j];
-      for (int s = SB; n < KTILE && s < d.width; ++s) {
+      for (int s = SB; n < KHI && s < d.width; ++s) {
         bool used = false;
         for (int j = 0; j < n; ++j) used = used || gs[j] == s;
         if (!used) gs[n++] = s;
       }
-      if (n < KTILE) error = "tile engine needs width >= SB + 7";
-      std::sort(gs, gs + KTILE);
+      if (n < KHI) error = "tile engine needs width >= SB + group slots";
+      std::sort(gs, gs + KHI);
       TB = tile_bits(prec);
       if (prec == 0) {
         RB = tile_geom().rb;
@@ -411,8 +422,8 @@ struct Gen {
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
   static int prefetch_distance() {
-    // default: one wave of 2 CTAs x 148 SMs (B200); C3 49.8 -> 49.3 ms, C3W 219 -> 213 ms
-    static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH")) : 296;
+    // default: one wave of CTAs per SM x 148 SMs (B200); C3 49.8 -> 49.3 ms, C3W 219 -> 213 ms
+    static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH")) : 148 * tile_minb_for(0);
     return v;
   }
   void bfly(int i, int bi) {
@@ -837,7 +848,9 @@ struct Gen {
   // C3, 3 (80 registers) is 18% slower (serialised loads)
   static int tile_minb_for(int prec) {
     const char* e = getenv("OWQS_TILE_MINB");
-    return e ? std::max(1, std::min(4, atoi(e))) : ((prec == 0 && tile_geom().rb == 6) ? 3 : 2);
+    if (e) return std::max(1, std::min(8, atoi(e)));
+    if (prec == 0 && tile_g(0) < KTILE) return 2 << (KTILE - tile_g(0));  // 4- / 2-warp CTAs
+    return (prec == 0 && tile_geom().rb == 6) ? 3 : 2;
   }
   int tile_minb() const { return tile_minb_for(prec); }
   int n_local_ = 0, n_cta_ = 0, n_group_ = 0, next_bar_ = 1;
@@ -1369,7 +1382,7 @@ struct Gen {
       << (small ? "pc_global" : "pc") << ") {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
       << "  using namespace owqs;\n"
       << "  // tile engine: width " << d.width << ", tile group slots";
-    for (int j = 0; j < KTILE; ++j) o << " " << gs[j];
+    for (int j = 0; j < KHI; ++j) o << " " << gs[j];
     o << " (pass's " << d.nb_hi << "), " << d.n_ops << " ops, " << nbf << " butterflies, reduction " << red << ", "
       << ph.size() << " phase(s), " << n_trans << " transpose(s), " << iters << " tile(s) per CTA, warp bits";
     for (int j = 0; j < WB; ++j) o << " t" << lays[l_load].Wb[j];
@@ -1599,7 +1612,7 @@ std::string jit_nvrtc_version(int* major, int* minor) {
 
 int jit_engine(const StepDesc& d, int prec) {
   if (d.kind != ST_PASS) return 0;
-  if (d.width >= tile_bits(prec) && d.nb_hi <= KTILE && !getenv("OWQS_JIT_NO_TILE")) return 2;
+  if (d.width >= tile_bits(prec) && d.nb_hi <= tile_g(prec) && !getenv("OWQS_JIT_NO_TILE")) return 2;
   if (d.nb_hi > KMAX_AOT) return -1;  // needs the tile engine
   const int SB = prec == 0 ? 6 : 5;
   const int unr = jit_unr_of(d.nb_hi);
@@ -1610,8 +1623,7 @@ int jit_engine(const StepDesc& d, int prec) {
 bool jit_eligible(const StepDesc& d, int prec) { return jit_engine(d, prec) > 0; }
 
 int jit_max_group(int prec, bool no_jit) {
-  (void)prec;
-  return (!no_jit && !getenv("OWQS_JIT_NO_TILE")) ? KTILE : KMAX_AOT;
+  return (!no_jit && !getenv("OWQS_JIT_NO_TILE")) ? tile_g(prec) : KMAX_AOT;
 }
 
 int jit_smem_carveout(int engine, int prec) {
@@ -1619,7 +1631,7 @@ int jit_smem_carveout(int engine, int prec) {
   if (const char* e = getenv("OWQS_CARVEOUT")) return atoi(e);
   // CTAs per SM (register-limited) x (tile + static + reserved), as a percentage of 228 KB
   // (static: red_s[8][4] + flag; reserved: 1 KB per CTA) -- 3 x 64 KB tiles fit the 196 KB split
-  const int per = kTileSmem + 288 + 1024;
+  const int per = jit_dyn_smem(2, prec) + 288 + 1024;
   const int ctas = Gen::tile_minb_for(prec);
   return std::min(100, (ctas * per * 100 + 233471) / 233472);
 }
@@ -1649,7 +1661,9 @@ unsigned jit_tile_blocks(const StepDesc& d, int prec) {
   return (unsigned)(nbu > cap ? cap : nbu);
 }
 
-int jit_dyn_smem(int engine) { return engine == 2 ? kTileSmem : 0; }
+int jit_dyn_smem(int engine, int prec) {
+  return engine == 2 ? 16 << (tile_bits(prec) - (prec == 0 ? 1 : 0)) : 0;  // one 16 B unit per pair / amplitude
+}
 
 const std::string& jit_prelude() {
   static const std::string s = std::string(kPreludeInternal) + "\n" + kPreludeCommon + "\n" + kHelpers;
@@ -1777,7 +1791,7 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(jit_block_threads(eng, prec));
-    cfg.dynamicSmemBytes = (size_t)jit_dyn_smem(eng);
+    cfg.dynamicSmemBytes = (size_t)jit_dyn_smem(eng, prec);
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1790,7 +1804,7 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
   const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));
   void* args[] = {&dd, &pp};
   return cudaLaunchKernel((const void*)k, dim3((unsigned)blocks), dim3(256), args,
-                          (size_t)jit_dyn_smem(eng), s);
+                          (size_t)jit_dyn_smem(eng, prec), s);
 }
 
 }  // namespace owqs

@@ -30,7 +30,7 @@ int jit_max_group(int prec, bool no_jit);
 // True when the step runs as a generated pass kernel.
 bool jit_eligible(const StepDesc& d, int prec);
 // Dynamic shared memory (bytes) and threads per block an engine's kernels are launched with.
-int jit_dyn_smem(int engine);
+int jit_dyn_smem(int engine, int prec);
 int jit_block_threads(int engine, int prec);
 // A tile-engine pass small enough (<= 2 waves) to decide and reduce inside its own kernel (no
 // decide_kernel / grid_finish_kernel launches).

@@ -689,7 +689,7 @@ struct Packer {
   }
 
   // group slots allowed in a pass of (shard) width w
-  int wide_at(int w) const { return (kwide > KMAX_AOT && w >= SB + KTILE) ? kwide : kmax_hi; }
+  int wide_at(int w) const { return (kwide > KMAX_AOT && w >= SB + kwide) ? kwide : kmax_hi; }
   // last step that computes something (a SWAP only permutes: it preserves the norm)
   StepDesc* last_compute() {
     for (int i = (int)pr.steps.size() - 1; i >= 0; --i)
