@@ -422,8 +422,11 @@ struct Gen {
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
   static int prefetch_distance() {
-    // default: one wave of CTAs per SM x 148 SMs (B200); C3 49.8 -> 49.3 ms, C3W 219 -> 213 ms
-    static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH")) : 148 * tile_minb_for(0);
+    // 13-bit tiles (2 CTAs per SM): one wave ahead, 148 x 2, measured C3 49.8 -> 49.3 ms, C3W 219 ->
+    // 213 ms. 12-bit tiles (4 CTAs per SM, default): off -- the extra resident CTAs already hide the
+    // load latency and the prefetch costs issue slots (C3 43.4 -> 42.8 ms, C3E 42.8 -> 41.2 ms)
+    static const int v = getenv("OWQS_PREFETCH") ? atoi(getenv("OWQS_PREFETCH"))
+                                                 : (tile_g(0) == KTILE ? 148 * tile_minb_for(0) : 0);
     return v;
   }
   void bfly(int i, int bi) {
