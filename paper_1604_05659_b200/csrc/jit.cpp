@@ -131,7 +131,7 @@ inline int tile_g(int prec) {
 inline TileGeom tile_geom() {
   static const TileGeom g = [] {
     const char* e = getenv("OWQS_TILE_RB");
-    const int rb = (e && atoi(e) == 6) ? 6 : 5;
+    const int rb = (e && atoi(e) >= 4 && atoi(e) <= 6) ? atoi(e) : 5;
     return TileGeom{rb, 1 + tile_g(0) - rb};  // 6 + G tile bits = RB + 5 lane bits + WB
   }();
   return g;
