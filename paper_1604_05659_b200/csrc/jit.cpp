@@ -126,7 +126,11 @@ inline int tile_g(int prec) {
     const char* e = getenv("OWQS_TILE_G");
     return (e && atoi(e) >= 5 && atoi(e) <= KTILE) ? atoi(e) : 6;
   }();
-  return prec == 0 ? g : KTILE;
+  static const int g128 = [] {  // complex128: 6 (11-bit tiles, 4-warp CTAs, 4 per SM: C3 94.9 ms)
+    const char* e = getenv("OWQS_TILE_G128");  // 7 (8-warp CTAs): 96.1 ms, 5: 97.3 ms
+    return (e && atoi(e) >= 5 && atoi(e) <= KTILE) ? atoi(e) : 6;
+  }();
+  return prec == 0 ? g : g128;
 }
 inline TileGeom tile_geom() {
   static const TileGeom g = [] {
@@ -299,7 +303,7 @@ struct Gen {
         NSEL = t0free ? RB : RB - 1;
       } else {
         RB = 4;
-        WB = 3;
+        WB = tile_g(1) - 4;  // 5 + G tile bits = 4 register + 5 lane + WB warp bits
         FB = 0;
         LS = 0;
         NSEL = 4;
@@ -852,7 +856,7 @@ struct Gen {
   static int tile_minb_for(int prec) {
     const char* e = getenv("OWQS_TILE_MINB");
     if (e) return std::max(1, std::min(8, atoi(e)));
-    if (prec == 0 && tile_g(0) < KTILE) return 2 << (KTILE - tile_g(0));  // 4- / 2-warp CTAs
+    if (tile_g(prec) < KTILE) return 2 << (KTILE - tile_g(prec));  // 4- / 2-warp CTAs
     return (prec == 0 && tile_geom().rb == 6) ? 3 : 2;
   }
   int tile_minb() const { return tile_minb_for(prec); }
@@ -1639,7 +1643,10 @@ int jit_smem_carveout(int engine, int prec) {
   return std::min(100, (ctas * per * 100 + 233471) / 233472);
 }
 
-int jit_block_threads(int engine, int prec) { return (engine == 2 && prec == 0) ? (32 << tile_geom().wb) : 256; }
+int jit_block_threads(int engine, int prec) {
+  if (engine != 2) return 256;
+  return prec == 0 ? (32 << tile_geom().wb) : (32 << (tile_g(1) - 4));
+}
 
 bool jit_tile_small(const StepDesc& d, int prec) {
   if (jit_engine(d, prec) != 2) return false;

@@ -31,12 +31,12 @@ def test_generated_kernels_compile(shape, prec):
 
 def test_wide_passes_need_the_tile_engine():
     """Group slots per pass on the tile engine: 6 for complex64 (12-bit tiles, 4-warp CTAs; 7 with
-    OWQS_TILE_G=7), 7 for complex128; 4 otherwise (AOT / direct)."""
+    OWQS_TILE_G=7), 6 for complex128 (11-bit tiles); 4 otherwise (AOT / direct)."""
     p = W.config_pattern("C3")
     wide = compile_host(p, "sampled", 64)
     narrow = compile_host(p, "sampled", 64, flags=FLAG_NO_JIT)
     c128 = compile_host(p, "sampled", 128)
-    assert max(s.nb_hi for s in wide.steps) == 6 and max(s.nb_hi for s in c128.steps) == 7
+    assert max(s.nb_hi for s in wide.steps) == 6 and max(s.nb_hi for s in c128.steps) == 6
     assert max(s.nb_hi for s in narrow.steps) <= 4
     # wider tiles fuse more butterflies per state sweep: about half the passes (52 vs 100)
     assert wide.info["n_passes"] < 0.6 * narrow.info["n_passes"]
