@@ -108,6 +108,7 @@ struct owqs_ctx {
   void* d_out_full = nullptr;  // owqs_submit_host: whole permuted output (<= kFullOutMaxBytes)
   size_t out_full_bytes = 0;
   void* h_staging = nullptr;  // pinned
+  int32_t* h_err = nullptr;   // pinned, one per shard: device error flags copied in stream order
   bool has_input = false, has_output = false;
   int out_cm = -1;
   int pending = 0;  // owqs_submit_host: 1 + compiled mode of the enqueued run, until owqs_wait
@@ -371,6 +372,19 @@ owqs_status do_swap(owqs_ctx* ctx, const StepDesc& d) {
   return OWQS_OK;
 }
 
+// Page-locked staging layout for one run: RunParams at 0, forced outcomes at 4096, then the run's
+// readbacks (outcomes, prob0, the reduction result) copied in stream order right after the run.
+struct RunStaging {
+  size_t forced = 4096, outcomes, prob0, red, end;
+  explicit RunStaging(int64_t K) {
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    outcomes = forced + up((size_t)std::max<int64_t>(K, 1));
+    prob0 = outcomes + up((size_t)std::max<int64_t>(K, 1));
+    red = prob0 + up((size_t)std::max<int64_t>(K, 1) * sizeof(double));
+    end = red + 4 * sizeof(double);
+  }
+};
+
 // Enqueue one run on ctx->stream without synchronising the host (run parameters and forced
 // outcomes go through the page-locked staging buffer, so the copies are truly asynchronous; no
 // earlier copy from it is pending because every call ends synchronised or with owqs_wait).
@@ -381,9 +395,10 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
   rp->mode = mode;
   rp->seed = seed;
   CU(cudaMemcpyAsync(ctx->d_run, rp, sizeof(RunParams), cudaMemcpyHostToDevice, ctx->stream));
+  const RunStaging rs(ctx->hp.n_measure);
+  if (rs.end > kStagingBytes) return fail(ctx, OWQS_E_ARG, "too many measurements");
   if (mode == OWQS_FORCED && ctx->hp.n_measure > 0) {
-    if ((size_t)ctx->hp.n_measure + 4096 > kStagingBytes) return fail(ctx, OWQS_E_ARG, "too many measurements");
-    uint8_t* hf = static_cast<uint8_t*>(ctx->h_staging) + 4096;
+    uint8_t* hf = static_cast<uint8_t*>(ctx->h_staging) + rs.forced;
     memcpy(hf, forced, ctx->hp.n_measure);
     CU(cudaMemcpyAsync(ctx->d_forced, hf, ctx->hp.n_measure, cudaMemcpyHostToDevice, ctx->stream));
   }
@@ -458,6 +473,19 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
     if (st != OWQS_OK) return st;
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream));
+  // error flags to page-locked memory in stream order (a synchronous 4-byte cudaMemcpy after the
+  // run would queue in the copy engine behind other contexts' multi-GiB output transfers)
+  for (size_t r = 0; r < ctx->shards.size(); ++r)
+    CU(cudaMemcpyAsync(ctx->h_err + r, ctx->shards[r].d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+  {
+    uint8_t* hs = static_cast<uint8_t*>(ctx->h_staging);
+    const int64_t K = ctx->hp.n_measure;
+    if (K > 0) {
+      CU(cudaMemcpyAsync(hs + rs.outcomes, ctx->d_outcome, K, cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaMemcpyAsync(hs + rs.prob0, ctx->d_prob0, K * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    }
+    CU(cudaMemcpyAsync(hs + rs.red, ctx->shards[0].d_red, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  }
   ctx->has_input = false;
   ctx->out_cm = cmi;
   return OWQS_OK;
@@ -471,11 +499,7 @@ owqs_status run_complete(owqs_ctx* ctx, int cmi) {
   ctx->stats.last_run_ms = ms;
   ctx->last_cm = cmi;
   int32_t herr = 0;
-  for (auto& s : ctx->shards) {
-    int32_t e = 0;
-    CU(cudaMemcpy(&e, s.d_err, sizeof(e), cudaMemcpyDeviceToHost));
-    herr |= e;
-  }
+  for (size_t r = 0; r < ctx->shards.size(); ++r) herr |= ctx->h_err[r];
   ctx->has_output = true;
   if (herr) return fail(ctx, OWQS_E_BRANCH, "forced outcome on a branch with probability < 1e-12");
   return OWQS_OK;
@@ -786,6 +810,8 @@ owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
   if (cudaMalloc(&ctx->d_run, sizeof(RunParams)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (cudaMalloc(&ctx->d_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (cudaMallocHost(&ctx->h_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
+  if (cudaMallocHost(&ctx->h_err, std::max<size_t>(1, ctx->shards.size()) * sizeof(int32_t)) != cudaSuccess)
+    return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (nr > 1 && !loopback) {
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_id, sizeof(id));
@@ -817,6 +843,7 @@ void owqs_destroy(owqs_ctx* ctx) {
   cudaFree(ctx->d_staging);
   cudaFree(ctx->d_out_full);
   if (ctx->h_staging) cudaFreeHost(ctx->h_staging);
+  if (ctx->h_err) cudaFreeHost(ctx->h_err);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -1094,20 +1121,23 @@ owqs_status run_substates(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const ui
 }
 
 // After a completed run: outcomes / prob0 to the caller, stats, the EOWQS norm check.
+// (after run_complete: the run's readbacks are in the page-locked staging, RunStaging)
 owqs_status finish_run(owqs_ctx* ctx, int cmi, int mode, owqs_status s, uint8_t* outcomes_out, double* prob0_out) {
   const int64_t K = ctx->hp.n_measure;
+  const RunStaging rs(K);
+  const uint8_t* hs = static_cast<const uint8_t*>(ctx->h_staging);
   if (K > 0 && (s == OWQS_OK || s == OWQS_E_BRANCH)) {
     if (outcomes_out) {
       if (mode == OWQS_EOWQS)
         memset(outcomes_out, 0, K);
       else
-        CU(cudaMemcpy(outcomes_out, ctx->d_outcome, K, cudaMemcpyDeviceToHost));
+        memcpy(outcomes_out, hs + rs.outcomes, K);
     }
     if (prob0_out) {
       if (mode == OWQS_EOWQS)
         for (int64_t i = 0; i < K; ++i) prob0_out[i] = -1.0;
       else
-        CU(cudaMemcpy(prob0_out, ctx->d_prob0, K * sizeof(double), cudaMemcpyDeviceToHost));
+        memcpy(prob0_out, hs + rs.prob0, K * sizeof(double));
     }
   }
   if (s != OWQS_OK) return s;
@@ -1126,7 +1156,7 @@ owqs_status finish_run(owqs_ctx* ctx, int cmi, int mode, owqs_status s, uint8_t*
   ctx->stats.phys_bits = pr.phys_bits;
   if (mode == OWQS_EOWQS) {
     double red[4];
-    CU(cudaMemcpy(red, ctx->shards[0].d_red, sizeof(red), cudaMemcpyDeviceToHost));
+    memcpy(red, hs + rs.red, sizeof(red));
     const double tol = ctx->prec == 1 ? 1e-8 : 1e-3;
     if (!(std::fabs(red[0] - 1.0) <= tol))
       return fail(ctx, OWQS_E_NOT_DETERMINISTIC,
