@@ -36,8 +36,13 @@ print("ok")
 """
 
 
-def test_several_tiles_per_cta_vs_oracle(require_gpu):
-    env = dict(os.environ, OWQS_TILE_MAX_BLOCKS="4", PYTHONPATH=ROOT + os.pathsep + os.path.join(ROOT, "tests"))
+@pytest.mark.parametrize("extra", [{"OWQS_TILE_MAX_BLOCKS": "4"},
+                                   {"OWQS_TILE_G": "7", "OWQS_TILE_G128": "7"},
+                                   {"OWQS_TILE_G": "5", "OWQS_TILE_MAX_BLOCKS": "8"}])
+def test_tile_geometries_vs_oracle(require_gpu, extra):
+    """several tiles per CTA, and the non-default tile sizes (13-bit complex64 / 12-bit complex128
+    tiles with 8-warp CTAs; 11-bit complex64 tiles with 2-warp CTAs)."""
+    env = dict(os.environ, PYTHONPATH=ROOT + os.pathsep + os.path.join(ROOT, "tests"), **extra)
     r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
                        timeout=900)
     assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]

@@ -118,3 +118,27 @@ def test_t0_free_option_conflict_free_and_fewer_transposes(monkeypatch):
     assert tot > 0 and bad == 0
     assert count(free) <= count(base)
     assert any("reinterpret_cast<float2*>" in s for s in free.values())
+
+
+@pytest.mark.parametrize("g", ["5", "7"])
+def test_other_tile_sizes_generate_conflict_free(g):
+    """OWQS_TILE_G = 5 / 7 (2- / 8-warp complex64 CTAs) still generate conflict-free transposes
+    (the setting is read once per process: checked in a subprocess)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(__file__))
+    code = ("import sys; sys.path.insert(0, 'tools')\n"
+            "from bank_check import conflicted_accesses\n"
+            "from paper_1604_05659_b200.host import jit_host\n"
+            "from workloads import patterns as W\n"
+            "src = jit_host(W.config_pattern('BW:16x6', seed=1), 'sampled', 64, sources=True)['sources']\n"
+            "bad, tot = conflicted_accesses(src)\n"
+            "threads = {int(x) for x in __import__('re').findall(r'__launch_bounds__\\((\\d+),', ''.join(src.values()))}\n"
+            "print(bad, tot, sorted(threads))\n")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, capture_output=True, text=True, timeout=600,
+                         env=dict(os.environ, OWQS_TILE_G=g))
+    assert out.returncode == 0, out.stderr[-2000:]
+    bad, tot, threads = out.stdout.split(" ", 2)
+    assert int(bad) == 0 and int(tot) > 0
+    assert str(32 << (int(g) - 4)) in threads
