@@ -135,7 +135,8 @@ inline int tile_g(int prec) {
 inline TileGeom tile_geom() {
   static const TileGeom g = [] {
     const char* e = getenv("OWQS_TILE_RB");
-    const int rb = (e && atoi(e) >= 4 && atoi(e) <= 6) ? atoi(e) : 5;
+    int rb = (e && atoi(e) >= 4 && atoi(e) <= 6) ? atoi(e) : 5;
+    if (1 + tile_g(0) - rb < 1) rb = 5;  // at least one warp bit
     return TileGeom{rb, 1 + tile_g(0) - rb};  // 6 + G tile bits = RB + 5 lane bits + WB
   }();
   return g;
@@ -297,7 +298,7 @@ struct Gen {
       if (prec == 0) {
         RB = tile_geom().rb;
         WB = tile_geom().wb;
-        t0free = free_t0;
+        t0free = free_t0 && RB <= 5;  // a phase holds at most 5 selected bits (Phase::S)
         FB = t0free ? 0 : 1;
         LS = 1;
         NSEL = t0free ? RB : RB - 1;
