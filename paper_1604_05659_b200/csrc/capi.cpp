@@ -66,6 +66,9 @@ struct CompiledMode {
   std::vector<int> jit_blocks;
   int n_jit = 0;
   PassCoef* d_pc = nullptr;  // one decision block per step (engine-2 generated kernels)
+  // EOWQS: every decision is run-independent (outcomes 0, no signals, no probabilities, static
+  // scales), so d_pc written by the first EOWQS run is reused and later runs launch no decide kernel
+  bool pc_static_ready = false;
 };
 // one rank's part of the state and its reduction scratch
 struct Shard {
@@ -138,8 +141,8 @@ double kernels_per_run(const owqs_ctx* ctx, const CompiledMode& m) {
     const StepDesc& s = m.prog.steps[i];
     n += 1;
     if (i < m.jit_name.size() && !m.jit_name[i].empty() && jit_engine(s, ctx->prec) == 2 &&
-        !jit_tile_small(s, ctx->prec))
-      n += 1 + (s.red_kind != RED_NONE ? 1 : 0);  // decide + grid finish
+        !jit_tile_small(s, ctx->prec))  // decide (not in EOWQS runs after the first) + grid finish
+      n += (m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE") ? 0 : 1) + (s.red_kind != RED_NONE ? 1 : 0);
   }
   return n;
 }
@@ -403,7 +406,10 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
     CU(cudaMemcpyAsync(ctx->d_forced, hf, ctx->hp.n_measure, cudaMemcpyHostToDevice, ctx->stream));
   }
   for (auto& s : ctx->shards) CU(cudaMemsetAsync(s.d_err, 0, sizeof(int32_t), ctx->stream));
-  const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH);
+  // EOWQS after its first run: the decisions are already in d_pc (CompiledMode::pc_static_ready);
+  // the first run launches directly so that no captured graph contains the decide kernels
+  const bool static_pc = mode == OWQS_EOWQS && m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE");
+  const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH) && (mode != OWQS_EOWQS || static_pc);
   const bool prof = (ctx->cfg.flags & OWQS_FLAG_PROFILE) != 0;
   if (prof) {
     if (ctx->prof_cm != cmi && m.gexec) {  // event lists follow the compiled mode
@@ -432,7 +438,7 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
         const bool jit = !m.jit_fn.empty() && m.jit_fn[i];
         const int eng = jit ? jit_engine(s, ctx->prec) : 0;
         const bool small = eng == 2 && jit_tile_small(s, ctx->prec);
-        if (eng == 2 && !small) CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream));
+        if (eng == 2 && !small && !static_pc) CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream));
         for (size_t r = 0; r < ctx->shards.size(); ++r) {
           if (jit)
             CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream));
@@ -502,6 +508,7 @@ owqs_status run_complete(owqs_ctx* ctx, int cmi) {
   for (size_t r = 0; r < ctx->shards.size(); ++r) herr |= ctx->h_err[r];
   ctx->has_output = true;
   if (herr) return fail(ctx, OWQS_E_BRANCH, "forced outcome on a branch with probability < 1e-12");
+  if (cmi == 1) ctx->cm[1].pc_static_ready = true;  // the EOWQS mode's decisions are in d_pc
   return OWQS_OK;
 }
 
