@@ -147,9 +147,17 @@ void owqs_destroy(owqs_ctx* ctx);
 
 /* Load a pattern in its GIVEN (execution) order (L67; right-to-left notation already reversed).
  * Validates D0-D3 (L83-91), inserts implicit N, builds the dependency DAG of non-commuting
- * commands (Eqs. 14-16) and runs PROA (Eq. 18 with the tuning of L487). No device work.
+ * commands (Eqs. 14-16) and runs PROA (Eq. 18 with the tuning of L487). No device memory is
+ * touched (device buffers are allocated at the first input / run).
  * inputs[n_in], outputs[n_out] : qubit ids; bit k of the input/output index is inputs[k]/outputs[k].
  * domain_pool[pool_len]        : qubit ids referenced by the cmds' signal domains.
+ * Sub-states (§4.1): when the pattern's entanglement graph has several components (all
+ * inputs count as one) and no signal domain crosses them, each component runs as its own state
+ * vector (memory of the largest, not of their sum) and owqs_get_output returns their tensor
+ * product; single rank only, disabled by OWQS_FLAG_ONE_STATE. Calls that need one state vector
+ * (owqs_output_inner / _norm, owqs_recognize*, owqs_run_batch, owqs_submit_host, owqs_plan_order,
+ * owqs_launch_profile) then return OWQS_E_STATE. owqs_stats().n_substates reports the split.
+ * The pass kernels are generated and NVRTC-compiled here (kept in a process-wide cache).
  * Errors: OWQS_E_ARG, OWQS_E_PATTERN (message names the command index). */
 owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in,
                               const int32_t* outputs, int32_t n_out,
