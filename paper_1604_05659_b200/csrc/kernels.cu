@@ -998,6 +998,9 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
   // the pass kernel that follows is launched with programmatic stream serialisation: let it start
   // (it issues its state loads, then griddepcontrol.wait-s for this grid before reading pc)
   if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // launched behind grid_finish_kernel with programmatic serialisation too: wait for the previous
+  // grid (the reduction this pass decides from) before reading anything it wrote
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ PassShared sh;
   pass_prologue(d, p, sh, true);
   const int t = threadIdx.x;
@@ -1019,6 +1022,8 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
 // (fenced counter) sums gpart[0..G) in order. G <= RED_MAX_GROUPS CTAs of 256 threads keep the
 // 2^15-partial sum of a 2^28-amplitude pass at a few microseconds (one CTA: ~24 us).
 __global__ void __launch_bounds__(256) grid_finish_kernel(DevPtrs p, unsigned nblk, int nred) {
+  // let the next pass's decide kernel (one warp) launch now; it waits for this grid before reading
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   __shared__ double red[8][4];
   __shared__ int last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1069,8 +1074,25 @@ cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaSt
 }
 
 cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s) {
-  decide_kernel<<<1, 32, 0, s>>>(d, p, pc, getenv("OWQS_PDL_NO_TRIGGER") ? 0 : 1);
-  return cudaGetLastError();
+  static const bool no_trigger = getenv("OWQS_PDL_NO_TRIGGER") != nullptr;
+  static const bool no_pdl = getenv("OWQS_NO_PDL") != nullptr || getenv("OWQS_NO_DECIDE_PDL") != nullptr;
+  const int trig = no_trigger ? 0 : 1;
+  if (no_pdl) {
+    decide_kernel<<<1, 32, 0, s>>>(d, p, pc, trig);
+    return cudaGetLastError();
+  }
+  // programmatic serialisation behind the previous kernel (grid_finish_kernel triggers at its
+  // start): the decide kernel's launch latency overlaps the reduction's finish
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, decide_kernel, d, p, pc, trig);
 }
 
 static inline int unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
