@@ -97,6 +97,11 @@ typedef struct {
                                         entanglement graph has several components (default: each
                                         component is its own sub-state, PAPER §4.1; see
                                         owqs_load_pattern)                                        */
+#define OWQS_FLAG_MEASURED_NORM 0x200u /* structural decisions (a measurement whose partner is a
+                                          fresh |+>: prob0 = 1/2 ||psi||^2, Eq. 13) from a ||psi||^2
+                                          reduced by the previous pass instead of its exact value 1
+                                          (DESIGN R-13): one extra reduction per pass; prob0_out then
+                                          reports the device-measured value                       */
 #define OWQS_FLAG_LOOPBACK    0x20u /* n_ranks > 1 on ONE device: the context holds every rank's
                                        shard and runs them one after the other (swaps and
                                        all-reduces by device copies); for testing the sharded path
@@ -167,7 +172,14 @@ owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in
 /* Input state of the input qubits (L153). amps: HOST array of n_amps = 2^n_in complex128 values,
  * interleaved (re, im). Copied to the device (converted to complex64 at precision 64).
  * Multi-rank: every rank passes the full array; each copies its shard.
- * Errors: OWQS_E_ARG (size), OWQS_E_STATE (no pattern), OWQS_E_NOMEM, OWQS_E_CUDA. */
+ * CONTRACT (every owqs_set_input_* / owqs_submit_host / owqs_run_batch input): the state must be
+ * normalised, |1 - ||psi||^2| <= 1e-9 (precision 128) / 1e-5 (precision 64). A measurement whose
+ * partner qubit is a fresh |+> has prob0 = 1/2 ||psi||^2 exactly (Eq. 3 / Eq. 13; DESIGN
+ * R-13); the executor takes ||psi||^2 = 1 there instead of reducing the state, and Eq. 4's
+ * renormalisation keeps it 1 after every measurement that does reduce. The library
+ * reduces ||psi||^2 on the device during the copy and refuses other inputs with OWQS_E_ARG (the
+ * context then has no input); owqs_submit_host reports it from owqs_wait.
+ * Errors: OWQS_E_ARG (size, norm), OWQS_E_STATE (no pattern), OWQS_E_NOMEM, OWQS_E_CUDA. */
 owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps);
 
 /* Same from a HOST buffer at `precision` (64: interleaved float pairs, 8 B per amplitude; 128:
@@ -178,11 +190,14 @@ owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precisi
 
 /* Same from a DEVICE buffer on the context's device. precision 64: interleaved float pairs;
  * 128: interleaved double pairs. The buffer is read during the call only. NCCL multi-rank: the
- * buffer holds this rank's shard (n_amps = 2^n_in / n_ranks); loopback: the full state. */
+ * buffer holds this rank's shard (n_amps = 2^n_in / n_ranks); loopback: the full state.
+ * Same-precision input is copied and its norm^2 reduced in one sweep (norm contract above, the
+ * all-ranks norm in the multi-rank case); the call synchronises the context's stream. */
 owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t precision, int64_t n_amps);
 
 /* Device-generated Haar-random input (documented counter generator, workloads/inputs.py):
- * amp_j = sqrt(-2 ln u1) e^{2 pi i u2} from splitmix64 of (seed, j), then normalised. */
+ * amp_j = sqrt(-2 ln u1) e^{2 pi i u2} from splitmix64 of (seed, j), then normalised (so it meets
+ * the norm contract of owqs_set_input by construction). */
 owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed);
 
 /* Execute the loaded pattern on the current input (consumes it: the state becomes the output).
@@ -207,7 +222,8 @@ owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t
  * until owqs_wait. Two contexts on different streams pipeline: one run's PCIe copies overlap the
  * other's kernels. Single rank only (OWQS_E_ARG). Any other call on the context before owqs_wait
  * returns OWQS_E_STATE. Errors found while enqueueing are returned here; errors of the run itself
- * (OWQS_E_BRANCH, OWQS_E_NOT_DETERMINISTIC, CUDA faults) are returned by owqs_wait. */
+ * (OWQS_E_BRANCH, OWQS_E_NOT_DETERMINISTIC, CUDA faults) and an input that breaks the norm
+ * contract of owqs_set_input (OWQS_E_ARG, output not valid) are returned by owqs_wait. */
 owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced,
                              const void* in_amps, int32_t in_precision, int64_t n_in, void* out_amps,
                              int32_t out_precision, int64_t n_out);
@@ -220,7 +236,8 @@ owqs_status owqs_wait(owqs_ctx* ctx, uint8_t* outcomes_out, double* prob0_out);
  * inputs  : HOST [n_batch][2^n_in] complex128 interleaved (input k of state b at b*2^n_in + k)
  * seeds   : [n_batch] sampled-mode seeds (NULL: all 0); forced: [n_batch][n_measure] (OWQS_FORCED)
  * outputs : HOST [n_batch][2^n_out] complex128; outcomes / prob0 (may be NULL): [n_batch][n_measure]
- * Semantics per state are those of owqs_set_input + owqs_run + owqs_get_output; EOWQS applies the
+ * Semantics per state are those of owqs_set_input + owqs_run + owqs_get_output (OWQS_E_ARG for an
+ * input off the norm contract, |1 - ||psi||^2| > 1e-9, checked on the host); EOWQS applies the
  * gflow gate, OWQS_E_BRANCH if any forced branch is impossible, OWQS_E_NOT_DETERMINISTIC if any
  * EOWQS output norm^2 is off by more than the owqs_run tolerance. Does not touch the context's
  * current input/output. */
@@ -240,6 +257,13 @@ owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, i
 /* Output into a DEVICE buffer (precision 64: float pairs, 128: double pairs), n_amps >= 2^n_out
  * (single rank). */
 owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precision, int64_t n_amps);
+
+/* Sampled output amplitudes ("the state of the output qubits is reported", for states too
+ * large to copy out: SURVEY §8(a) a10 "device-side compare"): amps[i] = output amplitude idx[i],
+ * caller order (bit k <-> outputs[k]), idx: HOST [n] in [0, 2^n_out), amps: HOST [n] complex128
+ * interleaved, any state precision. Multi-rank: collective, every rank receives all n values.
+ * Errors: OWQS_E_ARG (index range), OWQS_E_STATE (no output, sub-states), OWQS_E_NOMEM. */
+owqs_status owqs_get_output_sample(owqs_ctx* ctx, const int64_t* idx, int64_t n, double* amps);
 
 /* <a|b> of the output states of two contexts with the same output qubits, on the device.
  * Multi-rank: both contexts need the same sharding and final layout (collective call). */

@@ -16,12 +16,14 @@ FLAG_NO_GRAPH, FLAG_NO_FUSE, FLAG_GIVEN_ORDER, FLAG_NO_TUNE, FLAG_PROFILE, FLAG_
 FLAG_NO_GFLOW = 64
 FLAG_NO_JIT = 128
 FLAG_ONE_STATE = 256  # keep a disconnected pattern in one state vector (no sub-states)
+FLAG_MEASURED_NORM = 512  # structural decisions from a reduced ||psi||^2 instead of 1 (DESIGN R-13)
 KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = ["owqs_create", "owqs_destroy", "owqs_load_pattern", "owqs_set_input", "owqs_set_input_host",
             "owqs_get_output_host", "owqs_set_input_device",
             "owqs_set_input_random", "owqs_run", "owqs_submit_host", "owqs_wait", "owqs_run_batch", "owqs_get_output", "owqs_get_output_device",
+            "owqs_get_output_sample",
             "owqs_output_inner", "owqs_output_norm", "owqs_nccl_unique_id", "owqs_recognize", "owqs_recognize_choi",
             "owqs_pattern_info", "owqs_plan_order", "owqs_gflow",
             "owqs_set_proa_weights", "owqs_stats", "owqs_launch_profile", "owqs_last_error", "owqs_version"]
@@ -75,6 +77,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
         "owqs_run_batch": (C.c_int, [ctx, C.c_int, C.c_int64, P(C.c_double), P(C.c_uint64), P(C.c_uint8),
                                      P(C.c_double), P(C.c_uint8), P(C.c_double)]),
         "owqs_get_output_device": (C.c_int, [ctx, C.c_void_p, C.c_int32, C.c_int64]),
+        "owqs_get_output_sample": (C.c_int, [ctx, C.POINTER(C.c_int64), C.c_int64, C.POINTER(C.c_double)]),
         "owqs_output_inner": (C.c_int, [ctx, ctx, P(C.c_double), P(C.c_double)]),
         "owqs_output_norm": (C.c_int, [ctx, P(C.c_double)]),
         "owqs_nccl_unique_id": (C.c_int, [C.c_void_p]),

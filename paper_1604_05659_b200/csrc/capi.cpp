@@ -31,6 +31,9 @@ cudaError_t launch_basis(void* state, int prec, uint64_t n, uint64_t k, cudaStre
 cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, uint64_t j0, cudaStream_t s);
 cudaError_t launch_scale(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
 cudaError_t launch_norm(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
+cudaError_t launch_sample_out(const void* shard, int prec, const int64_t* idx, uint64_t n, int nbits, const int* slots,
+                              uint64_t rank, int wl, void* out, cudaStream_t s);
+cudaError_t launch_copy_norm(const DevPtrs& p, int prec, const void* src, uint64_t n, cudaStream_t s);
 cudaError_t launch_dot(const DevPtrs& p, const void* a, const void* b, uint64_t n, cudaStream_t s);
 cudaError_t launch_dot_t(const DevPtrs& p, int prec, const void* a, const void* b, uint64_t n, cudaStream_t s);
 cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_width, int pl, int bit, bool unpack,
@@ -112,6 +115,7 @@ struct owqs_ctx {
   size_t out_full_bytes = 0;
   void* h_staging = nullptr;  // pinned
   int32_t* h_err = nullptr;   // pinned, one per shard: device error flags copied in stream order
+  double* h_innorm = nullptr;  // pinned: ||psi_in||^2 of the last input (R-13 precondition), stream-ordered
   bool has_input = false, has_output = false;
   int out_cm = -1;
   int pending = 0;  // owqs_submit_host: 1 + compiled mode of the enqueued run, until owqs_wait
@@ -214,7 +218,8 @@ owqs_status compile_modes(owqs_ctx* ctx) {
     auto t0 = std::chrono::steady_clock::now();
     CompiledMode& m = ctx->cm[i];
     plan_and_compile(ctx->hp, i == 1 ? 2 : 0, SB, fuse, given, w, m.plan, m.prog, ctx->n_global,
-                     jit_max_group(ctx->prec, (ctx->cfg.flags & OWQS_FLAG_NO_JIT) != 0));
+                     jit_max_group(ctx->prec, (ctx->cfg.flags & OWQS_FLAG_NO_JIT) != 0),
+                     (ctx->cfg.flags & OWQS_FLAG_MEASURED_NORM) != 0);
     if (!m.prog.error.empty()) return fail(ctx, OWQS_E_ARG, m.prog.error);
     m.schedule_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     m.valid = true;
@@ -643,6 +648,14 @@ owqs_status run_batch_internal(owqs_ctx* ctx, int mode, int64_t nb, const double
   if (ctx->n_ranks > 1) return fail(ctx, OWQS_E_ARG, "batched replicas run on a single rank");
   if (((size_t)ctx->elem << pr.phys_bits) > (size_t)kBatchMaxBytes)
     return fail(ctx, OWQS_E_ARG, "batched replicas need a physical width <= 12 (complex128: 12, complex64: 13)");
+  // R-13 precondition on every replica's input (small widths: checked on the host)
+  for (int64_t b = 0; b < nb; ++b) {
+    double n2 = 0.0;
+    const double* x = inputs + (size_t)b * (2ull << ni);
+    for (uint64_t i = 0; i < (2ull << ni); ++i) n2 += x[i] * x[i];
+    if (!(std::fabs(n2 - 1.0) <= 1e-9))
+      return fail(ctx, OWQS_E_ARG, "batch input " + std::to_string(b) + " not normalised: ||psi||^2 = " + std::to_string(n2));
+  }
   owqs_status s = ensure_device(ctx);
   if (s != OWQS_OK) return s;
   if (!m.d_steps) {
@@ -817,6 +830,7 @@ owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
   if (cudaMalloc(&ctx->d_run, sizeof(RunParams)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (cudaMalloc(&ctx->d_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (cudaMallocHost(&ctx->h_staging, kStagingBytes) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
+  if (cudaMallocHost(&ctx->h_innorm, sizeof(double)) != cudaSuccess) return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (cudaMallocHost(&ctx->h_err, std::max<size_t>(1, ctx->shards.size()) * sizeof(int32_t)) != cudaSuccess)
     return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (nr > 1 && !loopback) {
@@ -851,6 +865,7 @@ void owqs_destroy(owqs_ctx* ctx) {
   cudaFree(ctx->d_out_full);
   if (ctx->h_staging) cudaFreeHost(ctx->h_staging);
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
+  if (ctx->h_innorm) cudaFreeHost(ctx->h_innorm);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
@@ -952,6 +967,35 @@ owqs_status load_compiled(owqs_ctx* ctx) {
   return OWQS_OK;
 }
 
+// R-13 precondition (Eq. 3-4): a measurement whose partner is a fresh |+>
+// has prob0 = 1/2 ||psi||^2, and the structural decisions take ||psi||^2 = 1 without a reduction,
+// so every caller input must be normalised (the oracle refuses the same inputs).
+// input_norm_enqueue: ||psi_in||^2 of the state just written (the shards' red_result, unless the
+// copy kernel already reduced it) all-reduced over the ranks and copied, in stream order, to
+// page-locked memory; input_norm_check reads it after a synchronisation.
+constexpr double kInNormTol64 = 1e-5, kInNormTol128 = 1e-9;
+
+owqs_status input_norm_enqueue(owqs_ctx* ctx, bool reduced) {
+  const uint64_t per = (1ull << ctx->hp.inputs.size()) >> ctx->n_global;
+  if (!reduced)
+    for (size_t r = 0; r < ctx->shards.size(); ++r)
+      CU(launch_norm(dev_ptrs(ctx, ctx->cm[0], (int)r), ctx->prec, per, ctx->stream));
+  owqs_status s = allreduce_red(ctx);
+  if (s != OWQS_OK) return s;
+  CU(cudaMemcpyAsync(ctx->h_innorm, ctx->shards[0].d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  return OWQS_OK;
+}
+
+owqs_status input_norm_check(owqs_ctx* ctx) {
+  const double n2 = *ctx->h_innorm, tol = ctx->prec == 1 ? kInNormTol128 : kInNormTol64;
+  if (!(std::fabs(n2 - 1.0) <= tol)) {
+    ctx->has_input = false;
+    return fail(ctx, OWQS_E_ARG, "input state not normalised: ||psi||^2 = " + std::to_string(n2) +
+                                     " (|1 - ||psi||^2| must be <= " + (ctx->prec == 1 ? "1e-9" : "1e-5") + ")");
+  }
+  return OWQS_OK;
+}
+
 owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps) {
   return owqs_set_input_host(ctx, amps, 128, n_amps);
 }
@@ -976,9 +1020,13 @@ owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precisi
   if (s != OWQS_OK) return s;
   s = input_from_host_enqueue(ctx, amps, precision);
   if (s != OWQS_OK) return s;
+  s = input_norm_enqueue(ctx, false);
+  if (s != OWQS_OK) return s;
   CU(cudaStreamSynchronize(ctx->stream));
-  ctx->has_input = true;
   ctx->has_output = false;
+  s = input_norm_check(ctx);
+  if (s != OWQS_OK) return s;
+  ctx->has_input = true;
   return OWQS_OK;
 }
 
@@ -1027,14 +1075,19 @@ owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t p
   const size_t se = precision == 64 ? 8 : 16;
   for (size_t r = 0; r < ctx->shards.size(); ++r) {
     const char* src = (const char*)dev_amps + (ctx->loopback ? r * per * se : 0);
-    if (sp == ctx->prec) {
-      CU(cudaMemcpyAsync(ctx->shards[r].d_state, src, per * ctx->elem, cudaMemcpyDeviceToDevice, ctx->stream));
+    if (sp == ctx->prec) {  // one sweep: copy + ||psi||^2
+      CU(launch_copy_norm(dev_ptrs(ctx, ctx->cm[0], (int)r), ctx->prec, src, per, ctx->stream));
     } else {
       CU(launch_convert_in(src, sp, ctx->shards[r].d_state, ctx->prec, 0, per, ctx->stream));
     }
   }
-  ctx->has_input = true;
+  s = input_norm_enqueue(ctx, sp == ctx->prec);
+  if (s != OWQS_OK) return s;
+  CU(cudaStreamSynchronize(ctx->stream));
   ctx->has_output = false;
+  s = input_norm_check(ctx);
+  if (s != OWQS_OK) return s;
+  ctx->has_input = true;
   return OWQS_OK;
 }
 
@@ -1198,6 +1251,8 @@ owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const
   if (s != OWQS_OK) return s;
   s = input_from_host_enqueue(ctx, in_amps, in_precision);
   if (s != OWQS_OK) return s;
+  s = input_norm_enqueue(ctx, false);  // checked by owqs_wait (stream-ordered readback)
+  if (s != OWQS_OK) return s;
   ctx->has_input = true;
   ctx->has_output = false;
   const int cmi = mode == OWQS_EOWQS ? 1 : 0;
@@ -1216,6 +1271,13 @@ owqs_status owqs_wait(owqs_ctx* ctx, uint8_t* outcomes_out, double* prob0_out) {
   const int cmi = ctx->pending - 1;
   ctx->pending = 0;
   owqs_status s = run_complete(ctx, cmi);
+  if (s == OWQS_OK || s == OWQS_E_BRANCH) {  // the run completed: its input's norm is readable
+    const owqs_status sn = input_norm_check(ctx);
+    if (sn != OWQS_OK) {
+      ctx->has_output = false;
+      return sn;
+    }
+  }
   return finish_run(ctx, cmi, ctx->pending_mode, s, outcomes_out, prob0_out);
 }
 
@@ -1303,6 +1365,43 @@ owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precis
   if (s != OWQS_OK) return s;
   CU(cudaStreamSynchronize(ctx->stream));
   return OWQS_OK;
+}
+
+owqs_status owqs_get_output_sample(owqs_ctx* ctx, const int64_t* idx, int64_t n, double* amps) {
+  if (!ctx) return OWQS_E_ARG;
+  if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
+  if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_get_output_sample");
+  if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
+  if (n < 0 || (n > 0 && (!idx || !amps))) return fail(ctx, OWQS_E_ARG, "bad sample buffers");
+  if (n == 0) return OWQS_OK;
+  const int nbo = (int)ctx->hp.outputs.size();
+  for (int64_t i = 0; i < n; ++i)
+    if (idx[i] < 0 || (nbo < 63 && (uint64_t)idx[i] >= (1ull << nbo)))
+      return fail(ctx, OWQS_E_ARG, "sample index " + std::to_string(i) + " outside [0, 2^n_out)");
+  const Program& pr = ctx->cm[ctx->out_cm].prog;
+  const int wl = pr.phys_bits - ctx->n_global;
+  void* d = nullptr;
+  const size_t ib = (size_t)n * sizeof(int64_t), ob = (size_t)n * 2 * sizeof(double);
+  if (cudaMalloc(&d, ib + ob) != cudaSuccess) return fail(ctx, OWQS_E_NOMEM, "sample buffers");
+  auto done = [&](owqs_status st) {
+    cudaFree(d);
+    return st;
+  };
+  int64_t* d_idx = (int64_t*)d;
+  char* d_out = (char*)d + ib;
+  cudaError_t e = cudaMemcpyAsync(d_idx, idx, ib, cudaMemcpyHostToDevice, ctx->stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(d_out, 0, ob, ctx->stream);
+  for (size_t r = 0; e == cudaSuccess && r < ctx->shards.size(); ++r)
+    e = launch_sample_out(ctx->shards[r].d_state, ctx->prec, d_idx, (uint64_t)n, nbo, pr.out_slot.data(),
+                          (uint64_t)ctx->shard_rank((int)r), wl, d_out, ctx->stream);
+  if (e != cudaSuccess) return done(fail(ctx, OWQS_E_CUDA, cudaGetErrorString(e)));
+  if (ctx->n_ranks > 1 && !ctx->loopback &&
+      ncclAllReduce(d_out, d_out, (size_t)n * 2, ncclDouble, ncclSum, ctx->comm, ctx->stream) != ncclSuccess)
+    return done(fail(ctx, OWQS_E_NCCL, "all-reduce of the output samples"));
+  e = cudaMemcpyAsync(amps, d_out, ob, cudaMemcpyDeviceToHost, ctx->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return done(fail(ctx, OWQS_E_CUDA, cudaGetErrorString(e)));
+  return done(OWQS_OK);
 }
 
 owqs_status owqs_output_norm(owqs_ctx* ctx, double* norm2) {

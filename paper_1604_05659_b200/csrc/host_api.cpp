@@ -50,7 +50,8 @@ owqs_status owqs_host_compile(const int32_t* inputs, int32_t n_in, const int32_t
   if (flags & OWQS_FLAG_NO_TUNE) w.tune = false;
   plan_and_compile(h->hp, mode, precision == 64 ? 6 : 5, !(flags & OWQS_FLAG_NO_FUSE),
                    (flags & OWQS_FLAG_GIVEN_ORDER) != 0, w, h->plan, h->prog, n_global,
-                   jit_max_group(precision == 64 ? 0 : 1, (flags & OWQS_FLAG_NO_JIT) != 0));
+                   jit_max_group(precision == 64 ? 0 : 1, (flags & OWQS_FLAG_NO_JIT) != 0),
+                   (flags & OWQS_FLAG_MEASURED_NORM) != 0);
   h->elem = precision == 64 ? 8 : 16;
   h->mode = mode;
   h->precision = precision;
@@ -82,7 +83,8 @@ owqs_status owqs_host_substates(const owqs_host_plan* h, int32_t* n, uint64_t* m
       Program pr;
       plan_and_compile(parts[c], h->mode, h->precision == 64 ? 6 : 5, !(h->flags & OWQS_FLAG_NO_FUSE),
                        (h->flags & OWQS_FLAG_GIVEN_ORDER) != 0, h->w, pl, pr, 0,
-                       jit_max_group(h->precision == 64 ? 0 : 1, (h->flags & OWQS_FLAG_NO_JIT) != 0));
+                       jit_max_group(h->precision == 64 ? 0 : 1, (h->flags & OWQS_FLAG_NO_JIT) != 0),
+                       (h->flags & OWQS_FLAG_MEASURED_NORM) != 0);
       if (!pr.error.empty()) return OWQS_E_ARG;
       phys_bits[c] = pr.phys_bits;
     }

@@ -60,17 +60,6 @@ static __device__ __forceinline__ u64 sub2(u64 a, u64 b) { u64 r; asm("sub.rn.f3
 static __device__ __forceinline__ u64 shfl2(u64 x, int m) { return pk(__shfl_xor_sync(0xffffffffu, lo(x), m), __shfl_xor_sync(0xffffffffu, hi(x), m)); }
 static __device__ __forceinline__ u64 neg2(u64 x) { return pk(-lo(x), -hi(x)); }
 static __device__ __forceinline__ u64 flip2(u64 x, unsigned f) { return x ^ (((u64)f << 63) | ((u64)f << 31)); }
-static __device__ __forceinline__ void mbar_init(unsigned a, unsigned n) { asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(a), "r"(n) : "memory"); }
-static __device__ __forceinline__ void mbar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-static __device__ __forceinline__ void mbar_expect_tx(unsigned a, unsigned tx) { asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(a), "r"(tx) : "memory"); }
-static __device__ __forceinline__ void mbar_wait(unsigned a, unsigned par) {
-  unsigned done;
-  do { asm volatile("{ .reg .pred P1; mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2; selp.b32 %0, 1, 0, P1; }" : "=r"(done) : "r"(a), "r"(par) : "memory"); } while (!done);
-}
-static __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(dst), "l"(src), "r"(bytes), "r"(mbar) : "memory");
-}
-static __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 static __device__ __forceinline__ double fld(double x, unsigned f) { return __longlong_as_double(__double_as_longlong(x) ^ ((unsigned long long)f << 63)); }
 )OWQS";
 
@@ -426,6 +415,10 @@ struct Gen {
   }
   std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
 
+  static bool pdl_prefetch() {
+    static const bool v = !(getenv("OWQS_PDL_PREFETCH") && atoi(getenv("OWQS_PDL_PREFETCH")) == 0);
+    return v;
+  }
   static int prefetch_distance() {
     // 13-bit tiles (2 CTAs per SM): one wave ahead, 148 x 2, measured C3 49.8 -> 49.3 ms, C3W 219 ->
     // 213 ms. 12-bit tiles (4 CTAs per SM, default): off -- the extra resident CTAs already hide the
@@ -1449,14 +1442,6 @@ struct Gen {
       << "  for (unsigned it = 0; it < " << iters << "u; ++it) {\n"
       << "    const unsigned long long ub = (unsigned long long)blockIdx.x * " << iters << "ull + it;\n";
     emit_gb("gb0", "ub");
-    if (prec == 0)
-      for (int q = 0; q < P; q += 2)
-        o << "    u64 x" << q << ", x" << q + 1 << "; { const float4 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
-          << "ull) << 5) + lane_ld)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
-    else
-      for (int q = 0; q < P; ++q)
-        o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
-          << "ull) << 5) + lane_ld)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
     // L2 prefetch of the tile the CTA one wave later (blockIdx + D, D ~ resident CTAs) will load:
     // lane m < 16 of each warp bulk-prefetches that warp's m-th 512 B segment there, so the next
     // wave's load phase hits L2 instead of waiting on HBM (OWQS_PREFETCH=D; no extra DRAM bytes)
@@ -1470,9 +1455,29 @@ struct Gen {
       o << ";\n    asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], 512;\" :: \"l\"(st + ((gbp | wsl | ap) << 5)) : \"memory\");\n"
         << "    } }\n";
     }
-    // launched right behind decide_kernel (programmatic dependent launch): the loads above overlap
-    // the decisions; wait for them before the first read of PassCoef
-    if (!small) o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    // Launched with programmatic stream serialisation behind decide_kernel (or, with cached EOWQS
+    // decisions, behind the previous pass): PTX guarantees the prerequisite grid's stores only
+    // after griddepcontrol.wait, so every read of the state (and of PassCoef) comes after it. Before
+    // the wait, lane m < 16 of each warp bulk-prefetches its m-th 512 B load segment into L2 -- L2
+    // is the point of coherence, so a prefetched line can never be older than the writer's store
+    // (OWQS_PDL_PREFETCH=0: off).
+    if (!small) {
+      if (pdl_prefetch()) {
+        o << "    if (lane < 16) {\n      const unsigned long long ap = 0ull";
+        for (int k = 0; k < 4; ++k)
+          o << " | ((lane & " << (1 << k) << ") ? " << a_seg(l_load, prec == 0 ? 2 << k : 1 << k) << "ull : 0ull)";
+        o << ";\n      asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], 512;\" :: \"l\"(st + ((gb0 | wsl | ap) << 5)) : \"memory\");\n    }\n";
+      }
+      o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
+    }
+    if (prec == 0)
+      for (int q = 0; q < P; q += 2)
+        o << "    u64 x" << q << ", x" << q + 1 << "; { const float4 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
+          << "ull) << 5) + lane_ld)); x" << q << " = pk(w.x, w.y); x" << q + 1 << " = pk(w.z, w.w); }\n";
+    else
+      for (int q = 0; q < P; ++q)
+        o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
+          << "ull) << 5) + lane_ld)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
     if (nbf > 0 && prec == 0) o << "    const float sck = (float)pc->scale;\n    const u64 scale = bc(sck); (void)scale;\n";
     if (nbf > 0 && prec == 1) o << "    const double sck = pc->scale;\n    const double scale = sck; (void)scale;\n";
     lay = l_load;
@@ -1715,7 +1720,7 @@ std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
       if ((tf && atoi(tf) == 1) || (transposes_of(b2) < transposes_of(body) && smem2 <= smem1)) body = b2;
     }
   }
-  const std::string nm = std::string(eng == 2 ? "owqs_tma_" : "owqs_pass_") + (prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
+  const std::string nm = std::string(eng == 2 ? "owqs_tile_" : "owqs_pass_") + (prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
   const std::string key = "OWQS_KNAME";
   body.replace(body.find(key), key.size(), nm);
   if (name) *name = nm;

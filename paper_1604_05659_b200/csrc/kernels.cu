@@ -995,8 +995,10 @@ int max_partial_blocks() { return RED_MAX_BLOCKS + RED_MAX_GROUPS; }
 
 // Decisions of one pass for the generated pass kernels (one warp; PassCoef read by every CTA).
 __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevPtrs p, PassCoef* pc, int trigger) {
-  // the pass kernel that follows is launched with programmatic stream serialisation: let it start
-  // (it issues its state loads, then griddepcontrol.wait-s for this grid before reading pc)
+  // the pass kernel that follows is launched with programmatic stream serialisation: let its CTAs
+  // become resident now (they L2-prefetch their tile, then griddepcontrol.wait for this grid before
+  // any read of the state or of pc; this grid in turn completes only after its own wait below, so
+  // the previous pass's stores are visible to the pass kernel transitively)
   if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // launched behind grid_finish_kernel with programmatic serialisation too: wait for the previous
   // grid (the reduction this pass decides from) before reading anything it wrote
@@ -1251,6 +1253,34 @@ cudaError_t launch_permute_out(const void* state, int prec, void* out, int out_p
   return cudaGetLastError();
 }
 
+// owqs_get_output_sample: out[i] = output amplitude idx[i] (caller order, bit k <-> outputs[k]) for
+// the samples this shard owns (global state index G = sum_k bit_k(idx) << slot[k], owned when
+// G >> wl == rank); others are left untouched (the caller zero-fills and sums over ranks).
+template <typename T>
+__global__ void sample_out_kernel(const void* shard, const int64_t* idx, uint64_t n, int nbits, PermTab tab,
+                                  uint64_t rank, int wl, double2* out) {
+  typedef typename VT<T>::C C;
+  const C* st = reinterpret_cast<const C*>(shard);
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t y = (uint64_t)idx[i];
+    uint64_t G = 0;
+    for (int k = 0; k < nbits; ++k) G |= ((y >> k) & 1ull) << tab.slot[k];
+    if ((G >> wl) != rank) continue;
+    const C v = st[G & ((1ull << wl) - 1)];
+    out[i] = make_double2((double)v.x, (double)v.y);
+  }
+}
+
+cudaError_t launch_sample_out(const void* shard, int prec, const int64_t* idx, uint64_t n, int nbits, const int* slots,
+                              uint64_t rank, int wl, void* out, cudaStream_t s) {
+  PermTab t;
+  for (int k = 0; k < 64; ++k) t.slot[k] = (int8_t)(k < nbits ? slots[k] : 0);
+  const unsigned b = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(1024, (n + 255) / 256));
+  if (prec == 0) sample_out_kernel<float><<<b, 256, 0, s>>>(shard, idx, n, nbits, t, rank, wl, (double2*)out);
+  else sample_out_kernel<double><<<b, 256, 0, s>>>(shard, idx, n, nbits, t, rank, wl, (double2*)out);
+  return cudaGetLastError();
+}
+
 // Tensor merge of sub-states (PAPER §4.1: "two different sub-states are combined only
 // when ..."; the reported output is their tensor product): out[i] = prod_c f_c[pext(i, mask_c)],
 // where factor c holds the amplitudes of the output bits set in mask_c (bit k of its index <-> the
@@ -1347,6 +1377,30 @@ __global__ void __launch_bounds__(256) norm_kernel(DevPtrs p, uint64_t n) {
 cudaError_t launch_norm(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s) {
   if (prec == 0) norm_kernel<float><<<elem_blocks(n), 256, 0, s>>>(p, n);
   else norm_kernel<double><<<elem_blocks(n), 256, 0, s>>>(p, n);
+  return cudaGetLastError();
+}
+
+// Caller input into a shard with its norm^2 in the same sweep (owqs_set_input_device, same
+// precision): state[i] = src[i], red_result[0] = sum |src[i]|^2 (fp64). The structural decisions take
+// ||psi||^2 = 1 (DESIGN R-13, Eq. 3-4 / P:L105-109), so the library checks it on every input.
+template <typename T>
+__global__ void __launch_bounds__(256) copy_norm_kernel(DevPtrs p, const void* src, uint64_t n) {
+  typedef typename VT<T>::C C;
+  __shared__ PassShared sh;
+  const C* x = reinterpret_cast<const C*>(src);
+  C* st = reinterpret_cast<C*>(p.state);
+  double acc[4] = {0, 0, 0, 0};
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const C v = __ldcs(x + i);
+    __stcs(st + i, v);
+    acc[0] += (double)v.x * v.x + (double)v.y * v.y;
+  }
+  reduce_finish<1>(acc, p, sh);
+}
+
+cudaError_t launch_copy_norm(const DevPtrs& p, int prec, const void* src, uint64_t n, cudaStream_t s) {
+  if (prec == 0) copy_norm_kernel<float><<<elem_blocks(n), 256, 0, s>>>(p, src, n);
+  else copy_norm_kernel<double><<<elem_blocks(n), 256, 0, s>>>(p, src, n);
   return cudaGetLastError();
 }
 

@@ -634,6 +634,7 @@ struct Packer {
   // deferred lane work lands in passes with idle issue slots (L2-resident states are launch-bound:
   // no cap, fewest passes)
   int max_lane_bfly = -1;
+  bool measured_norm = false;  // OWQS_FLAG_MEASURED_NORM: structural decisions from a reduced ||psi||^2
   const int n_global;         // log2(ranks); positions >= width - n_global are rank bits
   std::vector<int> pos, at;   // virtual slot -> physical position, and back
 
@@ -980,12 +981,13 @@ struct Packer {
         at[pos[g]] = g;
         continue;
       }
-      // a structural first decision of a pass uses ||psi||^2 = 1, its exact value (the input is
-      // normalised by contract and every measurement renormalises by 1/sqrt(p_s)), instead of a norm
-      // reduced by the previous pass (reading R-13; OWQS_NORM1=0 restores the reduction): C3 43.1 ->
-      // 41.8 ms, C2 0.72 -> 0.62 ms. The output's norm is still reduced by the last pass.
-      static const bool norm1 = !(getenv("OWQS_NORM1") && atoi(getenv("OWQS_NORM1")) == 0);
-      if (cur.first_uses_red && (norm1 || !need_norm_before())) cur.first_uses_red = 0;
+      // a structural first decision of a pass uses ||psi||^2 = 1, its exact value, instead of a norm
+      // reduced by the previous pass (reading R-13): the input is normalised (enforced by every
+      // owqs_set_input_*), a structural measurement's p_s = 1/2 ||psi||^2 = 1/2 and a SHRINK's
+      // measured p_s both renormalise by 1/sqrt(p_s) (Eq. 4), so ||psi||^2 = 1 holds by induction.
+      // C3 43.1 -> 41.8 ms, C2 0.72 -> 0.62 ms. The output's norm is still reduced by the last pass.
+      // OWQS_FLAG_MEASURED_NORM keeps the reduction (tests check the reading with it at full width).
+      if (cur.first_uses_red && (!measured_norm || !need_norm_before())) cur.first_uses_red = 0;
       absorb_and_flush(cur);
       if (remap && wide) plan_remap(cur, nodes);
       emit(cur);
@@ -1053,7 +1055,7 @@ struct Packer {
 }  // namespace
 
 Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int SB, bool fuse, int n_global,
-                        int kwide) {
+                        int kwide, bool measured_norm) {
   const bool eowqs = mode == 2;
   Emitter em(hp, eowqs);
   em.run(plan);
@@ -1075,6 +1077,7 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
     }
   }
   Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1, n_global);
+  pk.measured_norm = measured_norm;
   pk.kwide = std::max(KMAX_AOT, std::min(KTILE, kwide));
   if (const char* env = getenv("OWQS_MAX_BFLY")) pk.max_bfly = std::max(1, std::min(MAX_BFLY, atoi(env)));
   {
@@ -1094,14 +1097,14 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
 }
 
 void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool given, const ProaWeights& w,
-                      Plan& plan, Program& prog, int n_global, int kwide) {
+                      Plan& plan, Program& prog, int n_global, int kwide, bool measured_norm) {
   if (mode != 2) {
     plan = make_plan(hp, false, given, w);
-    prog = compile_program(hp, plan, mode, SB, fuse, n_global, kwide);
+    prog = compile_program(hp, plan, mode, SB, fuse, n_global, kwide, measured_norm);
     return;
   }
   plan = make_plan(hp, true, given, w);
-  prog = compile_program(hp, plan, 2, SB, fuse, n_global, kwide);
+  prog = compile_program(hp, plan, 2, SB, fuse, n_global, kwide, measured_norm);
   Plan alt = make_plan(hp, false, given, w);
   Plan filt;
   for (int c : alt.order)
@@ -1109,7 +1112,7 @@ void plan_and_compile(const HostPattern& hp, int mode, int SB, bool fuse, bool g
   filt.m_cmds = alt.m_cmds;
   filt.ms = alt.ms;
   filt.paper_m = alt.paper_m;
-  Program ap = compile_program(hp, filt, 2, SB, fuse, n_global, kwide);
+  Program ap = compile_program(hp, filt, 2, SB, fuse, n_global, kwide, measured_norm);
   if (!prog.error.empty() ||
       (ap.error.empty() && (ap.phys_bits < prog.phys_bits ||
                             (ap.phys_bits == prog.phys_bits && ap.n_passes + ap.n_swaps < prog.n_passes + prog.n_swaps)))) {

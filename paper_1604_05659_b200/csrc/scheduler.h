@@ -75,14 +75,17 @@ struct Program {
 // mode: 0 sampled / 1 forced (OWQS) or 2 EOWQS. seg_bits: 6 for complex64, 5 for complex128.
 // kwide: group slots per pass for passes of width >= 13 (complex64 tile engine, up to KMAX_HI);
 // narrower passes and the ahead-of-time kernels use KMAX_AOT.
+// measured_norm (OWQS_FLAG_MEASURED_NORM): structural decisions reduce ||psi||^2 in the previous pass
+// instead of taking its exact value 1 (reading R-13) -- a device-measured check of that reading.
 Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int seg_bits, bool fuse,
-                        int n_global = 0, int kwide = KMAX_AOT);
+                        int n_global = 0, int kwide = KMAX_AOT, bool measured_norm = false);
 
 // Plan + compile for a mode. For EOWQS two candidates are compiled — PROA without dependencies
 // and the OWQS plan with its (identity) corrections dropped — and the one with the
 // smaller physical width, then fewer passes, is kept.
 void plan_and_compile(const HostPattern& hp, int mode, int seg_bits, bool fuse, bool given_order,
-                      const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0, int kwide = KMAX_AOT);
+                      const ProaWeights& w, Plan& plan, Program& prog, int n_global = 0, int kwide = KMAX_AOT,
+                      bool measured_norm = false);
 
 // Standard form N* E* M* C* of a validated pattern (standardize.cpp); with
 // signal_shift, t-domains are removed and returned per measured qubit in `shift` (new labels).

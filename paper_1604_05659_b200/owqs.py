@@ -213,6 +213,14 @@ class Simulator:
     def get_output_device(self, ptr: int, precision: int, n: int):
         self._check(self._lib.owqs_get_output_device(self._h, C.c_void_p(ptr), precision, n))
 
+    def get_output_sample(self, idx) -> np.ndarray:
+        """Output amplitudes at caller-order indices idx (owqs_get_output_sample; collective)."""
+        idx = np.ascontiguousarray(idx, dtype=np.int64)
+        out = np.zeros(idx.size, dtype=np.complex128)
+        self._check(self._lib.owqs_get_output_sample(self._h, idx.ctypes.data_as(C.POINTER(C.c_int64)), idx.size,
+                                                     out.ctypes.data_as(C.POINTER(C.c_double))))
+        return out
+
     def norm2(self) -> float:
         v = C.c_double()
         self._check(self._lib.owqs_output_norm(self._h, C.byref(v)))

@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1604_05659_b200 import Simulator
+from paper_1604_05659_b200 import FLAG_MEASURED_NORM, Simulator
 from parity_util import check, fidelity, TOL
 from workloads import patterns as W
 from workloads.inputs import haar_state
@@ -68,7 +68,7 @@ def test_config4_full_width_invariants(require_gpu):
     up to the branch phase (outcome independence of a J/CZ circuit pattern)."""
     p = W.config_pattern("C4", seed=1)
     s = Simulator(precision=64)
-    t = Simulator(precision=64)
+    t = Simulator(precision=64, flags=FLAG_MEASURED_NORM)  # structural prob0 reduced on the device
     try:
         for x in (s, t):
             x.load(p)
@@ -77,6 +77,7 @@ def test_config4_full_width_invariants(require_gpu):
         assert abs(s.norm2() - 1.0) < 1e-3
         outc, p0 = t.run("sampled", seed=5)
         assert np.max(np.abs(p0 - 0.5)) < 1e-5
+        assert abs(t.norm2() - 1.0) < 1e-5
         assert 0 < int(outc.sum()) < len(outc)  # a genuinely mixed branch
         ov = s.inner(t)
         assert 1.0 - abs(ov) ** 2 < 1e-4

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle
-from paper_1604_05659_b200 import FLAG_LOOPBACK, Simulator
+from paper_1604_05659_b200 import FLAG_LOOPBACK, FLAG_MEASURED_NORM, Simulator
 from parity_util import TOL, check, fidelity
 from workloads import patterns as W
 from workloads.inputs import haar_state
@@ -60,7 +60,7 @@ def test_loopback_cluster_outcome_independence(require_gpu):
     """Config 5 family sharded (26 x 8 cluster, fp64, 8 virtual ranks): EOWQS equals random forced
     branches up to a global phase, every prob0 = 1/2, norm 1."""
     p = W.config_pattern("CL:26x8", seed=1)
-    a = Simulator(precision=128, flags=FLAG_LOOPBACK, n_ranks=8)
+    a = Simulator(precision=128, flags=FLAG_LOOPBACK | FLAG_MEASURED_NORM, n_ranks=8)
     try:
         a.load(p)
         a.set_input_random(3)

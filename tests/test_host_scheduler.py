@@ -193,7 +193,7 @@ def test_substate_split_host():
     assert sum(masks) == (1 << len(p.outputs)) - 1 and all(a & b == 0 for a in masks for b in masks if a is not b)
     # the inputs' circuit (4 wires) is sub-state 0; the cluster (3 rows) and the lone |+> follow
     assert masks[0] == 0b10100101 and masks[2] == 0b00001000
-    assert [b for _, b in parts] == [4, 3, 1] or max(b for _, b in parts) <= 4
+    assert [b for _, b in parts] == [4, 3, 1]
     assert max(b for _, b in parts) < compile_host(p, "sampled", 64).info["phys_bits"]
     ci, co, cc = fragment(W.config_pattern("BW:3x2", seed=2), 0, True)
     cross = W.Pattern(ci, co + [501], cc + [W.N(500), W.N(501), W.E(500, 501), W.M(500, 0.4, sdom=(ci[0],))])

@@ -146,3 +146,21 @@ def test_other_tile_sizes_generate_conflict_free(g):
     bad, tot, threads = out.stdout.split(" ", 2)
     assert int(bad) == 0 and int(tot) > 0
     assert str(32 << (int(g) - 4)) in threads
+
+
+@pytest.mark.parametrize("shape,prec", [("C3", 64), ("BW:16x6", 128)])
+def test_tile_kernels_read_state_after_pdl_wait(shape, prec):
+    """Tile kernels are launched with programmatic stream serialisation; PTX makes the prerequisite
+    grid's stores visible only after griddepcontrol.wait, so no state load (or PassCoef read) may
+    precede it -- only L2 bulk prefetches (L2 is the point of coherence)."""
+    r = jit_host(W.config_pattern(shape, seed=3), "sampled", prec, sources=True)
+    n = 0
+    for k, s in r["sources"].items():
+        if k < 0 or "tile engine" not in s:
+            continue
+        body = s[s.index("__global__"):]
+        w = body.find("griddepcontrol.wait")
+        assert w > 0
+        assert "__ldcs(" not in body[:w] and "pc->" not in body[:w].split("// pc:")[-1].split("\n", 1)[-1]
+        n += 1
+    assert n > 0

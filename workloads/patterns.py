@@ -184,6 +184,29 @@ def brickwork_circuit(n: int, depth: int, seed: int) -> List[tuple]:
     return gates
 
 
+def prefix_pattern(pattern: Pattern, k_cmds: int) -> Pattern:
+    """The first k commands of `pattern` (given order) as a pattern of their own: same inputs, the
+    outputs are the qubits live after them (prepared and not measured), in order of preparation.
+    Used for full-width parity on a prefix (both sides run the same command list)."""
+    cmds = list(pattern.cmds[:k_cmds])
+    live = list(pattern.inputs)
+    for c in cmds:
+        if c.kind == KIND_N:
+            live.append(c.q0)
+        elif c.kind == KIND_E:
+            for q in (c.q0, c.q1):
+                if q not in live:
+                    live.append(q)  # implicit N (reading R-11)
+        elif c.kind == KIND_M:
+            live.remove(c.q0)
+    return Pattern(list(pattern.inputs), live, cmds, pattern.name + f"[:{k_cmds}]")
+
+
+def brickwork_layer_cmds(n: int, layers: int) -> int:
+    """Commands in the first `layers` layers of an n-wire brickwork pattern (4 per J, 1 per CZ)."""
+    return sum(4 * n + len(range(l % 2, n - 1, 2)) for l in range(layers))
+
+
 # --------------------------------------------------------------------------------------------
 # Patterns printed or implied by the paper
 # --------------------------------------------------------------------------------------------
@@ -371,3 +394,58 @@ def random_general_pattern(seed: int, n_in: int = 2, n_total: int = 9, n_out: in
         if d and rng.uniform() < 0.5:
             cmds.append((X if rng.uniform() < 0.5 else Z)(q, d))
     return Pattern(inputs, outputs, cmds, f"random{seed}")
+
+
+def wide_random_pattern(seed: int, n_in: int = 16, width_hi: int = 20, rounds: int = 4,
+                        n_out: int = 12) -> Pattern:
+    """A grow/shrink-heavy random pattern (rules D0-D3) at tile-engine widths: each round prepares
+    fresh qubits E-joined to two live qubits each (the state grows: GROW), entangles random live
+    pairs, then measures live qubits whose neighbours are all live (no fresh partner to absorb them:
+    SHRINK with the full (n0, n1, c) reduction of Eq. 13), with random angles, random s/t domains
+    over earlier outcomes and random X/Z corrections. Parity-test workload for the paths the
+    brickwork / cluster configs never take."""
+    rng = np.random.default_rng(seed)
+    live = list(range(n_in))
+    nxt = n_in
+    measured: List[int] = []
+    edges = set()
+    cmds: List[Cmd] = []
+    outputs: List[int] = []
+
+    def dom():
+        if not measured or rng.uniform() < 0.3:
+            return ()
+        k = int(rng.integers(1, min(3, len(measured)) + 1))
+        return tuple(int(x) for x in rng.choice(measured, size=k, replace=False))
+
+    def edge(a, b):
+        key = (min(a, b), max(a, b))
+        if a != b and key not in edges:
+            edges.add(key)
+            cmds.append(E(a, b))
+
+    for r in range(rounds):
+        while len(live) < width_hi:
+            q = nxt
+            nxt += 1
+            cmds.append(N(q))
+            for a in rng.choice(live, size=2, replace=False):
+                edge(int(a), q)
+            live.append(q)
+        for _ in range(width_hi // 2):
+            a, b = (int(x) for x in rng.choice(live, size=2, replace=False))
+            edge(a, b)
+        for q in rng.choice(live, size=3, replace=False):
+            d = dom()
+            if d:
+                cmds.append((X if rng.uniform() < 0.5 else Z)(int(q), d))
+        last = r == rounds - 1
+        k = len(live) - n_out if last else int(rng.integers(3, 6))
+        cand = [q for q in live if q not in outputs]
+        for q in rng.choice(cand, size=k, replace=False):
+            q = int(q)
+            cmds.append(M(q, float(rng.uniform(0, 2 * math.pi)), sdom=dom(), tdom=dom()))
+            measured.append(q)
+            live.remove(q)
+    outputs = list(live)
+    return Pattern(list(range(n_in)), outputs, cmds, f"WR:{seed}:{n_in}:{width_hi}")
