@@ -39,27 +39,39 @@ WORKLOADS = {
 }
 
 
+# oracle sample of the reference arm and of cpu_baseline (the same one): the pattern's first J gate
+# at full width -- N, E, M, X: one command of every kind the J/CZ workloads consist of except the
+# diagonal CZ (E is there), a measurement included (~15-20 s of numpy at 2^29 amplitudes)
+REF_CMDS = 4
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: C3 on one GPU; C4 sharded over the ranks (SURVEY §8(e)) for N > 1")
     ap.add_argument("--precision", type=int, default=64, choices=[64, 128])
     ap.add_argument("--flags", type=int, default=0, help="OWQS_FLAG_* for the timed context")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", action="store_true",
-                    help="with torchrun N > 1: shard ONE problem over the N ranks (NCCL swaps / all-reduce, "
-                         "strong scaling) instead of running N replicas")
+                    help="N > 1: shard ONE problem over the N ranks (NCCL swaps / all-reduce, strong scaling); "
+                         "the default for N > 1")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: every rank runs its own replica of the workload instead (weak scaling)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="no GPU: N ranks over gloo compile the sharded program of the workload and agree on "
+                         "its schedule; prints the JSON line shape with value null (CPU check of the N > 1 launch)")
     ap.add_argument("--loopback", type=int, default=1,
                     help="N = 1: shard the problem over this many virtual ranks on the one GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-contexts", type=int, default=3,
                     help="e2e serving pipeline depth: contexts (own state + stream) submitted round-robin")
     ap.add_argument("--ref-cmds", type=int, default=None,
-                    help="oracle sample: first k commands at full width (default 4 for cpu_baseline, "
-                         "2 per step for --impl reference so K+W steps finish in minutes)")
+                    help="oracle sample: first k commands at full width (default REF_CMDS = 4, one J gate, "
+                         "for both cpu_baseline and every --impl reference step)")
     return ap.parse_args()
 
 
@@ -132,18 +144,11 @@ class ClockSampler:
 def oracle_prefix_sample(pattern, psi, k_cmds, seed):
     """Run the oracle on the first k commands of `pattern` (full width). Returns (seconds, k)."""
     import oracle
-    from workloads.patterns import KIND_M, KIND_N, Pattern
-    cmds = pattern.cmds[:k_cmds]
-    live = list(pattern.inputs)
-    for c in cmds:
-        if c.kind == KIND_N:
-            live.append(c.q0)
-        elif c.kind == KIND_M:
-            live.remove(c.q0)
-    pre = Pattern(list(pattern.inputs), live, list(cmds), pattern.name + f"[:{k_cmds}]")
+    from workloads.patterns import prefix_pattern
+    pre = prefix_pattern(pattern, k_cmds)
     t0 = time.perf_counter()
     oracle.run(pre, psi, mode="sampled", seed=seed)
-    return time.perf_counter() - t0, len(cmds)
+    return time.perf_counter() - t0, len(pre.cmds)
 
 
 def peaks():
@@ -176,9 +181,9 @@ def run_reference(args, rank, world):
     n = len(pattern.inputs)
     psi = haar_state(n, 1)
     times = []
-    k = args.ref_cmds or 2
+    k = args.ref_cmds or REF_CMDS
     for s in range(args.warmup + args.steps):
-        dt, k = oracle_prefix_sample(pattern, psi, args.ref_cmds or 2, seed=s)
+        dt, k = oracle_prefix_sample(pattern, psi, k, seed=s)
         if s >= args.warmup:
             times.append(dt)
     t = sum(times)
@@ -354,7 +359,16 @@ def run_ours(args, rank, world, local_rank):
     n_cmd = st["n_commands"]
     problems = 1 if shard else world  # replicas each run the whole pattern
     value = problems * n_cmd * args.steps / (ms / 1e3)
-    hbm_gbs = st["bytes_per_run"] * (1 if shard else 1) / (ms_per_step / 1e3) / 1e9  # per GPU
+    hbm_gbs = st["bytes_per_run"] / (ms_per_step / 1e3) / 1e9  # per GPU (passes + swap pack / unpack)
+    hbm_agg = None
+    if shard:
+        # SURVEY §8(d) 8-GPU fraction: sum over ranks of (pass bytes + swap pack / unpack + the NCCL send
+        # and receive of half a shard per swap) over (time x ranks x peak), the collectives included in
+        # the timed region; every rank moves the same bytes
+        shard_bytes = (2 ** st["phys_bits"] >> (world.bit_length() - 1)) * (8 if prec == 64 else 16)
+        per_rank = st["bytes_per_run"] + st["n_swaps"] * shard_bytes
+        hbm_agg = {"bytes_per_rank_per_run": per_rank, "swaps_per_run": st["n_swaps"],
+                   "gbs_per_gpu": per_rank / (ms_per_step / 1e3) / 1e9}
 
     # ---- roofline of the dominant kernel: per-launch CUDA events over profiled runs ----
     # A state pass moves 2S bytes (S = 2^w amplitudes x 8/16 B; S for a read-only reduction pass) and
@@ -509,7 +523,7 @@ def run_ours(args, rank, world, local_rank):
         if psi_host is None:
             psi_host = x.to(torch.complex128).cpu().numpy()
         psi_host = psi_host / np.linalg.norm(psi_host)
-        dt, k = oracle_prefix_sample(pattern, psi_host, args.ref_cmds or 4, seed=1)
+        dt, k = oracle_prefix_sample(pattern, psi_host, args.ref_cmds or REF_CMDS, seed=1)
         cpu = {"value": k / dt, "unit": "commands/s", "cores": 1, "kind": "oracle",
                "sample": f"oracle (numpy complex128, given order, single thread) on the first {k} commands "
                          f"of {args.workload} at full width ({n_in}->{n_in + 1} qubits): {dt:.1f} s",
@@ -536,6 +550,9 @@ def run_ours(args, rank, world, local_rank):
                    "input": "device counter-Haar per step" if (shard or big) else "resident copy per step",
                    "load_pattern_s": load_s, "schedule_ms": st["schedule_ms"]},
         "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / peak,
+        "hbm_aggregate": (dict(hbm_agg, frac=hbm_agg["gbs_per_gpu"] / peak, ranks=world,
+                               note="north star: >= 0.60 of the aggregate HBM roofline incl. swap traffic")
+                          if hbm_agg else None),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -548,11 +565,66 @@ def run_ours(args, rank, world, local_rank):
     return 0
 
 
+def spawn(args):
+    """python bench.py --gpus N (N > 1) outside torchrun: re-launch as N ranks on this node, the way the
+    driver does (torch.distributed.run, rendezvous on 127.0.0.1)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dry_run(args, rank, world):
+    """--dry-run (CPU, gloo): every rank compiles the workload's program sharded over `world` ranks
+    (include/owqs_host.h) and the ranks all-reduce its schedule (passes, swaps, bytes) -- the N > 1 launch
+    path without a GPU. No state is simulated: value is null."""
+    import torch
+    import torch.distributed as dist
+    from paper_1604_05659_b200.host import compile_host
+    if world > 1:
+        dist.init_process_group("gloo")
+    pattern, mode = pattern_for(args.workload)
+    hp = compile_host(pattern, "eowqs" if mode == "eowqs" else "sampled", args.precision, args.flags,
+                      n_ranks=world if world > 1 else 1)
+    mine = torch.tensor([hp.info["n_passes"], hp.info["n_swaps"], hp.info["phys_bits"]], dtype=torch.float64)
+    agree = True
+    if world > 1:
+        lo, hi = mine.clone(), mine.clone()
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX)
+        agree = bool(torch.equal(lo, hi))
+    if rank == 0:
+        print(json.dumps({
+            "metric": "pattern commands/s", "value": None, "unit": "commands/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == 64 else "f64", "data": "synthetic", "dry_run": True,
+            "config": {"workload": WORKLOADS[args.workload], "mode": mode, "parallelism": f"shard{world}",
+                       "phys_bits": hp.info["phys_bits"], "passes_per_run": hp.info["n_passes"],
+                       "swaps_per_run": hp.info["n_swaps"], "ranks_agree_on_schedule": agree,
+                       "backend": "gloo (CPU): schedule only, no kernels"}}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if agree else 1
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.workload is None:
+        args.workload = "C4" if world > 1 and not args.replicas else "C3"
+    if world > 1 and not args.replicas:
+        args.shard = True
+    if args.dry_run:
+        return dry_run(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
     if world > 1:

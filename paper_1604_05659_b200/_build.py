@@ -68,7 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         o = os.path.join(BUILD, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + hdrs):
-            out = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            # -rdc: decide_kernel updates graph kernel nodes through the device runtime (cudadevrt)
+            out = _run([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-rdc=true", "-Xcompiler", "-fPIC",
                         "-Xptxas", "-v", "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o])
             if verbose:
                 print(out)
@@ -84,8 +85,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                   f'-DOWQS_NVRTC_PATH="{NVRTC_LIB}"', "-c", s, "-o", o])
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xlinker", "--no-undefined",
-              "-L/usr/lib/x86_64-linux-gnu", "-lnccl",
+        _run([NVCC, *ARCH, "-shared", "-rdc=true", "-o", tmp, *objs, "-Xlinker", "--no-undefined",
+              "-L/usr/lib/x86_64-linux-gnu", "-lnccl", "-lcudadevrt",
               "-lpthread", "-ldl", "-lrt"])
         shutil.move(tmp, LIB)
     return LIB

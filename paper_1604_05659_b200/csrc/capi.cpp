@@ -41,8 +41,9 @@ cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_w
 cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
-                       cudaStream_t s);
-cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s);
+                       cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node);
+cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s,
+                          const cudaGraphDeviceNode_t* nodes, int n_nodes, size_t off);
 cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaStream_t s);
 cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base, int K, int n_batch, const void* in,
                          void* out, int n_in, int n_out, const int* out_slot, int phys, int prec, cudaStream_t s);
@@ -69,6 +70,14 @@ struct CompiledMode {
   std::vector<int> jit_blocks;
   int n_jit = 0;
   PassCoef* d_pc = nullptr;  // one decision block per step (engine-2 generated kernels)
+  // coefp: the tile kernels take the decisions as their by-value PassCoef parameter (DESIGN.md
+  // §5.1): in the captured graph decide_kernel writes it into the device-updatable kernel node(s)
+  // of its pass (handles in d_devnodes[step * shards + r], parameter offset coef_off[step]); the
+  // EOWQS mode's decisions are run-independent and set by the host at capture (static_cp)
+  bool coefp = false;
+  cudaGraphDeviceNode_t* d_devnodes = nullptr;
+  std::vector<size_t> coef_off;
+  std::vector<PassCoef> static_cp;
   // EOWQS: every decision is run-independent (outcomes 0, no signals, no probabilities, static
   // scales), so d_pc written by the first EOWQS run is reused and later runs launch no decide kernel
   bool pc_static_ready = false;
@@ -196,7 +205,40 @@ void free_mode(CompiledMode& m) {
   if (m.d_sig) cudaFree(m.d_sig);
   if (m.d_steps) cudaFree(m.d_steps);
   if (m.d_pc) cudaFree(m.d_pc);
+  if (m.d_devnodes) cudaFree(m.d_devnodes);
   m = CompiledMode();
+}
+
+// EOWQS decisions of one tile pass (every outcome 0, no probabilities; reading R-15: the
+// corrections are dropped, so every signal is 0 and Eq. 2 gives theta = alpha): what decide_kernel
+// computes in mode 2 (device_common.cuh pass_prologue), fixed by the pattern alone -- the butterfly
+// coefficient a = e^{-i alpha}, k = 1/sqrt2 per slot-reuse butterfly (1 for an elimination), the
+// pass scale = prod k, conditional ops off. Set once as the graph nodes' PassCoef parameter.
+void static_eowqs_coef(const StepDesc& d, const std::vector<MStatic>& mst, PassCoef& c) {
+  c = PassCoef{};
+  double scale = 1.0;
+  int b = 0;
+  for (int i = 0; i < d.n_ops; ++i) {
+    const Op& op = d.ops[i];
+    if (op.type != OP_BFLY) {
+      c.cond[i] = op.cond ? 0 : 1;
+      continue;
+    }
+    c.cond[i] = 1;
+    const MStatic& ms = mst[op.m];
+    const double ar = std::cos(ms.alpha), ai = -std::sin(ms.alpha);
+    scale *= ms.reuse ? 0.70710678118654752440 : 1.0;
+    c.ard[b] = ar;
+    c.aid[b] = ai;
+    c.ar[b] = (float)ar;
+    const float fai = (float)ai, nfai = -fai;
+    uint32_t uh, ul;
+    memcpy(&uh, &fai, 4);
+    memcpy(&ul, &nfai, 4);
+    c.B[b] = ((uint64_t)uh << 32) | ul;
+    ++b;
+  }
+  c.scale = scale;
 }
 
 void drop_graphs(owqs_ctx* ctx) {
@@ -234,7 +276,10 @@ owqs_status compile_modes(owqs_ctx* ctx) {
       for (size_t k = 0; k < m.prog.steps.size(); ++k) {
         if (!jit_eligible(m.prog.steps[k], ctx->prec)) continue;
         std::string nm;
-        std::string src = jit_pass_source(m.prog.steps[k], ctx->prec, &nm);
+        // graph launches (the default) take the decisions as kernel parameters; direct launches
+        // (OWQS_FLAG_NO_GRAPH) read them from the PassCoef pointer
+        m.coefp = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH) && !getenv("OWQS_COEF_POINTER");
+        std::string src = jit_pass_source(m.prog.steps[k], ctx->prec, &nm, m.coefp);
         if (src.empty()) return fail(ctx, OWQS_E_ARG, "pass kernel generation failed for step " + std::to_string(k));
         m.jit_name[k] = nm;
         ++m.n_jit;
@@ -300,6 +345,10 @@ owqs_status ensure_device(owqs_ctx* ctx) {
       CU(cudaMemcpy(m.d_sig, m.prog.sig_pool.data(), m.prog.sig_pool.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     if (m.n_jit > 0 && !m.d_pc) CU(cudaMalloc(&m.d_pc, m.prog.steps.size() * sizeof(PassCoef)));
+    if (m.n_jit > 0 && m.coefp && !m.d_devnodes) {
+      CU(cudaMalloc(&m.d_devnodes, m.prog.steps.size() * ctx->shards.size() * sizeof(cudaGraphDeviceNode_t)));
+      CU(cudaMemset(m.d_devnodes, 0, m.prog.steps.size() * ctx->shards.size() * sizeof(cudaGraphDeviceNode_t)));
+    }
     if (m.n_jit > 0 && m.jit_fn.empty()) {
       std::vector<cudaKernel_t> fn(m.prog.steps.size(), nullptr);
       std::vector<int> blocks(m.prog.steps.size(), 0);
@@ -335,6 +384,16 @@ owqs_status ensure_device(owqs_ctx* ctx) {
       for (size_t k = 0; k < m.jit_name.size(); ++k)
         if (!m.jit_name[k].empty() && !fn[k])
           return fail(ctx, OWQS_E_CUDA, "generated kernel " + m.jit_name[k] + " missing from its cubin");
+      m.coef_off.assign(m.prog.steps.size(), (size_t)-1);
+      m.static_cp.assign(i == 1 ? m.prog.steps.size() : 0, PassCoef{});
+      for (size_t k = 0; k < m.jit_name.size(); ++k) {
+        const StepDesc& sd = m.prog.steps[k];
+        if (!fn[k] || jit_engine(sd, ctx->prec) != 2 || jit_tile_small(sd, ctx->prec)) continue;
+        m.coef_off[k] = jit_coef_param_offset(fn[k]);
+        if (m.coefp && m.coef_off[k] == (size_t)-1)
+          return fail(ctx, OWQS_E_CUDA, "generated kernel " + m.jit_name[k] + ": no PassCoef parameter");
+        if (i == 1) static_eowqs_coef(sd, m.prog.mst, m.static_cp[k]);
+      }
       m.jit_fn = fn;
       m.jit_blocks = blocks;
     }
@@ -411,10 +470,18 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
     CU(cudaMemcpyAsync(ctx->d_forced, hf, ctx->hp.n_measure, cudaMemcpyHostToDevice, ctx->stream));
   }
   for (auto& s : ctx->shards) CU(cudaMemsetAsync(s.d_err, 0, sizeof(int32_t), ctx->stream));
-  // EOWQS after its first run: the decisions are already in d_pc (CompiledMode::pc_static_ready);
-  // the first run launches directly so that no captured graph contains the decide kernels
-  const bool static_pc = mode == OWQS_EOWQS && m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE");
+  // Decisions of the tile passes. coefp (graph launches): the sampled / forced graph's decide kernels
+  // write them into the device-updatable pass-kernel nodes; EOWQS's are run-independent and set by
+  // the host at capture, no decide kernel at all. Otherwise (OWQS_FLAG_NO_GRAPH) the kernels read
+  // d_pc; EOWQS after its first run reuses it (CompiledMode::pc_static_ready) -- that first run
+  // launches directly so that no captured graph contains the decide kernels.
+  const bool eowqs_static = mode == OWQS_EOWQS && m.coefp;
+  const bool static_pc = eowqs_static || (mode == OWQS_EOWQS && m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE"));
   const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH) && (mode != OWQS_EOWQS || static_pc);
+  const bool dev_update = m.coefp && !eowqs_static;  // sampled / forced graph: device node updates
+  const size_t NS = ctx->shards.size();
+  std::vector<cudaGraphDeviceNode_t> hnodes(dev_update ? m.prog.steps.size() * NS : 0, nullptr);
+  if (m.coefp && !use_graph) return fail(ctx, OWQS_E_STATE, "parameter-coefficient kernels need a CUDA graph");
   const bool prof = (ctx->cfg.flags & OWQS_FLAG_PROFILE) != 0;
   if (prof) {
     if (ctx->prof_cm != cmi && m.gexec) {  // event lists follow the compiled mode
@@ -443,10 +510,15 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
         const bool jit = !m.jit_fn.empty() && m.jit_fn[i];
         const int eng = jit ? jit_engine(s, ctx->prec) : 0;
         const bool small = eng == 2 && jit_tile_small(s, ctx->prec);
-        if (eng == 2 && !small && !static_pc) CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream));
+        const bool upd = dev_update && eng == 2 && !small;
+        if (eng == 2 && !small && !static_pc)
+          CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream, upd ? m.d_devnodes + i * NS : nullptr,
+                           upd ? (int)NS : 0, upd ? m.coef_off[i] : 0));
         for (size_t r = 0; r < ctx->shards.size(); ++r) {
           if (jit)
-            CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream));
+            CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream,
+                          (eowqs_static && eng == 2 && !small) ? &m.static_cp[i] : nullptr,
+                          (upd && capturing) ? &hnodes[i * NS + r] : nullptr));
           else
             CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
         }
@@ -475,6 +547,14 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
     CU(cudaStreamEndCapture(ctx->stream, &g));
     CU(cudaGraphInstantiate(&m.gexec, g, 0));
     cudaGraphDestroy(g);
+    if (dev_update) {
+      // handles of the device-updatable pass-kernel nodes for their decide kernels; a graph whose
+      // nodes are updated from the device must be uploaded before it is launched
+      CU(cudaMemcpyAsync(m.d_devnodes, hnodes.data(), hnodes.size() * sizeof(cudaGraphDeviceNode_t),
+                         cudaMemcpyHostToDevice, ctx->stream));
+      CU(cudaGraphUpload(m.gexec, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
   }
   CU(cudaEventRecord(ctx->ev0, ctx->stream));
   if (use_graph) {
@@ -512,6 +592,7 @@ owqs_status run_complete(owqs_ctx* ctx, int cmi) {
   int32_t herr = 0;
   for (size_t r = 0; r < ctx->shards.size(); ++r) herr |= ctx->h_err[r];
   ctx->has_output = true;
+  if (herr & 2) return fail(ctx, OWQS_E_CUDA, "device-side update of a pass kernel's graph node failed");
   if (herr) return fail(ctx, OWQS_E_BRANCH, "forced outcome on a branch with probability < 1e-12");
   if (cmi == 1) ctx->cm[1].pc_static_ready = true;  // the EOWQS mode's decisions are in d_pc
   return OWQS_OK;

@@ -269,8 +269,13 @@ struct Gen {
   std::vector<Pend> pend;
   std::string error;
 
-  Gen(const StepDesc& dd, int pr, bool use_tile, bool free_t0 = false)
+  // coefficient source of a tile kernel: "cp." = the kernel's by-value PassCoef parameter (constant
+  // bank: uniform-register FFMA2 / DFMA operands, written into the graph node by decide_kernel or by
+  // the host for EOWQS), "pc->" = the PassCoef decide_kernel wrote to global memory (registers)
+  std::string PC = "pc->";
+  Gen(const StepDesc& dd, int pr, bool use_tile, bool free_t0 = false, bool coefp = false)
       : d(dd), prec(pr), tile(use_tile), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1) {
+    if (coefp && use_tile) PC = "cp.";
     if (tile) {
       KHI = tile_g(pr);
       UNR = 1;
@@ -413,7 +418,7 @@ struct Gen {
     if (k == SK_BASE) return "((unsigned)(gb" + std::to_string(u) + " >> " + std::to_string(b) + ") & 1u)";
     return "((rk >> " + std::to_string(b) + ") & 1u)";
   }
-  std::string cond_expr(int i) const { return (tile ? "pc->cond[" : "sh.cond[") + std::to_string(i) + "]"; }
+  std::string cond_expr(int i) const { return (tile ? PC + "cond[" : std::string("sh.cond[")) + std::to_string(i) + "]"; }
 
   static bool pdl_prefetch() {
     static const bool v = !(getenv("OWQS_PDL_PREFETCH") && atoi(getenv("OWQS_PDL_PREFETCH")) == 0);
@@ -440,13 +445,13 @@ struct Gen {
     const bool fold = tile && scale_pending;
     if (fold) scale_pending = false;
     if (fold && prec == 0)
-      o << "      const float ar = pc->ar[" << bi << "] * sck; const u64 cB = mul2(pc->B[" << bi << "], bc(sck));  // scale folded\n";
+      o << "      const float ar = " << PC << "ar[" << bi << "] * sck; const u64 cB = mul2(" << PC << "B[" << bi << "], bc(sck));  // scale folded\n";
     else if (fold)
-      o << "      const double ar = pc->ard[" << bi << "] * sck, ai = pc->aid[" << bi << "] * sck;  // scale folded\n";
+      o << "      const double ar = " << PC << "ard[" << bi << "] * sck, ai = " << PC << "aid[" << bi << "] * sck;  // scale folded\n";
     else if (tile && prec == 0)
-      o << "      const float ar = pc->ar[" << bi << "]; const u64 cB = pc->B[" << bi << "];\n";
+      o << "      const float ar = " << PC << "ar[" << bi << "]; const u64 cB = " << PC << "B[" << bi << "];\n";
     else if (tile)
-      o << "      const double ar = pc->ard[" << bi << "], ai = pc->aid[" << bi << "];\n";
+      o << "      const double ar = " << PC << "ard[" << bi << "], ai = " << PC << "aid[" << bi << "];\n";
     else if (prec == 0)
       o << "      const float ar = s_ar[" << bi << "]; const u64 cB = s_B[" << bi << "];\n";
     else
@@ -1380,7 +1385,8 @@ struct Gen {
       choose_bank_classes(used);
     }
     o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* "
-      << (small ? "pc_global" : "pc") << ") {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
+      << (small ? "pc_global" : "pc") << ", const owqs::PassCoef cp) {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
+      << "  (void)cp;\n"
       << "  using namespace owqs;\n"
       << "  // tile engine: width " << d.width << ", tile group slots";
     for (int j = 0; j < KHI; ++j) o << " " << gs[j];
@@ -1478,8 +1484,8 @@ struct Gen {
       for (int q = 0; q < P; ++q)
         o << "    double xr" << q << ", xi" << q << "; { const double2 w = __ldcs(st + (((gb0 | wsl | " << a_seg(l_load, q)
           << "ull) << 5) + lane_ld)); xr" << q << " = w.x; xi" << q << " = w.y; }\n";
-    if (nbf > 0 && prec == 0) o << "    const float sck = (float)pc->scale;\n    const u64 scale = bc(sck); (void)scale;\n";
-    if (nbf > 0 && prec == 1) o << "    const double sck = pc->scale;\n    const double scale = sck; (void)scale;\n";
+    if (nbf > 0 && prec == 0) o << "    const float sck = (float)" << PC << "scale;\n    const u64 scale = bc(sck); (void)scale;\n";
+    if (nbf > 0 && prec == 1) o << "    const double sck = " << PC << "scale;\n    const double scale = sck; (void)scale;\n";
     lay = l_load;
     for (int q = 0; q < P; ++q) perm[q] = q;
     std::vector<int> bidx(d.n_ops, -1);
@@ -1701,10 +1707,11 @@ int transposes_of(const std::string& s) {
 }
 }  // namespace
 
-std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
+std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, bool coefp) {
   const int eng = jit_engine(d, prec);
   if (!eng) return "";
-  Gen g(d, prec, eng == 2);
+  coefp = coefp && eng == 2 && !jit_tile_small(d, prec);
+  Gen g(d, prec, eng == 2, false, coefp);
   if (!g.error.empty()) return "";
   std::string body = g.run();
   if (!g.error.empty()) return "";
@@ -1713,7 +1720,7 @@ std::string jit_pass_source(const StepDesc& d, int prec, std::string* name) {
   // OWQS_T0_FREE=0 / 1 forces it off / on for every pass
   const char* tf = getenv("OWQS_T0_FREE");
   if (eng == 2 && prec == 0 && !(tf && atoi(tf) == 0)) {
-    Gen g2(d, prec, true, true);
+    Gen g2(d, prec, true, true, coefp);
     std::string b2 = g2.error.empty() ? g2.run() : std::string();
     if (g2.error.empty() && !b2.empty()) {
       const int smem1 = count_of(body, "reinterpret_cast<"), smem2 = count_of(b2, "reinterpret_cast<");
@@ -1791,30 +1798,47 @@ std::string jit_compile(const std::vector<std::string>& names, const std::vector
   return "";
 }
 
+size_t jit_coef_param_offset(cudaKernel_t k) {
+  size_t off = 0, size = 0;
+  if (cudaFuncGetParamInfo((const void*)k, 3, &off, &size) != cudaSuccess || size != sizeof(PassCoef)) {
+    cudaGetLastError();
+    return (size_t)-1;
+  }
+  return off;
+}
+
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
-                       cudaStream_t s) {
+                       cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node) {
   const int eng = jit_engine(d, prec);
   const int SB = prec == 0 ? 6 : 5;
   const int unr = jit_unr_of(d.nb_hi);
   StepDesc dd = d;
   DevPtrs pp = p;
   const PassCoef* pcc = pc;
-  if (eng == 2) {  // non-persistent: one CTA per 13-bit tile (or iters tiles above RED_MAX_BLOCKS)
-    const uint64_t nbu = 1ull << (d.width - tile_bits(prec));
+  if (eng == 2) {  // non-persistent: one CTA per tile (or iters tiles above RED_MAX_BLOCKS)
+    static const PassCoef zero{};
+    PassCoef cp = cp_host ? *cp_host : zero;
     const uint64_t blocks = jit_tile_blocks(d, prec);  // the generator's tiles-per-CTA use the same count
-    (void)nbu;
-    void* args[] = {&dd, &pp, &pcc};
+    void* args[] = {&dd, &pp, &pcc, &cp};
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)blocks);
     cfg.blockDim = dim3(jit_block_threads(eng, prec));
     cfg.dynamicSmemBytes = (size_t)jit_dyn_smem(eng, prec);
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = (getenv("OWQS_NO_PDL") || jit_tile_small(d, prec)) ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelExC(&cfg, (const void*)k, args);
+    if (dev_node) {  // captured launch whose PassCoef parameter decide_kernel rewrites every run
+      attr[1].id = cudaLaunchAttributeDeviceUpdatableKernelNode;
+      attr[1].val.deviceUpdatableKernelNode.deviceUpdatable = 1;
+      attr[1].val.deviceUpdatableKernelNode.devNode = nullptr;
+      cfg.numAttrs = 2;
+    }
+    const cudaError_t e = cudaLaunchKernelExC(&cfg, (const void*)k, args);
+    if (dev_node) *dev_node = attr[1].val.deviceUpdatableKernelNode.devNode;
+    return e;
   }
   const int slack = d.width - SB - d.nb_hi - (unr == 4 ? 2 : (unr == 2 ? 1 : 0)) - 3;
   const uint64_t blocks = std::min<uint64_t>(1ull << slack, (uint64_t)std::max(1, max_blocks));

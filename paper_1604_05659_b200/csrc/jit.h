@@ -11,6 +11,8 @@
 
 #include <stdint.h>
 
+#include <cuda_runtime_api.h>
+
 #include <string>
 #include <vector>
 
@@ -41,8 +43,13 @@ unsigned jit_tile_blocks(const StepDesc& d, int prec);
 int jit_smem_carveout(int engine, int prec);
 
 // Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
-// a hash of the body (identical passes share one kernel).
-std::string jit_pass_source(const StepDesc& d, int prec, std::string* name);
+// a hash of the body (identical passes share one kernel). coefp: tile kernels read the pass's
+// decisions from their by-value PassCoef parameter (graph launches: decide_kernel writes it into the
+// device-updatable kernel node, the host for run-independent EOWQS decisions) instead of from the
+// PassCoef pointer (direct launches, OWQS_FLAG_NO_GRAPH).
+std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, bool coefp = true);
+// Byte offset of the by-value PassCoef parameter in a tile kernel's parameter buffer.
+size_t jit_coef_param_offset(cudaKernel_t k);
 
 // The common prelude every generated translation unit starts with.
 const std::string& jit_prelude();

@@ -878,6 +878,95 @@ __global__ void permute_out_kernel(const void* state, void* out, int nbits, Perm
   }
 }
 
+// Output permutation through shared-memory tiles (the whole output in one launch): out bit k <- state
+// bit slot[k]. A tile fixes every state bit outside TS = {state bits 0..4} u {slot[0..4]} (padded
+// with further low state bits to 10 bits); it is read in state order (TS's low bits are state bits
+// 0..4: 256 B runs per warp for complex64) and written in output order (its lowest output bits are
+// output bits 0..4: 256 B runs), so both sides are coalesced -- the per-element loop of
+// permute_out_kernel reads 32 scattered sectors per warp instead.
+constexpr int PERM_T = 10;
+struct PermPlan {
+  int8_t ts[PERM_T];     // tile bit j (e index) <- state position ts[j], ascending
+  int8_t fo[PERM_T];     // output-order bit i (f index) <- e bit fo[i]
+  int8_t op[PERM_T];     // ... at output position op[i], ascending
+  int8_t other[64];      // state positions outside the tile, ascending (tile id bits)
+  int8_t other_out[64];  // their output positions
+  int n_other;
+};
+
+template <typename T, typename TO>
+__global__ void __launch_bounds__(256) permute_out_tiled_kernel(const void* state, void* out, PermPlan pl, uint64_t n_tiles) {
+  typedef typename VT<T>::C C;
+  typedef typename VT<TO>::C CO;
+  __shared__ C tile[1 << PERM_T];
+  const C* st = reinterpret_cast<const C*>(state);
+  CO* o = reinterpret_cast<CO*>(out);
+  for (uint64_t tid = blockIdx.x; tid < n_tiles; tid += gridDim.x) {
+    uint64_t sb = 0, ob = 0;
+    for (int k = 0; k < pl.n_other; ++k) {
+      const uint64_t b = (tid >> k) & 1ull;
+      sb |= b << pl.other[k];
+      ob |= b << pl.other_out[k];
+    }
+#pragma unroll
+    for (int r = 0; r < (1 << PERM_T) / 256; ++r) {
+      const unsigned e = threadIdx.x + 256u * r;
+      uint64_t si = sb;
+#pragma unroll
+      for (int j = 0; j < PERM_T; ++j) si |= (uint64_t)((e >> j) & 1u) << pl.ts[j];
+      tile[e] = __ldcs(st + si);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < (1 << PERM_T) / 256; ++r) {
+      const unsigned f = threadIdx.x + 256u * r;
+      unsigned e = 0;
+      uint64_t oi = ob;
+#pragma unroll
+      for (int i = 0; i < PERM_T; ++i) {
+        const unsigned b = (f >> i) & 1u;
+        e |= b << pl.fo[i];
+        oi |= (uint64_t)b << pl.op[i];
+      }
+      const C v = tile[e];
+      __stcs(o + oi, make_c<TO>((TO)v.x, (TO)v.y));
+    }
+    __syncthreads();
+  }
+}
+
+// false when the slots are not a permutation of [0, nbits) or nbits < PERM_T (caller falls back)
+static bool make_perm_plan(int nbits, const int* slots, PermPlan& pl) {
+  if (nbits < PERM_T || nbits > 62) return false;
+  int o_of_s[64];
+  for (int k = 0; k < 64; ++k) o_of_s[k] = -1;
+  for (int k = 0; k < nbits; ++k) {
+    if (slots[k] < 0 || slots[k] >= nbits || o_of_s[slots[k]] >= 0) return false;
+    o_of_s[slots[k]] = k;
+  }
+  uint64_t m = 0;
+  for (int k = 0; k < 5; ++k) m |= (1ull << k) | (1ull << slots[k]);
+  for (int k = 0; k < nbits && __builtin_popcountll(m) < PERM_T; ++k) m |= 1ull << k;
+  int j = 0, q = 0;
+  for (int s = 0; s < nbits; ++s) {
+    if ((m >> s) & 1) pl.ts[j++] = (int8_t)s;
+    else {
+      pl.other[q] = (int8_t)s;
+      pl.other_out[q] = (int8_t)o_of_s[s];
+      ++q;
+    }
+  }
+  pl.n_other = q;
+  int idx[PERM_T];
+  for (int i = 0; i < PERM_T; ++i) idx[i] = i;
+  std::sort(idx, idx + PERM_T, [&](int a, int b) { return o_of_s[pl.ts[a]] < o_of_s[pl.ts[b]]; });
+  for (int i = 0; i < PERM_T; ++i) {
+    pl.fo[i] = (int8_t)idx[i];
+    pl.op[i] = (int8_t)o_of_s[pl.ts[idx[i]]];
+  }
+  return true;
+}
+
 template <typename TI, typename T>
 __global__ void convert_in_kernel(const void* src, void* state, uint64_t j0, uint64_t count) {
   typedef typename VT<TI>::C CI;
@@ -994,12 +1083,14 @@ cudaError_t init_kernel_limits(int device) {
 int max_partial_blocks() { return RED_MAX_BLOCKS + RED_MAX_GROUPS; }
 
 // Decisions of one pass for the generated pass kernels (one warp; PassCoef read by every CTA).
-__global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevPtrs p, PassCoef* pc, int trigger) {
+__global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevPtrs p, PassCoef* pc, int trigger,
+                                                    const cudaGraphDeviceNode_t* nodes, int n_nodes, unsigned long long off) {
   // the pass kernel that follows is launched with programmatic stream serialisation: let its CTAs
   // become resident now (they L2-prefetch their tile, then griddepcontrol.wait for this grid before
   // any read of the state or of pc; this grid in turn completes only after its own wait below, so
-  // the previous pass's stores are visible to the pass kernel transitively)
-  if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // the previous pass's stores are visible to the pass kernel transitively). When the decisions go
+  // into the pass kernel's parameters (graph node update, below) it may start only after them.
+  if (trigger && n_nodes == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // launched behind grid_finish_kernel with programmatic serialisation too: wait for the previous
   // grid (the reduction this pass decides from) before reading anything it wrote
   asm volatile("griddepcontrol.wait;" ::: "memory");
@@ -1016,6 +1107,22 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
   }
   for (int i = t; i < d.n_ops; i += 32) pc->cond[i] = sh.cond[i];
   if (t == 0) pc->scale = sh.scale;
+  if (n_nodes > 0) {
+    // the pass kernel node(s) of the captured graph (device-updatable, one per local shard) take the
+    // decisions as their by-value PassCoef parameter: constant-bank operands in the generated
+    // kernels. The update must be visible before the dependent launch is triggered.
+    __syncwarp();
+    __threadfence();
+    if (t == 0) {
+      for (int k = 0; k < n_nodes; ++k) {
+        const cudaError_t e = cudaGraphKernelNodeSetParam(nodes[k], (size_t)off, pc, sizeof(PassCoef));
+        if (e != cudaSuccess) atomicExch(p.err, 2);
+      }
+      __threadfence();
+    }
+    __syncwarp();
+    if (trigger) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  }
 }
 
 // Sum of the block partials of a tile pass (fixed order: deterministic) into red_result.
@@ -1075,12 +1182,14 @@ cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaSt
   return cudaGetLastError();
 }
 
-cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s) {
+cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s,
+                          const cudaGraphDeviceNode_t* nodes, int n_nodes, size_t off) {
   static const bool no_trigger = getenv("OWQS_PDL_NO_TRIGGER") != nullptr;
   static const bool no_pdl = getenv("OWQS_NO_PDL") != nullptr || getenv("OWQS_NO_DECIDE_PDL") != nullptr;
   const int trig = no_trigger ? 0 : 1;
+  const unsigned long long o = (unsigned long long)off;
   if (no_pdl) {
-    decide_kernel<<<1, 32, 0, s>>>(d, p, pc, trig);
+    decide_kernel<<<1, 32, 0, s>>>(d, p, pc, trig, nodes, n_nodes, o);
     return cudaGetLastError();
   }
   // programmatic serialisation behind the previous kernel (grid_finish_kernel triggers at its
@@ -1094,7 +1203,7 @@ cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cud
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, decide_kernel, d, p, pc, trig);
+  return cudaLaunchKernelEx(&cfg, decide_kernel, d, p, pc, trig, nodes, n_nodes, o);
 }
 
 static inline int unr_of(int khi) { return khi == 0 ? 4 : (khi == 1 ? 2 : 1); }
@@ -1243,6 +1352,16 @@ cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base
 
 cudaError_t launch_permute_out(const void* state, int prec, void* out, int out_prec, int nbits, const int* slots,
                                uint64_t j0, uint64_t count, cudaStream_t s) {
+  PermPlan pl;
+  if (j0 == 0 && count == (1ull << nbits) && !getenv("OWQS_PERMUTE_SCALAR") && make_perm_plan(nbits, slots, pl)) {
+    const uint64_t n_tiles = 1ull << (nbits - PERM_T);
+    const unsigned b = (unsigned)std::min<uint64_t>(n_tiles, (uint64_t)(g_lim_ready ? g_lim.sm_count * 8 : 1184));
+    if (prec == 0 && out_prec == 0) permute_out_tiled_kernel<float, float><<<b, 256, 0, s>>>(state, out, pl, n_tiles);
+    else if (prec == 0) permute_out_tiled_kernel<float, double><<<b, 256, 0, s>>>(state, out, pl, n_tiles);
+    else if (out_prec == 0) permute_out_tiled_kernel<double, float><<<b, 256, 0, s>>>(state, out, pl, n_tiles);
+    else permute_out_tiled_kernel<double, double><<<b, 256, 0, s>>>(state, out, pl, n_tiles);
+    return cudaGetLastError();
+  }
   PermTab t;
   for (int k = 0; k < 64; ++k) t.slot[k] = (int8_t)(k < nbits ? slots[k] : 0);
   unsigned b = elem_blocks(count);

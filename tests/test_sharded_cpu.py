@@ -86,10 +86,14 @@ def _worker(rank, world, port, cases, out_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_program_matches_oracle(world):
+    # config 4's shape (brickwork, sampled) and config 5's (flow cluster, EOWQS and forced) scaled to
+    # oracle size; world 8 = the 8-GPU split of SURVEY §8(e) (3 rank bits)
     cases = [("BW:14x6", 3, "sampled", 128), ("BW:15x4", 4, "eowqs", 64), ("CL:13x4", 5, "forced", 128),
              ("QFT:13", 1, "sampled", 128)]
+    if world == 8:
+        cases = [("BW:14x6", 3, "sampled", 128), ("CL:13x4", 5, "eowqs", 128), ("CL:13x4", 6, "forced", 128)]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     mp.start_processes(_worker, args=(world, _free_port(), cases, q), nprocs=world, join=True,
