@@ -36,6 +36,8 @@ WORKLOADS = {
     "C3E": "config 3 in EOWQS mode (positive branch, no probabilities)",
     "C5E32": "config 5's per-rank shard on one GPU: 32 x 8 flow cluster (2^32 complex64 = 32 GiB, the width "
              "each of 8 ranks holds for config 5), EOWQS",
+    "C3M": "config 3 with 8 of its 28 wires measured after the last layer (SHRINK-heavy: 8 eliminations with "
+           "the Eq. 13 reduction), sampled OWQS",
 }
 
 
@@ -457,7 +459,7 @@ def run_ours(args, rank, world, local_rank):
         h_in = torch.empty(N, dtype=hdt, pin_memory=True)
         h_in.copy_(x.to(hdt))
         a_in = h_in.numpy()
-        assert 2 ** len(pattern.outputs) == N
+        N_out = 2 ** len(pattern.outputs)
         k_e2e = max(4 * args.e2e_contexts, args.steps)  # the pipeline fills over the first C steps
         # serving pipeline over --e2e-contexts contexts on their own streams (owqs_submit_host / owqs_wait): every
         # step still does its own H2D copy, run and D2H copy, but one context's PCIe copies overlap
@@ -468,7 +470,7 @@ def run_ours(args, rank, world, local_rank):
         ctxs = [sim] + extra
         for x in extra:
             x.load(pattern)
-        h_outs = [torch.empty(N, dtype=hdt, pin_memory=True) for _ in ctxs]
+        h_outs = [torch.empty(N_out, dtype=hdt, pin_memory=True) for _ in ctxs]
         busy = [False] * len(ctxs)
 
         def e2e_step(i):
@@ -507,7 +509,7 @@ def run_ours(args, rank, world, local_rank):
             dt = float(t.item())
         hb = N * (8 if prec == 64 else 16)
         e2e = {"value": problems * n_cmd * k_e2e / dt, "unit": "commands/s", "h2d_bytes_per_step": hb,
-               "d2h_bytes_per_step": hb, "steps": k_e2e, "ms_per_step": 1e3 * dt / k_e2e,
+               "d2h_bytes_per_step": N_out * (8 if prec == 64 else 16), "steps": k_e2e, "ms_per_step": 1e3 * dt / k_e2e,
                "host_buffers": f"page-locked complex{prec}",
                "pipeline": (f"{len(ctxs)} contexts on separate streams (owqs_submit_host / owqs_wait)"
                             if loop <= 1 else "synchronous set_input / run / get_output")}

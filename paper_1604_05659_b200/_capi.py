@@ -17,7 +17,8 @@ FLAG_NO_GFLOW = 64
 FLAG_NO_JIT = 128
 FLAG_ONE_STATE = 256  # keep a disconnected pattern in one state vector (no sub-states)
 FLAG_MEASURED_NORM = 512  # structural decisions from a reduced ||psi||^2 instead of 1 (DESIGN R-13)
-KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap"}
+KCLASS_NAMES = {0: "pass", 1: "small_pass", 2: "grow", 3: "shrink", 4: "reduce", 5: "swap", 6: "rhok",
+                7: "shrinkk"}
 
 # every symbol include/owqs.h declares (checked by tests/test_capi_symbols.py)
 EXPORTED = ["owqs_create", "owqs_destroy", "owqs_load_pattern", "owqs_set_input", "owqs_set_input_host",
@@ -117,7 +118,8 @@ class StepDesc(C.Structure):
                 ("shrink_m", C.c_int32), ("n_bfly", C.c_int32), ("first_uses_red", C.c_int32),
                 ("first_full_rho", C.c_int32), ("pad", C.c_int32), ("ops", Op * MAX_OPS),
                 ("absorb", C.c_uint64 * MAX_BFLY), ("swap_local", C.c_int32), ("swap_global", C.c_int32),
-                ("n_remap", C.c_int32), ("remap_a", C.c_int32 * 6), ("remap_b", C.c_int32 * 6)]
+                ("n_remap", C.c_int32), ("remap_a", C.c_int32 * 6), ("remap_b", C.c_int32 * 6),
+                ("jk", C.c_int32), ("jm_pos", C.c_int32 * 4), ("jm", C.c_int32 * 4), ("j_src", C.c_int8 * 64)]
 
 
 class MStatic(C.Structure):

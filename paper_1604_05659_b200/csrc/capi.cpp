@@ -41,7 +41,7 @@ cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_w
 cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
-                       cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node);
+                       cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node, bool no_pdl);
 cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s,
                           const cudaGraphDeviceNode_t* nodes, int n_nodes, size_t off);
 cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaStream_t s);
@@ -74,10 +74,17 @@ struct CompiledMode {
   // §5.1): in the captured graph decide_kernel writes it into the device-updatable kernel node(s)
   // of its pass (handles in d_devnodes[step * shards + r], parameter offset coef_off[step]); the
   // EOWQS mode's decisions are run-independent and set by the host at capture (static_cp)
-  bool coefp = false;
+  // COEF_CONST instead: decide_kernel's PassCoef is copied by a graph memcpy node into the kernel's
+  // module __constant__ (cp_sym[step]); EOWQS's from d_static_cp (copied once when the kernel is
+  // used by this step only, cp_once). Kernel nodes stay ordinary graph nodes (ncu-profilable).
+  int coef_src = 0;  // jit.h COEF_*
+  bool coefp = false;  // coef_src != COEF_POINTER
   cudaGraphDeviceNode_t* d_devnodes = nullptr;
   std::vector<size_t> coef_off;
   std::vector<PassCoef> static_cp;
+  PassCoef* d_static_cp = nullptr;
+  std::vector<void*> cp_sym;
+  std::vector<char> cp_once;
   // EOWQS: every decision is run-independent (outcomes 0, no signals, no probabilities, static
   // scales), so d_pc written by the first EOWQS run is reused and later runs launch no decide kernel
   bool pc_static_ready = false;
@@ -113,6 +120,8 @@ struct owqs_ctx {
   double* d_red_all = nullptr;
   size_t shard_bytes = 0;
   void* d_swap = nullptr;  // two half-shard buffers (send, receive)
+  void* d_jscratch = nullptr;  // ST_SHRINKK output (joint k-outcome measurement), jscratch_bytes
+  size_t jscratch_bytes = 0;
   // run state
   RunParams* d_run = nullptr;
   uint8_t* d_outcome = nullptr;
@@ -195,6 +204,7 @@ DevPtrs dev_ptrs(owqs_ctx* ctx, const CompiledMode& m, int i) {
   p.err = s.d_err;
   p.rank = ctx->shard_rank(i);
   p.local_width = m.prog.phys_bits - ctx->n_global;
+  p.scratch = ctx->d_jscratch;
   return p;
 }
 
@@ -206,6 +216,7 @@ void free_mode(CompiledMode& m) {
   if (m.d_steps) cudaFree(m.d_steps);
   if (m.d_pc) cudaFree(m.d_pc);
   if (m.d_devnodes) cudaFree(m.d_devnodes);
+  if (m.d_static_cp) cudaFree(m.d_static_cp);
   m = CompiledMode();
 }
 
@@ -239,6 +250,16 @@ void static_eowqs_coef(const StepDesc& d, const std::vector<MStatic>& mst, PassC
     ++b;
   }
   c.scale = scale;
+}
+
+// Where the tile kernels read their decisions (jit.h COEF_*): OWQS_FLAG_NO_GRAPH -> the pointer;
+// else OWQS_COEF_SRC=ptr|param|const (default const)
+int coef_source(uint32_t flags) {
+  if (flags & OWQS_FLAG_NO_GRAPH) return COEF_POINTER;
+  const char* e = getenv("OWQS_COEF_SRC");
+  if (e && !strcmp(e, "ptr")) return COEF_POINTER;
+  if (e && !strcmp(e, "param")) return COEF_PARAM;
+  return COEF_CONST;
 }
 
 void drop_graphs(owqs_ctx* ctx) {
@@ -278,8 +299,9 @@ owqs_status compile_modes(owqs_ctx* ctx) {
         std::string nm;
         // graph launches (the default) take the decisions as kernel parameters; direct launches
         // (OWQS_FLAG_NO_GRAPH) read them from the PassCoef pointer
-        m.coefp = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH) && !getenv("OWQS_COEF_POINTER");
-        std::string src = jit_pass_source(m.prog.steps[k], ctx->prec, &nm, m.coefp);
+        m.coef_src = coef_source(ctx->cfg.flags);
+        m.coefp = m.coef_src != COEF_POINTER;
+        std::string src = jit_pass_source(m.prog.steps[k], ctx->prec, &nm, m.coef_src);
         if (src.empty()) return fail(ctx, OWQS_E_ARG, "pass kernel generation failed for step " + std::to_string(k));
         m.jit_name[k] = nm;
         ++m.n_jit;
@@ -322,6 +344,19 @@ owqs_status ensure_device(owqs_ctx* ctx) {
     if (ctx->n_global > 0) CU(cudaMalloc(&ctx->d_swap, need));  // two halves: send | receive
     ctx->shard_bytes = need;
   }
+  size_t jneed = 0;
+  for (int i = 0; i < 2; ++i)
+    for (const StepDesc& sd : ctx->cm[i].prog.steps)
+      if (sd.kind == ST_SHRINKK) jneed = std::max(jneed, (size_t)ctx->elem << (sd.width - sd.jk));
+  if (ctx->jscratch_bytes < jneed) {
+    drop_graphs(ctx);
+    cudaFree(ctx->d_jscratch);
+    ctx->d_jscratch = nullptr;
+    ctx->jscratch_bytes = 0;
+    if (cudaMalloc(&ctx->d_jscratch, jneed) != cudaSuccess)
+      return fail(ctx, OWQS_E_NOMEM, "joint-measurement scratch of " + std::to_string(jneed >> 20) + " MiB");
+    ctx->jscratch_bytes = jneed;
+  }
   size_t K = std::max<size_t>(1, (size_t)ctx->hp.n_measure);
   if (ctx->k_cap < K) {
     cudaFree(ctx->d_outcome);
@@ -345,7 +380,7 @@ owqs_status ensure_device(owqs_ctx* ctx) {
       CU(cudaMemcpy(m.d_sig, m.prog.sig_pool.data(), m.prog.sig_pool.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
     if (m.n_jit > 0 && !m.d_pc) CU(cudaMalloc(&m.d_pc, m.prog.steps.size() * sizeof(PassCoef)));
-    if (m.n_jit > 0 && m.coefp && !m.d_devnodes) {
+    if (m.n_jit > 0 && m.coef_src == COEF_PARAM && !m.d_devnodes) {
       CU(cudaMalloc(&m.d_devnodes, m.prog.steps.size() * ctx->shards.size() * sizeof(cudaGraphDeviceNode_t)));
       CU(cudaMemset(m.d_devnodes, 0, m.prog.steps.size() * ctx->shards.size() * sizeof(cudaGraphDeviceNode_t)));
     }
@@ -366,6 +401,13 @@ owqs_status ensure_device(owqs_ctx* ctx) {
           if (m.jit_name[k].empty() || fn[k]) continue;
           if (std::find(jm.names.begin(), jm.names.end(), m.jit_name[k]) == jm.names.end()) continue;
           CU(cudaLibraryGetKernel(&fn[k], lib, m.jit_name[k].c_str()));
+          if (m.coef_src == COEF_CONST && jit_engine(m.prog.steps[k], ctx->prec) == 2 &&
+              !jit_tile_small(m.prog.steps[k], ctx->prec)) {
+            if (m.cp_sym.empty()) m.cp_sym.assign(m.prog.steps.size(), nullptr);
+            size_t bytes = 0;
+            CU(cudaLibraryGetGlobal(&m.cp_sym[k], &bytes, lib, (m.jit_name[k] + "_cp").c_str()));
+            if (bytes != sizeof(PassCoef)) return fail(ctx, OWQS_E_CUDA, "generated kernel " + m.jit_name[k] + ": bad _cp symbol");
+          }
           const int eng = jit_engine(m.prog.steps[k], ctx->prec);
           const int dyn = jit_dyn_smem(eng, ctx->prec);
           if (dyn > 0) {
@@ -390,9 +432,25 @@ owqs_status ensure_device(owqs_ctx* ctx) {
         const StepDesc& sd = m.prog.steps[k];
         if (!fn[k] || jit_engine(sd, ctx->prec) != 2 || jit_tile_small(sd, ctx->prec)) continue;
         m.coef_off[k] = jit_coef_param_offset(fn[k]);
-        if (m.coefp && m.coef_off[k] == (size_t)-1)
+        if (m.coef_src == COEF_PARAM && m.coef_off[k] == (size_t)-1)
           return fail(ctx, OWQS_E_CUDA, "generated kernel " + m.jit_name[k] + ": no PassCoef parameter");
         if (i == 1) static_eowqs_coef(sd, m.prog.mst, m.static_cp[k]);
+      }
+      if (m.coef_src == COEF_CONST && i == 1 && !m.cp_sym.empty()) {
+        // EOWQS: run-independent decisions; a kernel used by one step only gets them once here,
+        // shared kernels get a memcpy node per run from d_static_cp
+        CU(cudaMalloc(&m.d_static_cp, m.prog.steps.size() * sizeof(PassCoef)));
+        CU(cudaMemcpy(m.d_static_cp, m.static_cp.data(), m.prog.steps.size() * sizeof(PassCoef), cudaMemcpyHostToDevice));
+        m.cp_once.assign(m.prog.steps.size(), 0);
+        for (size_t k = 0; k < m.cp_sym.size(); ++k) {
+          if (!m.cp_sym[k]) continue;
+          int uses = 0;
+          for (size_t j = 0; j < m.cp_sym.size(); ++j) uses += m.cp_sym[j] == m.cp_sym[k];
+          if (uses == 1) {
+            CU(cudaMemcpy(m.cp_sym[k], &m.static_cp[k], sizeof(PassCoef), cudaMemcpyHostToDevice));
+            m.cp_once[k] = 1;
+          }
+        }
       }
       m.jit_fn = fn;
       m.jit_blocks = blocks;
@@ -478,7 +536,7 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
   const bool eowqs_static = mode == OWQS_EOWQS && m.coefp;
   const bool static_pc = eowqs_static || (mode == OWQS_EOWQS && m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE"));
   const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH) && (mode != OWQS_EOWQS || static_pc);
-  const bool dev_update = m.coefp && !eowqs_static;  // sampled / forced graph: device node updates
+  const bool dev_update = m.coef_src == COEF_PARAM && !eowqs_static;  // sampled / forced: device node updates
   const size_t NS = ctx->shards.size();
   std::vector<cudaGraphDeviceNode_t> hnodes(dev_update ? m.prog.steps.size() * NS : 0, nullptr);
   if (m.coefp && !use_graph) return fail(ctx, OWQS_E_STATE, "parameter-coefficient kernels need a CUDA graph");
@@ -514,11 +572,20 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
         if (eng == 2 && !small && !static_pc)
           CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream, upd ? m.d_devnodes + i * NS : nullptr,
                            upd ? (int)NS : 0, upd ? m.coef_off[i] : 0));
+        // COEF_CONST: the pass's decisions into its kernel's __constant__ (graph memcpy node)
+        bool after_copy = false;
+        if (m.coef_src == COEF_CONST && eng == 2 && !small && !m.cp_sym.empty() && m.cp_sym[i]) {
+          const PassCoef* src = eowqs_static ? (m.cp_once.empty() || m.cp_once[i] ? nullptr : m.d_static_cp + i) : m.d_pc + i;
+          if (src) {
+            CU(cudaMemcpyAsync(m.cp_sym[i], src, sizeof(PassCoef), cudaMemcpyDeviceToDevice, ctx->stream));
+            after_copy = true;
+          }
+        }
         for (size_t r = 0; r < ctx->shards.size(); ++r) {
           if (jit)
             CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream,
                           (eowqs_static && eng == 2 && !small) ? &m.static_cp[i] : nullptr,
-                          (upd && capturing) ? &hnodes[i * NS + r] : nullptr));
+                          (upd && capturing) ? &hnodes[i * NS + r] : nullptr, after_copy && r == 0));
           else
             CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
         }
@@ -938,6 +1005,7 @@ void owqs_destroy(owqs_ctx* ctx) {
   }
   cudaFree(ctx->d_red_all);
   cudaFree(ctx->d_swap);
+  cudaFree(ctx->d_jscratch);
   cudaFree(ctx->d_run);
   cudaFree(ctx->d_outcome);
   cudaFree(ctx->d_prob0);
@@ -1774,10 +1842,12 @@ owqs_status owqs_launch_profile(owqs_ctx* ctx, int32_t* kclass, double* bytes, f
     int kc = step_kclass(s, ctx->prec);
     if (kclass) kclass[i] = kc;
     if (bytes)
-      bytes[i] = s.kind == ST_GROW     ? 3 * S
-                 : s.kind == ST_SHRINK ? 1.5 * S
-                 : s.kind == ST_SWAP   ? 2 * S
-                                       : (s.n_ops > 0 ? 2 * S : S);
+      bytes[i] = s.kind == ST_GROW       ? 3 * S
+                 : s.kind == ST_SHRINK   ? 1.5 * S
+                 : s.kind == ST_SWAP     ? 2 * S
+                 : s.kind == ST_RHOK     ? S
+                 : s.kind == ST_SHRINKK  ? S + 3 * std::ldexp(S, -s.jk)
+                                         : (s.n_ops > 0 ? 2 * S : S);
     if (ms) {
       float t = 0;
       CU(cudaEventElapsedTime(&t, ctx->prof_ev[i], ctx->prof_ev[i + 1]));

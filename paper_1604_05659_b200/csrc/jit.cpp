@@ -273,9 +273,12 @@ struct Gen {
   // bank: uniform-register FFMA2 / DFMA operands, written into the graph node by decide_kernel or by
   // the host for EOWQS), "pc->" = the PassCoef decide_kernel wrote to global memory (registers)
   std::string PC = "pc->";
-  Gen(const StepDesc& dd, int pr, bool use_tile, bool free_t0 = false, bool coefp = false)
+  int coef_src = 0;  // 0 pointer, 1 by-value parameter, 2 module __constant__ (jit.h)
+  Gen(const StepDesc& dd, int pr, bool use_tile, bool free_t0 = false, int csrc = 0)
       : d(dd), prec(pr), tile(use_tile), SB(pr == 0 ? 6 : 5), EPV(pr == 0 ? 2 : 1) {
-    if (coefp && use_tile) PC = "cp.";
+    coef_src = use_tile ? csrc : 0;
+    if (coef_src == 1) PC = "cp.";
+    if (coef_src == 2) PC = "OWQS_KNAME_cp.";
     if (tile) {
       KHI = tile_g(pr);
       UNR = 1;
@@ -1384,6 +1387,7 @@ struct Gen {
       used.erase(std::unique(used.begin(), used.end()), used.end());
       choose_bank_classes(used);
     }
+    if (coef_src == 2) o << "__constant__ owqs::PassCoef OWQS_KNAME_cp;  // the pass's decisions (graph memcpy node)\n";
     o << "extern \"C\" __global__ void __launch_bounds__(" << (32 << WB) << ", " << tile_minb() << ") OWQS_KNAME(const owqs::StepDesc d, const owqs::DevPtrs p, const owqs::PassCoef* "
       << (small ? "pc_global" : "pc") << ", const owqs::PassCoef cp) {  // pc: no __restrict__, so its loads stay behind griddepcontrol.wait\n"
       << "  (void)cp;\n"
@@ -1707,11 +1711,11 @@ int transposes_of(const std::string& s) {
 }
 }  // namespace
 
-std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, bool coefp) {
+std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, int coef_src) {
   const int eng = jit_engine(d, prec);
   if (!eng) return "";
-  coefp = coefp && eng == 2 && !jit_tile_small(d, prec);
-  Gen g(d, prec, eng == 2, false, coefp);
+  if (eng != 2 || jit_tile_small(d, prec)) coef_src = 0;
+  Gen g(d, prec, eng == 2, false, coef_src);
   if (!g.error.empty()) return "";
   std::string body = g.run();
   if (!g.error.empty()) return "";
@@ -1720,7 +1724,7 @@ std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, bool
   // OWQS_T0_FREE=0 / 1 forces it off / on for every pass
   const char* tf = getenv("OWQS_T0_FREE");
   if (eng == 2 && prec == 0 && !(tf && atoi(tf) == 0)) {
-    Gen g2(d, prec, true, true, coefp);
+    Gen g2(d, prec, true, true, coef_src);
     std::string b2 = g2.error.empty() ? g2.run() : std::string();
     if (g2.error.empty() && !b2.empty()) {
       const int smem1 = count_of(body, "reinterpret_cast<"), smem2 = count_of(b2, "reinterpret_cast<");
@@ -1729,7 +1733,7 @@ std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, bool
   }
   const std::string nm = std::string(eng == 2 ? "owqs_tile_" : "owqs_pass_") + (prec == 0 ? "c64_" : "c128_") + hex64(fnv1a(body));
   const std::string key = "OWQS_KNAME";
-  body.replace(body.find(key), key.size(), nm);
+  for (size_t at = body.find(key); at != std::string::npos; at = body.find(key, at + nm.size())) body.replace(at, key.size(), nm);
   if (name) *name = nm;
   return body;
 }
@@ -1808,7 +1812,7 @@ size_t jit_coef_param_offset(cudaKernel_t k) {
 }
 
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
-                       cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node) {
+                       cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node, bool no_pdl) {
   const int eng = jit_engine(d, prec);
   const int SB = prec == 0 ? 6 : 5;
   const int unr = jit_unr_of(d.nb_hi);
@@ -1827,7 +1831,7 @@ cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const 
     cfg.stream = s;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = (getenv("OWQS_NO_PDL") || jit_tile_small(d, prec)) ? 0 : 1;
+    attr[0].val.programmaticStreamSerializationAllowed = (no_pdl || getenv("OWQS_NO_PDL") || jit_tile_small(d, prec)) ? 0 : 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     if (dev_node) {  // captured launch whose PassCoef parameter decide_kernel rewrites every run

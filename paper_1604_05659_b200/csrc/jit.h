@@ -43,11 +43,16 @@ unsigned jit_tile_blocks(const StepDesc& d, int prec);
 int jit_smem_carveout(int engine, int prec);
 
 // Kernel source of one pass (no prelude). *name receives the kernel's extern "C" name, which is
-// a hash of the body (identical passes share one kernel). coefp: tile kernels read the pass's
-// decisions from their by-value PassCoef parameter (graph launches: decide_kernel writes it into the
-// device-updatable kernel node, the host for run-independent EOWQS decisions) instead of from the
-// PassCoef pointer (direct launches, OWQS_FLAG_NO_GRAPH).
-std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, bool coefp = true);
+// a hash of the body (identical passes share one kernel). coef_src: where a tile kernel reads the
+// pass's decisions (butterfly coefficients, scale, op conditions) --
+//   0 COEF_POINTER: the PassCoef decide_kernel wrote to global memory (registers);
+//   1 COEF_PARAM:   its by-value PassCoef parameter (constant bank 0: uniform operands), written into
+//                   the device-updatable graph node by decide_kernel (host: run-independent EOWQS);
+//   2 COEF_CONST:   the module's __constant__ <kernel>_cp (constant bank: uniform operands), filled by
+//                   a graph memcpy node from decide_kernel's output (host: EOWQS). Unlike 1, the
+//                   kernel nodes stay ordinary (profilable by ncu).
+enum { COEF_POINTER = 0, COEF_PARAM = 1, COEF_CONST = 2 };
+std::string jit_pass_source(const StepDesc& d, int prec, std::string* name, int coef_src = COEF_CONST);
 // Byte offset of the by-value PassCoef parameter in a tile kernel's parameter buffer.
 size_t jit_coef_param_offset(cudaKernel_t k);
 

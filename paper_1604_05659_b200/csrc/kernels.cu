@@ -679,6 +679,231 @@ __global__ void __launch_bounds__(512) small_pass_kernel(const StepDesc d, const
 }
 
 // ------------------------------------------------------------------------------------------------
+// Joint k-outcome measurement (PAPER §4.1 sub-state model L155-161, Fig. 6
+// L374-395): k consecutive eliminations share one pass that reduces the k qubits' 2^k x 2^k
+// reduced density matrix rho = Tr_rest |psi><psi| (ST_RHOK), and one pass that decides the k
+// outcomes in sequence from rho -- the conditional Eq. 3 probability of each given the earlier ones,
+// exactly what k single measurements see -- and applies the k projections + eliminations at once
+// (ST_SHRINKK: out = (prod_j <b_j|) psi / sqrt(P), width w -> w - k). Traffic S + (S + S/2^k)
+// instead of k (S + 1.5 S / 2^(j-1)) halving passes.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t pdep_pos(uint64_t v, const int32_t* pos, int n) {
+  uint64_t r = 0;
+  for (int j = 0; j < n; ++j) r |= ((v >> j) & 1ull) << pos[j];
+  return r;
+}
+
+// rho[a][b] += v[a] conj(v[b]) over every rest index, upper triangle (a <= b), fp64; block partials
+// then the last block sums them in a fixed order (deterministic) into partials[RHOK_RESULT_OFF ..]
+template <typename T, int K>
+__global__ void __launch_bounds__(256) rhok_kernel(const StepDesc d, const DevPtrs p) {
+  typedef typename VT<T>::C C;
+  constexpr int D = 1 << K, NV = 2 * (D * (D + 1) / 2);
+  const C* st = reinterpret_cast<const C*>(p.state);
+  const int w = d.width;
+  int32_t rest[64];
+  uint64_t mmask = 0;
+  for (int j = 0; j < K; ++j) mmask |= 1ull << d.jm_pos[j];
+  for (int b = 0, q = 0; b < w; ++b)
+    if (!((mmask >> b) & 1)) rest[q++] = b;
+  double acc[NV];
+#pragma unroll
+  for (int v = 0; v < NV; ++v) acc[v] = 0.0;
+  const uint64_t nrest = 1ull << (w - K);
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrest; r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t base = pdep_pos(r, rest, w - K);
+    double vr[D], vi[D];
+#pragma unroll
+    for (int x = 0; x < D; ++x) {
+      const C a = st[base | pdep_pos((uint64_t)x, d.jm_pos, K)];
+      vr[x] = (double)a.x;
+      vi[x] = (double)a.y;
+    }
+    int e = 0;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = a; b < D; ++b) {
+        acc[e++] += vr[a] * vr[b] + vi[a] * vi[b];  // Re v[a] conj(v[b])
+        acc[e++] += vi[a] * vr[b] - vr[a] * vi[b];  // Im
+      }
+  }
+  __shared__ double red[8][NV];
+  __shared__ int last;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int v = 0; v < NV; ++v) {
+    double x = acc[v];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLMASK, x, o);
+    if (lane == 0) red[warp][v] = x;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+    double t = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += red[q][v];
+    p.partials[(size_t)blockIdx.x * NV + v] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&p.counter[0], 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int v = threadIdx.x; v < NV; v += blockDim.x) {
+    double t = 0;
+    for (unsigned b = 0; b < gridDim.x; ++b) t += __ldcg(&p.partials[(size_t)b * NV + v]);
+    p.partials[RHOK_RESULT_OFF + v] = t;
+  }
+  if (threadIdx.x == 0) p.counter[0] = 0;
+}
+
+// Decide the group's outcomes from rho in the emitter's order and build the 2^k projection
+// coefficients (prod_j bra_j components / sqrt(P_joint); EOWQS: sqrt2^k scaling, outcomes 0).
+// One thread. bra of outcome s: (1, (-1)^s e^{-i theta}) / sqrt2 (Eqs. 11-12; R-1).
+__device__ void joint_decide(const StepDesc& d, const DevPtrs& p, bool record, double (*cv)[2], const double* rv) {
+  const int K = d.jk, mode = p.run->mode;
+  const double PI = 3.141592653589793238462643383279502884, R2 = 0.70710678118654752440;
+  double Rr[64], Ri[64];  // current (conditioned) reduced matrix over the undecided qubits, D x D
+  int D = 1 << K;
+  if (mode != 2) {
+    int e = 0;
+    for (int a = 0; a < D; ++a)
+      for (int b = a; b < D; ++b) {
+        Rr[a * D + b] = rv[e];
+        Ri[a * D + b] = rv[e + 1];
+        Rr[b * D + a] = rv[e];
+        Ri[b * D + a] = -rv[e + 1];
+        e += 2;
+      }
+  }
+  LocalOutcomes loc;
+  loc.n = 0;
+  double ur[JOINT_KMAX][2], ui[JOINT_KMAX][2];
+  double pj = 1.0;
+  for (int j = 0; j < K; ++j) {
+    const MStatic ms = p.mst[d.jm[j]];
+    int sg = 0, tg = 0;
+    if (mode != 2) {
+      sg = signal_parity(p, ms.s_off, ms.s_len, loc);
+      tg = signal_parity(p, ms.t_off, ms.t_len, loc);
+    }
+    const double theta = (sg ? -ms.alpha : ms.alpha) + (tg ? PI : 0.0);  // Eq. 2
+    double sn, cs;
+    sincos(theta, &sn, &cs);
+    const double er = cs, ei = -sn;  // e^{-i theta}
+    int outc = 0;
+    double P0 = -1.0;
+    if (mode != 2) {
+      // P0 = <+|R|+> summed over the other undecided qubits (qubit j is bit 0 of R's index)
+      double tot = 0.0, p0 = 0.0;
+      for (int a = 0; a < D; ++a) tot += Rr[a * D + a];
+      for (int a2 = 0; a2 < D / 2; ++a2) {
+        const int a0 = a2 << 1, a1 = a0 | 1;
+        // u = (1, e^{-i theta}) / sqrt2: sum_xy u_x R_xy conj(u_y)
+        const double r00 = Rr[a0 * D + a0], r11 = Rr[a1 * D + a1];
+        const double r01r = Rr[a0 * D + a1], r01i = Ri[a0 * D + a1];
+        // u0 R01 conj(u1) + u1 R10 conj(u0) = 2 Re(R01 conj(e^{-i theta})) / 2
+        p0 += 0.5 * (r00 + r11) + (r01r * er + r01i * ei);
+      }
+      p0 = fmin(fmax(p0, 0.0), tot);
+      P0 = tot > 0 ? p0 / tot : 0.0;
+      outc = mode == 0 ? (draw_uniform(p.run->seed, ms.key) <= P0 ? 0 : 1) : (p.forced[ms.ord] & 1);
+      double pS = outc ? 1.0 - P0 : P0;
+      if (pS < 1e-12) {
+        if (record) atomicExch(p.err, 1);
+        pS = 1.0;
+      }
+      pj *= pS;
+      // condition: R' = <b|R|b> on qubit j (bit 0), b the chosen bra
+      const double s1 = outc ? -1.0 : 1.0;
+      const double u1r = s1 * er, u1i = s1 * ei;  // u = (1, u1) / sqrt2
+      const int D2 = D / 2;
+      for (int a2 = 0; a2 < D2; ++a2)
+        for (int b2 = 0; b2 < D2; ++b2) {
+          const int a0 = a2 << 1, b0 = b2 << 1;
+          // sum_xy u_x R[a0|x][b0|y] conj(u_y) / 2
+          double sr = 0, si = 0;
+          for (int x = 0; x < 2; ++x)
+            for (int y = 0; y < 2; ++y) {
+              const double uxr = x ? u1r : 1.0, uxi = x ? u1i : 0.0;
+              const double uyr = y ? u1r : 1.0, uyi = y ? -u1i : 0.0;  // conj(u_y)
+              const double rr = Rr[(a0 | x) * D + (b0 | y)], ri = Ri[(a0 | x) * D + (b0 | y)];
+              const double tr = uxr * rr - uxi * ri, ti = uxr * ri + uxi * rr;
+              sr += tr * uyr - ti * uyi;
+              si += tr * uyi + ti * uyr;
+            }
+          Rr[a2 * D2 + b2] = 0.5 * sr;  // in place: (a2, b2) index <= (a0, b0) slots already read
+          Ri[a2 * D2 + b2] = 0.5 * si;
+        }
+      D = D2;
+    }
+    const double s1 = outc ? -1.0 : 1.0;
+    const double k = mode == 2 ? 1.0 : R2;
+    ur[j][0] = k;
+    ui[j][0] = 0.0;
+    ur[j][1] = k * s1 * er;
+    ui[j][1] = k * s1 * ei;
+    if (record) {
+      p.outcome[ms.ord] = (uint8_t)outc;
+      p.prob0[ms.ord] = P0;
+    }
+    if (loc.n < MAX_BFLY) {
+      loc.ord[loc.n] = ms.ord;
+      loc.out[loc.n] = (uint8_t)outc;
+      loc.n++;
+    }
+  }
+  const double scale = mode == 2 ? 1.0 : 1.0 / sqrt(pj);
+  for (int x = 0; x < (1 << K); ++x) {
+    double cr = scale, ci = 0.0;
+    for (int j = 0; j < K; ++j) {
+      const int b = (x >> j) & 1;
+      const double nr = cr * ur[j][b] - ci * ui[j][b], ni = cr * ui[j][b] + ci * ur[j][b];
+      cr = nr;
+      ci = ni;
+    }
+    cv[x][0] = cr;
+    cv[x][1] = ci;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) shrinkk_kernel(const StepDesc d, const DevPtrs p) {
+  typedef typename VT<T>::C C;
+  __shared__ double cv[1 << JOINT_KMAX][2];
+  __shared__ PassShared sh;
+  if (threadIdx.x == 0) joint_decide(d, p, blockIdx.x == 0, cv, p.partials + RHOK_RESULT_OFF);
+  __syncthreads();
+  const int K = d.jk, w = d.width, wo = w - K;
+  const C* st = reinterpret_cast<const C*>(p.state);
+  C* out = reinterpret_cast<C*>(p.scratch);
+  T cr[1 << JOINT_KMAX], ci[1 << JOINT_KMAX];
+  uint64_t moff[1 << JOINT_KMAX];
+  for (int x = 0; x < (1 << K); ++x) {
+    cr[x] = (T)cv[x][0];
+    ci[x] = (T)cv[x][1];
+    moff[x] = pdep_pos((uint64_t)x, d.jm_pos, K);
+  }
+  double acc[4] = {0, 0, 0, 0};
+  const uint64_t n = 1ull << wo;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    uint64_t src = 0;
+    for (int t = 0; t < wo; ++t) src |= ((i >> t) & 1ull) << d.j_src[t];
+    T orr = 0, oi = 0;
+    for (int x = 0; x < (1 << K); ++x) {
+      const C a = st[src | moff[x]];
+      orr += cr[x] * a.x - ci[x] * a.y;
+      oi += cr[x] * a.y + ci[x] * a.x;
+    }
+    out[i] = make_c<T>(orr, oi);
+    acc[0] += (double)orr * orr + (double)oi * oi;
+  }
+  if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
+}
+
+// ------------------------------------------------------------------------------------------------
 // Batched small-width replicas: one CTA runs the WHOLE step program on one
 // state held in shared memory; the grid walks a batch of independent inputs (config 1's 64
 // inputs, recognition's basis columns, seed sweeps). Per-state outcomes / prob0 / run params.
@@ -692,6 +917,7 @@ __global__ void __launch_bounds__(128) batch_kernel(const StepDesc* steps, int n
   C* s = reinterpret_cast<C*>(smem_raw);
   __shared__ PassShared sh;
   __shared__ double red[4];
+  __shared__ double rhok_w[4][RHOK_VALS], rhok_s[RHOK_VALS], cv_s[1 << JOINT_KMAX][2];
   const T r2 = (T)0.70710678118654752440;
   for (int b = blockIdx.x; b < n_batch; b += gridDim.x) {
     DevPtrs p = base;
@@ -760,6 +986,63 @@ __global__ void __launch_bounds__(128) batch_kernel(const StepDesc* steps, int n
         }
         __syncthreads();
       }
+      else if (d.kind == ST_RHOK) {  // joint measurement: rho of the jk positions (block, fixed order)
+        const int k = d.jk, D = 1 << k, w = d.width;
+        uint32_t mm = 0;
+        for (int j = 0; j < k; ++j) mm |= 1u << d.jm_pos[j];
+        double a[RHOK_VALS];
+        for (int v = 0; v < RHOK_VALS; ++v) a[v] = 0.0;
+        for (int r = threadIdx.x; r < (1 << (w - k)); r += blockDim.x) {
+          uint32_t base = 0;
+          for (int bit = 0, q = 0; bit < w; ++bit)
+            if (!((mm >> bit) & 1)) base |= (uint32_t)((r >> q++) & 1) << bit;
+          int e = 0;
+          for (int x = 0; x < D; ++x)
+            for (int y = x; y < D; ++y) {
+              const C u = s[base | (uint32_t)pdep_pos((uint64_t)x, d.jm_pos, k)];
+              const C v = s[base | (uint32_t)pdep_pos((uint64_t)y, d.jm_pos, k)];
+              a[e++] += (double)u.x * v.x + (double)u.y * v.y;
+              a[e++] += (double)u.y * v.x - (double)u.x * v.y;
+            }
+        }
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        for (int v = 0; v < RHOK_VALS; ++v) {
+          double x = a[v];
+          for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(FULLMASK, x, o);
+          if (lane == 0) rhok_w[warp][v] = x;
+        }
+        __syncthreads();
+        for (int v = threadIdx.x; v < RHOK_VALS; v += blockDim.x) {
+          double t = 0;
+          for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t += rhok_w[q][v];
+          rhok_s[v] = t;
+        }
+        __syncthreads();
+      } else if (d.kind == ST_SHRINKK) {
+        if (threadIdx.x == 0) joint_decide(d, p, true, cv_s, rhok_s);
+        __syncthreads();
+        const int k = d.jk, wo = d.width - k;
+        T o_r[16], o_i[16];
+        int cnt = 0;
+        for (int i = threadIdx.x; i < (1 << wo); i += blockDim.x, ++cnt) {
+          uint32_t src = 0;
+          for (int t2 = 0; t2 < wo; ++t2) src |= (uint32_t)((i >> t2) & 1) << d.j_src[t2];
+          T orr = 0, oi = 0;
+          for (int x = 0; x < (1 << k); ++x) {
+            const C v = s[src | (uint32_t)pdep_pos((uint64_t)x, d.jm_pos, k)];
+            const T cr = (T)cv_s[x][0], ci = (T)cv_s[x][1];
+            orr += cr * v.x - ci * v.y;
+            oi += cr * v.y + ci * v.x;
+          }
+          o_r[cnt] = orr;
+          o_i[cnt] = oi;
+          acc[0] += (double)orr * orr + (double)oi * oi;
+        }
+        __syncthreads();
+        cnt = 0;
+        for (int i = threadIdx.x; i < (1 << wo); i += blockDim.x, ++cnt) s[i] = make_c<T>(o_r[cnt], o_i[cnt]);
+        __syncthreads();
+      }
       if (d.red_kind != RED_NONE) block_sum4(acc, sh, red);
     }
     const int nout = 1 << n_out;
@@ -784,15 +1067,77 @@ __global__ void __launch_bounds__(256) grow_kernel(const StepDesc d, const DevPt
   const uint64_t n = 1ull << d.width;
   const T r = (T)0.70710678118654752440;
   double acc[4] = {0, 0, 0, 0};
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    C v = st[i];
-    v.x *= r;
-    v.y *= r;
-    st[i] = v;
-    st[i + n] = v;
-    acc[0] += 2.0 * ((double)v.x * v.x + (double)v.y * v.y);
+  if (sizeof(T) == 4 && d.width >= 1) {
+    // complex64: 16 B per thread access (two amplitudes), 512 B per warp instruction
+    float4* s4 = reinterpret_cast<float4*>(p.state);
+    const uint64_t n2 = n >> 1;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n2; i += (uint64_t)gridDim.x * blockDim.x) {
+      float4 v = __ldcs(s4 + i);
+      v.x *= (float)r; v.y *= (float)r; v.z *= (float)r; v.w *= (float)r;
+      __stcs(s4 + i, v);
+      __stcs(s4 + i + n2, v);
+      acc[0] += 2.0 * ((double)v.x * v.x + (double)v.y * v.y + (double)v.z * v.z + (double)v.w * v.w);
+    }
+  } else {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+      C v = st[i];
+      v.x *= r;
+      v.y *= r;
+      st[i] = v;
+      st[i + n] = v;
+      acc[0] += 2.0 * ((double)v.x * v.x + (double)v.y * v.y);
+    }
   }
   if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
+}
+
+// complex64 SHRINK body with 16 B accesses: each thread produces two consecutive output
+// amplitudes (a float4) from float4 loads of the 4-group rows (b >= 1), from two float4 loads that
+// each hold an (x_b=0, x_b=1) pair (b = 0), or from the lower / upper halves (b = top).
+__device__ __forceinline__ float2 shrink_out(float u0r, float u0i, float u1r, float u1i, float x0r, float x0i,
+                                             float x1r, float x1i) {
+  return make_float2(u0r * x0r - u0i * x0i + u1r * x1r - u1i * x1i, u0r * x0i + u0i * x0r + u1r * x1i + u1i * x1r);
+}
+__device__ void shrink_c64(int w, int b, float u0r, float u0i, float u1r, float u1i, float4* s4, double (&acc)[4]) {
+  const int top = w - 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  auto add = [&](float2 o) { acc[0] += (double)o.x * o.x + (double)o.y * o.y; };
+  if (b == top) {  // x0 = lower half, x1 = upper half; output = lower half
+    const uint64_t h2 = 1ull << (w - 2);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < h2; i += stride) {
+      const float4 x0 = __ldcs(s4 + i), x1 = __ldcs(s4 + i + h2);
+      const float2 o0 = shrink_out(u0r, u0i, u1r, u1i, x0.x, x0.y, x1.x, x1.y);
+      const float2 o1 = shrink_out(u0r, u0i, u1r, u1i, x0.z, x0.w, x1.z, x1.w);
+      __stcs(s4 + i, make_float4(o0.x, o0.y, o1.x, o1.y));
+      add(o0);
+      add(o1);
+    }
+  } else if (b == 0) {  // (x_b0, x_b1) adjacent: one float4 per (row of top); the top moves into slot 0
+    const uint64_t nq = 1ull << (w - 2), T2 = 1ull << (top - 1);  // float4 units; top bit in unit index
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq; i += stride) {
+      const float4 a = __ldcs(s4 + i), c = __ldcs(s4 + i + T2);  // a = (x00, x10), c = (x01, x11)
+      const float2 o0 = shrink_out(u0r, u0i, u1r, u1i, a.x, a.y, a.z, a.w);
+      const float2 o1 = shrink_out(u0r, u0i, u1r, u1i, c.x, c.y, c.z, c.w);
+      __stcs(s4 + i, make_float4(o0.x, o0.y, o1.x, o1.y));  // out[r] = o0, out[r | B] = o1
+      add(o0);
+      add(o1);
+    }
+  } else {  // float4 unit = amplitudes (2k, 2k + 1): both have the same b / top bits
+    const uint64_t nq2 = 1ull << (w - 3);
+    const uint64_t B = 1ull << (b - 1), TT = 1ull << (top - 1);  // in float4 units
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nq2; i += stride) {
+      uint64_t r = ((i >> (b - 1)) << b) | (i & (B - 1));
+      r = ((r >> (top - 1)) << top) | (r & (TT - 1));
+      const float4 x00 = __ldcs(s4 + r), x10 = __ldcs(s4 + (r | B)), x01 = __ldcs(s4 + (r | TT)), x11 = __ldcs(s4 + (r | B | TT));
+      const float2 a0 = shrink_out(u0r, u0i, u1r, u1i, x00.x, x00.y, x10.x, x10.y);
+      const float2 a1 = shrink_out(u0r, u0i, u1r, u1i, x00.z, x00.w, x10.z, x10.w);
+      const float2 c0 = shrink_out(u0r, u0i, u1r, u1i, x01.x, x01.y, x11.x, x11.y);
+      const float2 c1 = shrink_out(u0r, u0i, u1r, u1i, x01.z, x01.w, x11.z, x11.w);
+      __stcs(s4 + r, make_float4(a0.x, a0.y, a1.x, a1.y));
+      __stcs(s4 + (r | B), make_float4(c0.x, c0.y, c1.x, c1.y));
+      add(a0); add(a1); add(c0); add(c1);
+    }
+  }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -813,6 +1158,11 @@ __global__ void __launch_bounds__(256) shrink_kernel(const StepDesc d, const Dev
   C* st = reinterpret_cast<C*>(p.state);
   const int w = d.width, b = d.slot, top = w - 1;
   double acc[4] = {0, 0, 0, 0};
+  if (sizeof(T) == 4 && w >= 3) {
+    shrink_c64(w, b, (float)u0r, (float)u0i, (float)u1r, (float)u1i, reinterpret_cast<float4*>(p.state), acc);
+    if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
+    return;
+  }
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   if (b == top) {
     const uint64_t h = 1ull << (w - 1);
@@ -1251,6 +1601,8 @@ cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s) 
 // Kernel class of a step (OWQS_KCLASS_* of include/owqs.h).
 int step_kclass(const StepDesc& d, int prec) {
   const int SB = prec == 0 ? 6 : 5;
+  if (d.kind == ST_RHOK) return 6;
+  if (d.kind == ST_SHRINKK) return 7;
   if (d.kind == ST_GROW) return 2;
   if (d.kind == ST_SHRINK) return 3;
   if (d.kind == ST_SWAP) return 5;
@@ -1262,6 +1614,25 @@ int step_kclass(const StepDesc& d, int prec) {
 // Launch one step. prec: 0 complex64, 1 complex128.
 cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStream_t s) {
   const int SB = prec == 0 ? 6 : 5;
+  if (d.kind == ST_RHOK || d.kind == ST_SHRINKK) {
+    if (d.jk < 1 || d.jk > JOINT_KMAX || d.width < d.jk) return cudaErrorInvalidValue;
+    const uint64_t work = 1ull << (d.width - d.jk);
+    const unsigned blocks = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)g_lim.max_blocks_elem));
+    if (d.kind == ST_RHOK) {
+#define OWQS_RK(TT) \
+  switch (d.jk) { case 1: rhok_kernel<TT, 1><<<blocks, 256, 0, s>>>(d, p); break; \
+                  case 2: rhok_kernel<TT, 2><<<blocks, 256, 0, s>>>(d, p); break; \
+                  default: rhok_kernel<TT, 3><<<blocks, 256, 0, s>>>(d, p); break; }
+      if (prec == 0) { OWQS_RK(float) } else { OWQS_RK(double) }
+#undef OWQS_RK
+      return cudaGetLastError();
+    }
+    if (prec == 0) shrinkk_kernel<float><<<blocks, 256, 0, s>>>(d, p);
+    else shrinkk_kernel<double><<<blocks, 256, 0, s>>>(d, p);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemcpyAsync(p.state, p.scratch, (size_t)(prec == 0 ? 8 : 16) << (d.width - d.jk), cudaMemcpyDeviceToDevice, s);
+  }
   if (d.kind == ST_PASS) {
     const int khi = d.nb_hi;
     if (khi > KMAX_AOT) return cudaErrorInvalidValue;  // wide passes run only as generated tile kernels
@@ -1305,6 +1676,7 @@ cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStrea
     return cudaGetLastError();
   }
   uint64_t work = d.kind == ST_GROW ? (1ull << d.width) : (1ull << std::max(0, d.width - (d.slot == d.width - 1 ? 1 : 2)));
+  if (prec == 0 && d.width >= 3) work >>= 1;  // complex64: two amplitudes (16 B) per thread access
   uint64_t blocks = std::max<uint64_t>(1, std::min<uint64_t>((work + 255) / 256, (uint64_t)g_lim.max_blocks_elem));
   if (d.kind == ST_GROW) {
     if (prec == 0) grow_kernel<float><<<(unsigned)blocks, 256, 0, s>>>(d, p);

@@ -42,7 +42,10 @@ constexpr int KMAX_AOT = 4;      // ... in passes run by the ahead-of-time / dir
 constexpr int KTILE = 7;         // ... in passes run by the complex64 tile engine (13-bit CTA tile)
 constexpr int MAX_BFLY = 64;     // butterflies per pass (fused mode)
 
-enum StepKind : int32_t { ST_PASS = 0, ST_GROW = 1, ST_SHRINK = 2, ST_SWAP = 3 };
+enum StepKind : int32_t { ST_PASS = 0, ST_GROW = 1, ST_SHRINK = 2, ST_SWAP = 3, ST_RHOK = 4, ST_SHRINKK = 5 };
+// joint k-outcome measurement: up to JOINT_KMAX consecutive eliminations share
+// one reduced-density-matrix pass (ST_RHOK) and one projection + compaction pass (ST_SHRINKK)
+constexpr int JOINT_KMAX = 3;
 enum RedKind : int32_t { RED_NONE = 0, RED_NORM = 1, RED_RHO = 2 };
 
 // One device step. Passed by value as a kernel parameter.
@@ -72,6 +75,13 @@ struct StepDesc {
   // whose qubit has no further 2x2 op traded for a group slot of a still-active qubit)
   int32_t n_remap;
   int32_t remap_a[6], remap_b[6];
+  // ST_RHOK / ST_SHRINKK: jk measured qubits in the emitter's (= the caller's plan) order; bit j of the
+  // 2^jk joint index <-> physical position jm_pos[j] of the pre-group layout (width = the pre-group
+  // width), jm[j] = its M plan index; ST_SHRINKK output bit t < width - jk comes from position
+  // j_src[t] (the composition of jk SHRINK top moves, so the slot map is that of jk single SHRINKs)
+  int32_t jk;
+  int32_t jm_pos[4], jm[4];
+  signed char j_src[64];
 };
 
 // Decisions of one pass, computed once by decide_kernel and read by every CTA of the generated pass
@@ -127,6 +137,11 @@ struct DevPtrs {
   int32_t* err;                // device error flag (1 = forced branch with prob < 1e-12)
   uint32_t rank;               // multi-rank: this shard's rank = the global (top) index bits
   int32_t local_width;         // multi-rank: bits of the shard index (positions >= are rank bits)
+  void* scratch;               // ST_SHRINKK output (2^(width - jk) amplitudes), copied back into state
 };
+// ST_RHOK result (the 2^k x 2^k reduced density matrix, upper triangle incl. diagonal, re / im
+// interleaved) in the tail of the block-partials region of DevPtrs::partials
+constexpr int RHOK_VALS = 2 * ((1 << JOINT_KMAX) * ((1 << JOINT_KMAX) + 1) / 2);  // 72
+constexpr size_t RHOK_RESULT_OFF = (size_t)(1 << 20) * 4 - 128;
 
 }  // namespace owqs

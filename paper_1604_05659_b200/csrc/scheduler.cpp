@@ -604,6 +604,10 @@ double Program::bytes_per_run(int eb) const {
       b += 3 * S;
     else if (s.kind == ST_SWAP)
       b += 2 * S;  // pack (read S/2, write S/2) + unpack (read S/2, write S/2)
+    else if (s.kind == ST_RHOK)
+      b += S;  // read-only
+    else if (s.kind == ST_SHRINKK)
+      b += S + 3 * std::ldexp(S, -s.jk);  // read S, write S / 2^k to scratch, copy back
     else
       b += 1.5 * S;
   }
@@ -994,6 +998,48 @@ struct Packer {
     }
   }
 
+  // joint k-outcome measurement of consecutive eliminations: ST_RHOK +
+  // ST_SHRINKK for ops[i .. i + k). The physical bookkeeping is that of k single SHRINKs in a row
+  // (same final slot map); j_src records where each output bit comes from.
+  int joint_k = JOINT_KMAX;  // OWQS_JOINT_K (1 = off)
+  void joint_shrink(int i, int k) {
+    StepDesc r = blank(ST_RHOK), s = blank(ST_SHRINKK);
+    r.jk = s.jk = k;
+    int orig[64];
+    for (int b = 0; b < 64; ++b) orig[b] = b;
+    const int w0 = width;
+    for (int j = 0; j < k; ++j) {
+      const LOp& l = ops[i + j];
+      const int vm = l.a, pm = pos[vm];
+      r.jm_pos[j] = s.jm_pos[j] = orig[pm];
+      r.jm[j] = s.jm[j] = l.m;
+      const int vt = width - 1, pt = width - 1, u = at[pt], q = pos[vt];
+      if (vm == vt) {
+        if (pm != pt) {
+          pos[u] = pm;
+          at[pm] = u;
+        }
+      } else if (q == pt) {
+        pos[vm] = pm;
+        at[pm] = vm;
+      } else {
+        pos[vm] = q;
+        at[q] = vm;
+        pos[u] = pm;
+        at[pm] = u;
+      }
+      pos[vt] = vt;
+      at[pt] = vt;
+      orig[pm] = orig[pt];  // the physical top qubit moves into the freed position
+      --width;
+    }
+    for (int t = 0; t < w0 - k; ++t) s.j_src[t] = (int8_t)orig[t];
+    r.width = s.width = w0 - n_global;
+    if (!eowqs) emit(r);
+    emit(s);
+    pr.n_shrink += k;
+  }
+
   void run() {
     int lo = 0;
     const int n = (int)ops.size();
@@ -1002,39 +1048,80 @@ struct Packer {
       segment(lo, i);
       lo = i + 1;
       if (i == n) break;
+      if (ops[i].type == 11 && joint_k > 1) {
+        int k = 1;
+        while (k < joint_k && i + k < n && ops[i + k].type == 11) ++k;
+        if (k > 1) {
+          joint_shrink(i, k);
+          i += k - 1;
+          lo = i + 1;
+          continue;
+        }
+      }
       const LOp& l = ops[i];
-      if (l.type == 10) {
+      // GROW / SHRINK act on physical positions; with qubit remapping the emitter's virtual slots
+      // map through pos[] (the kernels' conventions: GROW appends at the physical top, SHRINK moves
+      // the physical top qubit into the freed position)
+      if (l.type == 10) {  // the emitter appends its virtual top slot l.a = width
         StepDesc g = blank(ST_GROW);
-        g.slot = l.a;
+        g.slot = width;
+        pos[l.a] = width;
+        at[width] = l.a;
         emit(g);
         ++width;
       } else {
+        const int vm = l.a, pm = pos[vm];
         if (!eowqs) {  // rho of the measured slot from the last pass (or a read-only pass)
           StepDesc* last = pr.steps.empty() ? nullptr : &pr.steps.back();
+          // the last pass reduces in its input layout: undo its store remap for vm's position
+          int pl = pm;
+          if (last && last->kind == ST_PASS)
+            for (int k = 0; k < last->n_remap; ++k) {
+              if (pm == last->remap_a[k]) pl = last->remap_b[k];
+              if (pm == last->remap_b[k]) pl = last->remap_a[k];
+            }
           bool room = last && last->kind == ST_PASS && last->red_kind == RED_NONE && last->width == width &&
-                      (l.a < SB || last->nb_hi < wide_at(last->width) ||
-                       std::find(last->bhi, last->bhi + last->nb_hi, l.a) != last->bhi + last->nb_hi);
+                      (pl < SB || last->nb_hi < wide_at(last->width) ||
+                       std::find(last->bhi, last->bhi + last->nb_hi, pl) != last->bhi + last->nb_hi);
           if (room) {
-            if (l.a >= SB && std::find(last->bhi, last->bhi + last->nb_hi, l.a) == last->bhi + last->nb_hi) {
-              last->bhi[last->nb_hi++] = l.a;
+            if (pl >= SB && std::find(last->bhi, last->bhi + last->nb_hi, pl) == last->bhi + last->nb_hi) {
+              last->bhi[last->nb_hi++] = pl;
               std::sort(last->bhi, last->bhi + last->nb_hi);
             }
             last->red_kind = RED_RHO;
-            last->red_slot = l.a;
+            last->red_slot = pl;
           } else {
             StepDesc r = blank(ST_PASS);
-            if (l.a >= SB) r.bhi[r.nb_hi++] = l.a;
+            if (pm >= SB) r.bhi[r.nb_hi++] = pm;
             r.red_kind = RED_RHO;
-            r.red_slot = l.a;
+            r.red_slot = pm;
             emit(r);
           }
         }
         StepDesc s = blank(ST_SHRINK);
-        s.slot = l.a;
+        s.slot = pm;
         s.shrink_m = l.m;
         s.first_uses_red = eowqs ? 0 : 1;
         s.first_full_rho = eowqs ? 0 : 1;
         emit(s);
+        // the emitter renames its virtual top vt into vm; physically the top qubit u moves into pm
+        const int vt = width - 1, pt = width - 1, u = at[pt], q = pos[vt];
+        if (vm == vt) {
+          if (pm != pt) {
+            pos[u] = pm;
+            at[pm] = u;
+          }
+        } else if (q == pt) {
+          pos[vm] = pm;
+          at[pm] = vm;
+        } else {
+          pos[vm] = q;
+          at[q] = vm;
+          pos[u] = pm;
+          at[pm] = u;
+        }
+        pos[vt] = vt;
+        at[pt] = vt;
         --width;
       }
     }
@@ -1078,6 +1165,7 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
   }
   Packer pk(em.ops, pr, SB, eowqs, fuse ? MAX_BFLY : 1, n_global);
   pk.measured_norm = measured_norm;
+  if (const char* e = getenv("OWQS_JOINT_K")) pk.joint_k = std::max(1, std::min(JOINT_KMAX, atoi(e)));
   pk.kwide = std::max(KMAX_AOT, std::min(KTILE, kwide));
   if (const char* env = getenv("OWQS_MAX_BFLY")) pk.max_bfly = std::max(1, std::min(MAX_BFLY, atoi(env)));
   {
@@ -1087,7 +1175,7 @@ Program compile_program(const HostPattern& hp, const Plan& plan, int mode, int S
     // default on (OWQS_REMAP=0 turns it off): C3 51 -> 35 passes, 51.0 -> 49.8 ms
     // (sharded programs too: a remap permutes local positions only; rank bits and the swap plan
     // follow the same pos / at maps)
-    pk.remap = (!env || atoi(env) != 0) && !resize && pk.kwide > KMAX_AOT;
+    pk.remap = (!env || atoi(env) != 0) && (!resize || !getenv("OWQS_REMAP_NO_RESIZE")) && pk.kwide > KMAX_AOT;
     if (const char* m = getenv("OWQS_REMAP_MARGIN")) pk.remap_margin = atoi(m);
   }
   if (const char* env = getenv("OWQS_KWIDE")) pk.kwide = std::max(KMAX_AOT, std::min(KTILE, atoi(env)));

@@ -12,7 +12,7 @@ import math
 import numpy as np
 
 OP_DIAG_E, OP_DIAG_Z, OP_X, OP_BFLY = 1, 2, 3, 4
-ST_PASS, ST_GROW, ST_SHRINK = 0, 1, 2
+ST_PASS, ST_GROW, ST_SHRINK, ST_SWAP, ST_RHOK, ST_SHRINKK = 0, 1, 2, 3, 4, 5
 RED_NONE, RED_NORM, RED_RHO = 0, 1, 2
 
 
@@ -85,6 +85,64 @@ class Interp:
         self.prob0[ms.ord] = P0
         loc[ms.ord] = outc
         return U
+
+    def _joint(self, d, v):
+        """ST_SHRINKK: decide jk outcomes in order from rho (conditional Eq. 3 probabilities),
+        project and eliminate them at once; output bit t <- position d.j_src[t]."""
+        k, w = d.jk, d.width
+        R = getattr(self, "rhok", None)
+        R = None if R is None else R.copy()
+        loc, us, pj = {}, [], 1.0
+        for j in range(k):
+            ms = self.p.mst[d.jm[j]]
+            s = t = 0
+            if self.mode != 2:
+                s = self.parity(ms.s_off, ms.s_len, loc)
+                t = self.parity(ms.t_off, ms.t_len, loc)
+            theta = (-ms.alpha if s else ms.alpha) + (math.pi if t else 0.0)
+            e = complex(math.cos(theta), -math.sin(theta))
+            outc, P0 = 0, -1.0
+            if self.mode != 2:
+                tot = float(np.trace(R).real)
+                u0 = np.array([1, e]) / math.sqrt(2)
+                D = R.shape[0]
+                p0 = 0.0
+                for a2 in range(D // 2):
+                    blk = R[2 * a2:2 * a2 + 2, 2 * a2:2 * a2 + 2]
+                    p0 += (u0 @ blk @ u0.conj()).real
+                p0 = min(max(p0, 0.0), tot)
+                P0 = p0 / tot if tot > 0 else 0.0
+                outc = (0 if _draw(self.seed, ms.key) <= P0 else 1) if self.mode == 0 else int(self.forced[ms.ord]) & 1
+                pS = 1 - P0 if outc else P0
+                if pS < 1e-12:
+                    self.err = 1
+                    pS = 1.0
+                pj *= pS
+                u = np.array([1, -e if outc else e]) / math.sqrt(2)
+                D2 = D // 2
+                Rn = np.zeros((D2, D2), dtype=complex)
+                for a2 in range(D2):
+                    for b2 in range(D2):
+                        Rn[a2, b2] = u @ R[2 * a2:2 * a2 + 2, 2 * b2:2 * b2 + 2] @ u.conj()
+                R = Rn
+            sg = -1.0 if outc else 1.0
+            kk = 1.0 if self.mode == 2 else 1 / math.sqrt(2)
+            us.append(np.array([kk, kk * sg * e]))
+            self.outcome[ms.ord] = outc
+            self.prob0[ms.ord] = P0
+            loc[ms.ord] = outc
+        scale = 1.0 if self.mode == 2 else 1 / math.sqrt(pj)
+        cv = np.array([scale * np.prod([us[j][(x >> j) & 1] for j in range(k)]) for x in range(1 << k)])
+        wo = w - k
+        i = np.arange(1 << wo)
+        src = np.zeros_like(i)
+        for tb in range(wo):
+            src |= ((i >> tb) & 1) << d.j_src[tb]
+        out = np.zeros(1 << wo, dtype=complex)
+        for x in range(1 << k):
+            off = sum(((x >> j) & 1) << d.jm_pos[j] for j in range(k))
+            out += cv[x] * v[src | off]
+        return out, cv
 
     def _allreduce(self):
         if self.world > 1:
@@ -163,6 +221,20 @@ class Interp:
                     cur = st[:n].copy()
                     st[dst] = cur
                 if d.red_kind != RED_NONE:
+                    self._allreduce()
+            elif d.kind == ST_RHOK:  # reduced density matrix of the jk measured positions
+                k = d.jk
+                pos = [d.jm_pos[j] for j in range(k)]
+                idx = np.arange(n)
+                rest = idx[np.all([((idx >> q) & 1) == 0 for q in pos], axis=0)]
+                V = np.stack([st[rest | sum(((x >> j) & 1) << pos[j] for j in range(k))] for x in range(1 << k)])
+                self.rhok = V @ V.conj().T  # rho[a][b] = sum_rest v_a conj(v_b)
+            elif d.kind == ST_SHRINKK:
+                st_new, cv = self._joint(d, st[:n])
+                m = st_new.size
+                st[:m] = st_new
+                if d.red_kind == RED_NORM:
+                    self.red[:] = [np.vdot(st[:m], st[:m]).real, 0, 0, 0]
                     self._allreduce()
             elif d.kind == ST_GROW:
                 x = st[:n] / math.sqrt(2)

@@ -260,3 +260,54 @@ def test_unnormalised_input_refused(require_gpu, prec):
         assert e.value.status_name == "OWQS_E_ARG"
     finally:
         b.close()
+
+
+@pytest.mark.parametrize("shape", ["BWM:16x20x7", "BWM:18x12x6", "BWM:14x6x5"])
+def test_measured_tail_vs_oracle(require_gpu, shape):
+    """Config 3M's family: a brickwork whose last k wires are measured after the last layer --
+    SHRINK steps (Eq. 13 rho reduction in the previous pass, Fig. 6 compaction) that follow
+    qubit-remapped tile passes (the packer maps the emitter's slots through the remap), both
+    precisions, sampled and forced."""
+    p = W.config_pattern(shape, seed=2)
+    psi = haar_state(len(p.inputs), 3)
+    for prec in (128, 64):
+        s = Simulator(precision=prec)
+        try:
+            # the tail measurements commute and PROA may order them differently from the given
+            # list: per-M prob0 differ (reading R-8), the joint branch probability and output do not
+            check(s, p, psi, "sampled", seed=5, same_order=False)
+            _both_refuse_or_check(s, p, psi, np.random.default_rng(4).integers(0, 2, p.n_measure))
+        finally:
+            s.close()
+
+
+@pytest.mark.parametrize("shape", ["BWM:14x6x5", "BWM:12x4x4"])
+def test_joint_measurement_matches_sequential(require_gpu, monkeypatch, shape):
+    """Joint k-outcome sampling (ST_RHOK + ST_SHRINKK): consecutive eliminations
+    decided from one reduced density matrix give the same outcome strings, per-M prob0 and outputs as
+    the same program with one SHRINK per measurement (OWQS_JOINT_K=1) and as the oracle, in fewer
+    passes."""
+    from paper_1604_05659_b200.host import compile_host
+    p = W.config_pattern(shape, seed=2)
+    psi = haar_state(len(p.inputs), 3)
+    joint = compile_host(p, "sampled", 128)
+    assert any(s.kind == 5 for s in joint.steps)
+    res = {}
+    for jk in ("3", "1"):
+        monkeypatch.setenv("OWQS_JOINT_K", jk)
+        for prec in (128, 64):
+            s = Simulator(precision=prec)
+            try:
+                out, _ = check(s, p, psi, "sampled", seed=7, same_order=False)
+                s.load(p)
+                s.set_input(psi)
+                outc, p0 = s.run("sampled", seed=7)
+                res[(jk, prec)] = (out, outc, p0, s.stats()["n_launches"])
+            finally:
+                s.close()
+    for prec in (128, 64):
+        a, b = res[("3", prec)], res[("1", prec)]
+        assert list(a[1]) == list(b[1])
+        assert np.max(np.abs(a[2] - b[2])) <= TOL[prec]["prob"]
+        assert np.max(np.abs(a[0] - b[0])) <= TOL[prec]["amp"]
+        assert a[3] < b[3]  # fewer launches

@@ -312,6 +312,11 @@ def config_pattern(name: str, seed: int = 1) -> Pattern:
         p = circuit_to_pattern(33, brickwork_circuit(33, 24, seed), "C4")
     elif name == "C5":
         p = cluster_pattern(35, 8, seed)
+    elif name == "C3M":
+        p = measured_tail(circuit_to_pattern(28, brickwork_circuit(28, 40, seed), "C3M"), 8, seed)
+    elif name.startswith("BWM:"):
+        n, d, k = (int(x) for x in name[4:].split("x"))
+        p = measured_tail(circuit_to_pattern(n, brickwork_circuit(n, d, seed), name), k, seed)
     elif name.startswith("QFT:"):
         n = int(name[4:])
         p = circuit_to_pattern(n, qft_circuit(n), name)
@@ -326,6 +331,16 @@ def config_pattern(name: str, seed: int = 1) -> Pattern:
         raise KeyError(name)
     p.meta["seed"] = seed
     return p
+
+
+def measured_tail(p: Pattern, k: int, seed: int) -> Pattern:
+    """Measure the last k output qubits of a circuit pattern in the XY plane (angles ~ U[0, 2pi)) after
+    its last command: measurements with no fresh neighbour, so each eliminates a qubit from the state
+    (SHRINK, Eq. 13 reduction, Fig. 6 compaction) -- the SHRINK-heavy workload C3M (config 3 with 8 of
+    its 28 wires read out)."""
+    rng = np.random.default_rng(10_000 + seed)
+    tail = [M(q, float(rng.uniform(0, 2 * math.pi))) for q in p.outputs[len(p.outputs) - k:]]
+    return Pattern(list(p.inputs), list(p.outputs[:len(p.outputs) - k]), list(p.cmds) + tail, p.name)
 
 
 def random_general_pattern(seed: int, n_in: int = 2, n_total: int = 9, n_out: int = 2,
