@@ -423,8 +423,11 @@ struct Gen {
   }
   std::string cond_expr(int i) const { return (tile ? PC + "cond[" : std::string("sh.cond[")) + std::to_string(i) + "]"; }
 
+  // own-tile L2 bulk prefetch before griddepcontrol.wait: off by default since the kernels stopped
+  // being instruction-fetch bound (ptxas -O1, tile planning): C3 34.48 -> 33.96 ms without it
+  // (OWQS_PDL_PREFETCH=1: on)
   static bool pdl_prefetch() {
-    static const bool v = !(getenv("OWQS_PDL_PREFETCH") && atoi(getenv("OWQS_PDL_PREFETCH")) == 0);
+    static const bool v = getenv("OWQS_PDL_PREFETCH") && atoi(getenv("OWQS_PDL_PREFETCH")) != 0;
     return v;
   }
   static int prefetch_distance() {
@@ -1470,7 +1473,7 @@ struct Gen {
     // after griddepcontrol.wait, so every read of the state (and of PassCoef) comes after it. Before
     // the wait, lane m < 16 of each warp bulk-prefetches its m-th 512 B load segment into L2 -- L2
     // is the point of coherence, so a prefetched line can never be older than the writer's store
-    // (OWQS_PDL_PREFETCH=0: off).
+    // (off by default, OWQS_PDL_PREFETCH=1).
     if (!small) {
       if (pdl_prefetch()) {
         o << "    if (lane < 16) {\n      const unsigned long long ap = 0ull";
@@ -1605,8 +1608,20 @@ std::string compile_tu(const std::string& src, std::vector<char>& cubin) {
   nvrtcProgram prog;
   nvrtcResult r = nv.create(&prog, src.c_str(), "owqs_pass_jit.cu", 0, nullptr, nullptr);
   if (r != NVRTC_SUCCESS) return std::string("nvrtcCreateProgram: ") + nv.errstr(r);
-  const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOWQS_JIT=1"};
-  r = nv.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOWQS_JIT=1"};
+  // ptxas -O1 by default: at -O2/-O3 ptxas interleaves the butterflies of a phase and
+  // rematerialises every coefficient load per use (C3 heavy pass: 582 LDCU, 3152 instructions =
+  // 50 KB of SASS, instruction-cache hit rate 63 %, "no instruction" the top warp stall); -O1 keeps
+  // 49 LDCU, 2632 instructions: C3 37.6 -> 36.0 ms, C3W 171.4 -> 164.5 ms. OWQS_PTXAS overrides
+  // ("default" = ptxas' own level).
+  static const std::string ptxas = [] {
+    const char* e = getenv("OWQS_PTXAS");
+    if (!e) return std::string("-O1");
+    return std::string(strcmp(e, "default") ? e : "");
+  }();
+  const std::string ptxas_opt = "--ptxas-options=" + ptxas;
+  if (!ptxas.empty()) opts.push_back(ptxas_opt.c_str());
+  r = nv.compile(prog, (int)opts.size(), opts.data());
   std::string err;
   if (r != NVRTC_SUCCESS) {
     size_t n = 0;

@@ -693,6 +693,43 @@ struct Packer {
     }
   }
 
+  // End of a pass with tile planning: choose the next pass's tile (plan_tile, limited to kmax qubits
+  // outside this pass's tile), then remap -- segment positions whose qubit is not in the next tile
+  // take next-tile qubits from this pass's group positions -- and return the next pass's group
+  // positions (after the remap).
+  template <typename PlanTile>
+  void plan_next(StepDesc& cur, std::vector<char>& in_t, PlanTile& plan_tile, std::vector<int>& planned) {
+    const int WL = wl();
+    std::vector<char> prev(64, 0);
+    for (int p = 0; p < SB && p < WL; ++p) prev[at[p]] = 1;
+    for (int j = 0; j < cur.nb_hi; ++j) prev[at[cur.bhi[j]]] = 1;
+    std::fill(in_t.begin(), in_t.end(), 0);
+    const int p0 = SB == 6 ? 1 : 0;  // complex64 keeps slot 0 (float4 pairs): its qubit stays
+    if (p0 == 1) in_t[at[0]] = 1;
+    plan_tile(&prev);
+    cur.n_remap = 0;
+    if (cur.n_ops > 0) {  // a read-only pass has no store to remap
+      std::vector<int> dead, live;
+      for (int p = p0; p < SB && p < WL; ++p)
+        if (!in_t[at[p]]) dead.push_back(p);
+      for (int j = 0; j < cur.nb_hi; ++j)
+        if (in_t[at[cur.bhi[j]]]) live.push_back(cur.bhi[j]);
+      for (size_t k = 0; k < dead.size() && k < live.size() && k < 6; ++k) {
+        const int a = live[k], b = dead[k];
+        cur.remap_a[cur.n_remap] = a;
+        cur.remap_b[cur.n_remap] = b;
+        ++cur.n_remap;
+        const int va = at[a], vb = at[b];
+        std::swap(pos[va], pos[vb]);
+        at[pos[va]] = va;
+        at[pos[vb]] = vb;
+      }
+    }
+    planned.clear();
+    for (int p = SB; p < WL; ++p)
+      if (in_t[at[p]]) planned.push_back(p);
+  }
+
   // group slots allowed in a pass of (shard) width w
   int wide_at(int w) const { return (kwide > KMAX_AOT && w >= SB + kwide) ? kwide : kmax_hi; }
   // last step that computes something (a SWAP only permutes: it preserves the norm)
@@ -812,6 +849,7 @@ struct Packer {
       int npred = 0;
       std::vector<int> succ;
       bool done = false;
+      int lev = 0;  // butterflies / X on the longest dependency path to this node
     };
     std::vector<Node> nodes;
     std::vector<int> last_write(64, -1);
@@ -881,8 +919,21 @@ struct Packer {
       std::sort(P.begin(), P.end());
       P.erase(std::unique(P.begin(), P.end()), P.end());
       nodes[i].npred = (int)P.size();
-      for (int p : P) nodes[p].succ.push_back(i);
+      for (int p : P) {
+        nodes[p].succ.push_back(i);
+        const int t = ops[nodes[p].op].type;
+        nodes[i].lev = std::max(nodes[i].lev, nodes[p].lev + ((t == 3 || t == 4) ? 1 : 0));
+      }
     }
+    // Pick order inside a pass: dependency level first (a wavefront: fronts stay flat, so later
+    // passes keep finding deep light cones), then stream order. Stream order alone (OWQS_LEVEL_PRIO=0)
+    // follows PROA's measurement sweep, which on C3 builds a slope-1 staircase across all wires
+    // that every later pass can only shift by two layers.
+    static const bool level_prio = !(getenv("OWQS_LEVEL_PRIO") && atoi(getenv("OWQS_LEVEL_PRIO")) == 0);
+    auto before = [&](int a, int b) {
+      if (level_prio && nodes[a].lev != nodes[b].lev) return nodes[a].lev < nodes[b].lev;
+      return nodes[a].op < nodes[b].op;
+    };
     std::vector<int> ready;
     for (int i = 0; i < N; ++i)
       if (nodes[i].npred == 0) ready.push_back(i);
@@ -893,6 +944,88 @@ struct Packer {
     const bool wide = wide_at(wl()) > KMAX_AOT;
     const int kmax = wide_at(wl());
     const int lane_cap = max_lane_bfly > 0 ? max_lane_bfly : (!wide && wl() + (SB == 6 ? 3 : 4) >= 28 ? 4 : 64);
+    // Tile planning (tile-engine passes; OWQS_SLOT_PICK=0: first-come slots + stream-order remap).
+    // A pass's tile is the SB segment positions plus kmax group positions. The planner grows the
+    // NEXT pass's tile qubit by qubit, each time adding the qubit that lets that pass run the most
+    // butterflies (a dry run of the list scheduler restricted to the candidate tile; ties: the qubit
+    // whose next 2x2 is earliest in the wavefront). It runs at the end of a pass, where the store's
+    // remap can still move up to kmax of this pass's tile qubits into the segment, so the next tile
+    // may hold at most kmax qubits from outside this pass's tile. First-come group slots plus a
+    // stream-order remap made C3 a slope-1 staircase front (17 of 38 passes with 12-25 butterflies).
+    static const bool slot_pick = !(getenv("OWQS_SLOT_PICK") && atoi(getenv("OWQS_SLOT_PICK")) == 0);
+    std::vector<int> touched;
+    std::vector<char> in_t(64, 0);  // dry-run tile, by virtual slot
+    auto dry_run = [&](int* n_ops_out) {
+      std::vector<int> rdy = ready;
+      int n_ops = 0, n_bfly = 0;
+      const int WL = wl();
+      touched.clear();
+      while (2 * n_ops + 2 <= MAX_OPS) {
+        int best = -1;
+        for (int k = 0; k < (int)rdy.size(); ++k) {
+          const Node& n = nodes[rdy[k]];
+          const LOp& l = ops[n.op];
+          if (l.type == 4 && n_bfly >= max_bfly) continue;
+          const bool diag = l.type == 1 || l.type == 2;
+          if (!diag && (pos[l.a] >= WL || !in_t[l.a])) continue;
+          if (best < 0 || before(rdy[k], rdy[best])) best = k;
+        }
+        if (best < 0) break;
+        const int id = rdy[best];
+        rdy[best] = rdy.back();
+        rdy.pop_back();
+        ++n_ops;
+        if (ops[nodes[id].op].type == 4) ++n_bfly;
+        for (int s : nodes[id].succ) {
+          touched.push_back(s);
+          if (--nodes[s].npred == 0) rdy.push_back(s);
+        }
+      }
+      for (int s : touched) ++nodes[s].npred;
+      if (n_ops_out) *n_ops_out = n_ops;
+      return n_bfly;
+    };
+    // grow the tile in_t (already holding `fixed`) to SB + kmax qubits; prev: the qubits the previous
+    // pass held (nullptr: no limit), at most kmax of the result may lie outside it
+    auto plan_tile = [&](const std::vector<char>* prev) {
+      const int WL = wl();
+      std::vector<int> next_node(64, -1);  // first not-done 2x2 node per virtual slot
+      for (int i = 0; i < (int)nodes.size(); ++i)
+        if (!nodes[i].done) {
+          const LOp& l = ops[nodes[i].op];
+          if ((l.type == 3 || l.type == 4) && next_node[l.a] < 0) next_node[l.a] = i;
+        }
+      int n_in = 0, n_out = 0;
+      for (int v = 0; v < 64; ++v)
+        if (in_t[v]) {
+          ++n_in;
+          if (prev && !(*prev)[v]) ++n_out;
+        }
+      while (n_in < SB + kmax) {
+        int best = -1, best_b = -1, best_o = -1;
+        for (int p = 0; p < WL; ++p) {
+          const int v = at[p];
+          if (in_t[v] || next_node[v] < 0) continue;
+          const bool out = prev && !(*prev)[v];
+          if (out && n_out >= kmax) continue;
+          in_t[v] = 1;
+          int o = 0;
+          const int b = dry_run(&o);
+          in_t[v] = 0;
+          if (best >= 0 && (b < best_b || (b == best_b && o < best_o))) continue;
+          if (best >= 0 && b == best_b && o == best_o && !before(next_node[v], next_node[best])) continue;
+          best = v;
+          best_b = b;
+          best_o = o;
+        }
+        if (best < 0) break;
+        in_t[best] = 1;
+        ++n_in;
+        if (prev && !(*prev)[best]) ++n_out;
+      }
+    };
+    std::vector<int> planned;  // group positions chosen for the next pass (valid when have_plan)
+    bool have_plan = false;
     while (remaining > 0) {
       StepDesc cur = blank(ST_PASS);
       int n_lane = 0;
@@ -903,6 +1036,20 @@ struct Packer {
           if (cur.bhi[j] == a) return true;
         return false;
       };
+      if (wide && slot_pick) {
+        if (!have_plan) {  // first pass of a segment: the segment qubits are given
+          std::fill(in_t.begin(), in_t.end(), 0);
+          for (int p = 0; p < SB && p < WL; ++p) in_t[at[p]] = 1;
+          plan_tile(nullptr);
+          planned.clear();
+          for (int p = SB; p < WL; ++p)
+            if (in_t[at[p]]) planned.push_back(p);
+        }
+        have_plan = false;
+        for (int p : planned)
+          if ((int)cur.nb_hi < kmax) cur.bhi[cur.nb_hi++] = p;
+        std::sort(cur.bhi, cur.bhi + cur.nb_hi);
+      }
       while (true) {
         if (2 * cur.n_ops + 2 > MAX_OPS) break;  // room for the FLUSH ops inserted afterwards
         // pick: (1) fits without a new slot, lowest stream index; (2) needs a new slot
@@ -916,9 +1063,9 @@ struct Packer {
           if (!diag && pos[l.a] >= WL) continue;  // 2x2 on a rank bit: needs a SWAP first
           bool fits = diag || has_slot(pos[l.a]);
           if (fits) {
-            if (best < 0 || n.op < nodes[ready[best]].op) best = k;
+            if (best < 0 || before(ready[k], ready[best])) best = k;
           } else if (cur.nb_hi < kmax) {
-            if (best_new < 0 || n.op < nodes[ready[best_new]].op) best_new = k;
+            if (best_new < 0 || before(ready[k], ready[best_new])) best_new = k;
           }
         }
         int pick = best >= 0 ? best : best_new;
@@ -993,7 +1140,12 @@ struct Packer {
       // OWQS_FLAG_MEASURED_NORM keeps the reduction (tests check the reading with it at full width).
       if (cur.first_uses_red && (!measured_norm || !need_norm_before())) cur.first_uses_red = 0;
       absorb_and_flush(cur);
-      if (remap && wide) plan_remap(cur, nodes);
+      if (remap && wide && slot_pick && remaining > 0) {
+        plan_next(cur, in_t, plan_tile, planned);
+        have_plan = true;
+      } else if (remap && wide) {
+        plan_remap(cur, nodes);
+      }
       emit(cur);
     }
   }
