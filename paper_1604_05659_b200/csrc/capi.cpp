@@ -31,6 +31,7 @@ cudaError_t launch_basis(void* state, int prec, uint64_t n, uint64_t k, cudaStre
 cudaError_t launch_haar(const DevPtrs& p, int prec, uint64_t n, uint64_t seed, uint64_t j0, cudaStream_t s);
 cudaError_t launch_scale(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
 cudaError_t launch_norm(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s);
+cudaError_t launch_readback(void* host_dst, const void* dev_src, size_t n, cudaStream_t s);
 cudaError_t launch_sample_out(const void* shard, int prec, const int64_t* idx, uint64_t n, int nbits, const int* slots,
                               uint64_t rank, int wl, void* out, cudaStream_t s);
 cudaError_t launch_copy_norm(const DevPtrs& p, int prec, const void* src, uint64_t n, cudaStream_t s);
@@ -166,7 +167,8 @@ double kernels_per_run(const owqs_ctx* ctx, const CompiledMode& m) {
         !jit_tile_small(s, ctx->prec))  // decide (not in EOWQS runs after the first) + grid finish
       n += (m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE") ? 0 : 1) + (s.red_kind != RED_NONE ? 1 : 0);
   }
-  return n;
+  // the run's readbacks (launch_readback: error flag per shard, outcomes + prob0, reduction)
+  return n + 1.0 + ((ctx->hp.n_measure > 0 ? 2.0 : 0.0) + 1.0) / (double)std::max<size_t>(1, ctx->shards.size());
 }
 
 owqs_status fail(owqs_ctx* c, owqs_status s, const std::string& m) {
@@ -631,18 +633,19 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
     if (st != OWQS_OK) return st;
   }
   CU(cudaEventRecord(ctx->ev1, ctx->stream));
-  // error flags to page-locked memory in stream order (a synchronous 4-byte cudaMemcpy after the
-  // run would queue in the copy engine behind other contexts' multi-GiB output transfers)
+  // error flags, outcomes, prob0 and the reduction to page-locked memory in stream order, written by
+  // a one-CTA kernel (launch_readback): a copy-engine D2H would queue behind other contexts'
+  // multi-GiB output transfers
   for (size_t r = 0; r < ctx->shards.size(); ++r)
-    CU(cudaMemcpyAsync(ctx->h_err + r, ctx->shards[r].d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(launch_readback(ctx->h_err + r, ctx->shards[r].d_err, sizeof(int32_t), ctx->stream));
   {
     uint8_t* hs = static_cast<uint8_t*>(ctx->h_staging);
     const int64_t K = ctx->hp.n_measure;
     if (K > 0) {
-      CU(cudaMemcpyAsync(hs + rs.outcomes, ctx->d_outcome, K, cudaMemcpyDeviceToHost, ctx->stream));
-      CU(cudaMemcpyAsync(hs + rs.prob0, ctx->d_prob0, K * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      CU(launch_readback(hs + rs.outcomes, ctx->d_outcome, K, ctx->stream));
+      CU(launch_readback(hs + rs.prob0, ctx->d_prob0, K * sizeof(double), ctx->stream));
     }
-    CU(cudaMemcpyAsync(hs + rs.red, ctx->shards[0].d_red, 4 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CU(launch_readback(hs + rs.red, ctx->shards[0].d_red, 4 * sizeof(double), ctx->stream));
   }
   ctx->has_input = false;
   ctx->out_cm = cmi;
@@ -1131,7 +1134,7 @@ owqs_status input_norm_enqueue(owqs_ctx* ctx, bool reduced) {
       CU(launch_norm(dev_ptrs(ctx, ctx->cm[0], (int)r), ctx->prec, per, ctx->stream));
   owqs_status s = allreduce_red(ctx);
   if (s != OWQS_OK) return s;
-  CU(cudaMemcpyAsync(ctx->h_innorm, ctx->shards[0].d_red, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  CU(launch_readback(ctx->h_innorm, ctx->shards[0].d_red, sizeof(double), ctx->stream));
   return OWQS_OK;
 }
 

@@ -1865,6 +1865,22 @@ __global__ void __launch_bounds__(256) norm_kernel(DevPtrs p, uint64_t n) {
   reduce_finish<1>(acc, p, sh);
 }
 
+// Small readbacks (error flags, outcomes, prob0, reductions, the input norm) into page-locked host
+// memory written by the SMs over PCIe (UVA: cudaMallocHost memory is mapped at the same address)
+// instead of a copy-engine cudaMemcpyAsync: a D2H copy queues behind other contexts' multi-GiB
+// output DMAs in the copy engine, and everything behind it on this stream (the run after the input
+// norm check, the output permutation) waits with it (e2e pipeline: 69.9 ms per C3 step).
+__global__ void readback_kernel(unsigned char* dst, const unsigned char* src, size_t n) {
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+
+cudaError_t launch_readback(void* host_dst, const void* dev_src, size_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  readback_kernel<<<1, 256, 0, s>>>(static_cast<unsigned char*>(host_dst), static_cast<const unsigned char*>(dev_src), n);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_norm(const DevPtrs& p, int prec, uint64_t n, cudaStream_t s) {
   if (prec == 0) norm_kernel<float><<<elem_blocks(n), 256, 0, s>>>(p, n);
   else norm_kernel<double><<<elem_blocks(n), 256, 0, s>>>(p, n);
