@@ -701,32 +701,60 @@ __global__ void __launch_bounds__(256) rhok_kernel(const StepDesc d, const DevPt
   constexpr int D = 1 << K, NV = 2 * (D * (D + 1) / 2);
   const C* st = reinterpret_cast<const C*>(p.state);
   const int w = d.width;
-  int32_t rest[64];
-  uint64_t mmask = 0;
-  for (int j = 0; j < K; ++j) mmask |= 1ull << d.jm_pos[j];
-  for (int b = 0, q = 0; b < w; ++b)
-    if (!((mmask >> b) & 1)) rest[q++] = b;
+  // rest index r -> state index: a zero bit inserted at each measured position, ascending (O(K) per
+  // element; the K measured offsets are per-thread constants)
+  int hole[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) hole[j] = d.jm_pos[j];
+#pragma unroll
+  for (int a = 0; a < K; ++a)
+#pragma unroll
+    for (int b = a + 1; b < K; ++b)
+      if (hole[b] < hole[a]) {
+        const int t = hole[a];
+        hole[a] = hole[b];
+        hole[b] = t;
+      }
+  uint64_t moff[D];
+#pragma unroll
+  for (int x = 0; x < D; ++x) moff[x] = pdep_pos((uint64_t)x, d.jm_pos, K);
   double acc[NV];
 #pragma unroll
   for (int v = 0; v < NV; ++v) acc[v] = 0.0;
   const uint64_t nrest = 1ull << (w - K);
-  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < nrest; r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t base = pdep_pos(r, rest, w - K);
-    double vr[D], vi[D];
+  // U rest indices per thread and iteration (a grid stride apart), all loads issued before the
+  // arithmetic: U * D independent 8 / 16 B loads in flight per thread (K <= 2; K = 3 keeps U = 1:
+  // its 72 fp64 accumulators already fill the register file)
+  constexpr int U = K <= 2 ? 4 : 1;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t r0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r0 < nrest; r0 += U * stride) {
+    C v[U][D];
 #pragma unroll
-    for (int x = 0; x < D; ++x) {
-      const C a = st[base | pdep_pos((uint64_t)x, d.jm_pos, K)];
-      vr[x] = (double)a.x;
-      vi[x] = (double)a.y;
+    for (int u = 0; u < U; ++u) {
+      const uint64_t r = r0 + u * stride;
+      uint64_t base = r < nrest ? r : r0;
+#pragma unroll
+      for (int j = 0; j < K; ++j) base = ((base >> hole[j]) << (hole[j] + 1)) | (base & ((1ull << hole[j]) - 1));
+#pragma unroll
+      for (int x = 0; x < D; ++x) v[u][x] = r < nrest ? st[base | moff[x]] : make_c<T>((T)0, (T)0);
     }
-    int e = 0;
 #pragma unroll
-    for (int a = 0; a < D; ++a)
+    for (int u = 0; u < U; ++u) {
+      double vr[D], vi[D];
 #pragma unroll
-      for (int b = a; b < D; ++b) {
-        acc[e++] += vr[a] * vr[b] + vi[a] * vi[b];  // Re v[a] conj(v[b])
-        acc[e++] += vi[a] * vr[b] - vr[a] * vi[b];  // Im
+      for (int x = 0; x < D; ++x) {
+        vr[x] = (double)v[u][x].x;
+        vi[x] = (double)v[u][x].y;
       }
+      int e = 0;
+#pragma unroll
+      for (int a = 0; a < D; ++a)
+#pragma unroll
+        for (int b = a; b < D; ++b) {
+          acc[e++] += vr[a] * vr[b] + vi[a] * vi[b];  // Re v[a] conj(v[b])
+          acc[e++] += vi[a] * vr[b] - vr[a] * vi[b];  // Im
+        }
+    }
   }
   __shared__ double red[8][NV];
   __shared__ int last;
@@ -869,36 +897,82 @@ __device__ void joint_decide(const StepDesc& d, const DevPtrs& p, bool record, d
   }
 }
 
-template <typename T>
+template <typename T, int K>
 __global__ void __launch_bounds__(256) shrinkk_kernel(const StepDesc d, const DevPtrs p) {
   typedef typename VT<T>::C C;
+  constexpr int D = 1 << K, MV = 2 * JOINT_KMAX;
   __shared__ double cv[1 << JOINT_KMAX][2];
   __shared__ PassShared sh;
   if (threadIdx.x == 0) joint_decide(d, p, blockIdx.x == 0, cv, p.partials + RHOK_RESULT_OFF);
   __syncthreads();
-  const int K = d.jk, w = d.width, wo = w - K;
+  const int w = d.width, wo = w - K;
   const C* st = reinterpret_cast<const C*>(p.state);
   C* out = reinterpret_cast<C*>(p.scratch);
-  T cr[1 << JOINT_KMAX], ci[1 << JOINT_KMAX];
-  uint64_t moff[1 << JOINT_KMAX];
-  for (int x = 0; x < (1 << K); ++x) {
+  T cr[D], ci[D];
+  uint64_t moff[D];
+#pragma unroll
+  for (int x = 0; x < D; ++x) {
     cr[x] = (T)cv[x][0];
     ci[x] = (T)cv[x][1];
     moff[x] = pdep_pos((uint64_t)x, d.jm_pos, K);
   }
+  // output bit t comes from source position j_src[t]: identity except for the <= 2K bits the
+  // eliminations moved (the top qubits into freed positions) -- a keep mask plus a short list
+  uint64_t keep = 0;
+  int nmv = 0, mv_t[MV], mv_s[MV];
+#pragma unroll
+  for (int q = 0; q < MV; ++q) mv_t[q] = mv_s[q] = 0;
+  bool general = false;
+  for (int t = 0; t < wo; ++t) {
+    if (d.j_src[t] == t) {
+      keep |= 1ull << t;
+      continue;
+    }
+#pragma unroll
+    for (int q = 0; q < MV; ++q)
+      if (q == nmv) {
+        mv_t[q] = t;
+        mv_s[q] = d.j_src[t];
+      }
+    if (nmv < MV) ++nmv;
+    else general = true;
+  }
   double acc[4] = {0, 0, 0, 0};
   const uint64_t n = 1ull << wo;
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    uint64_t src = 0;
-    for (int t = 0; t < wo; ++t) src |= ((i >> t) & 1ull) << d.j_src[t];
-    T orr = 0, oi = 0;
-    for (int x = 0; x < (1 << K); ++x) {
-      const C a = st[src | moff[x]];
-      orr += cr[x] * a.x - ci[x] * a.y;
-      oi += cr[x] * a.y + ci[x] * a.x;
+  // U output elements per thread and iteration (a grid stride apart), every load issued before the
+  // arithmetic (U * D independent loads in flight per thread)
+  constexpr int U = K <= 2 ? 4 : 2;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += U * stride) {
+    C v[U][D];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride < n ? i0 + u * stride : i0;
+      uint64_t src = i & keep;
+      if (!general) {
+#pragma unroll
+        for (int q = 0; q < MV; ++q)
+          if (q < nmv) src |= ((i >> mv_t[q]) & 1ull) << mv_s[q];
+      } else {
+        src = 0;
+        for (int t = 0; t < wo; ++t) src |= ((i >> t) & 1ull) << d.j_src[t];
+      }
+#pragma unroll
+      for (int x = 0; x < D; ++x) v[u][x] = st[src | moff[x]];
     }
-    out[i] = make_c<T>(orr, oi);
-    acc[0] += (double)orr * orr + (double)oi * oi;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i >= n) break;
+      T orr = 0, oi = 0;
+#pragma unroll
+      for (int x = 0; x < D; ++x) {
+        orr += cr[x] * v[u][x].x - ci[x] * v[u][x].y;
+        oi += cr[x] * v[u][x].y + ci[x] * v[u][x].x;
+      }
+      out[i] = make_c<T>(orr, oi);
+      acc[0] += (double)orr * orr + (double)oi * oi;
+    }
   }
   if (d.red_kind == RED_NORM) reduce_finish<1>(acc, p, sh);
 }
@@ -1627,8 +1701,12 @@ cudaError_t launch_step(const StepDesc& d, const DevPtrs& p, int prec, cudaStrea
 #undef OWQS_RK
       return cudaGetLastError();
     }
-    if (prec == 0) shrinkk_kernel<float><<<blocks, 256, 0, s>>>(d, p);
-    else shrinkk_kernel<double><<<blocks, 256, 0, s>>>(d, p);
+#define OWQS_SK(TT) \
+  switch (d.jk) { case 1: shrinkk_kernel<TT, 1><<<blocks, 256, 0, s>>>(d, p); break; \
+                  case 2: shrinkk_kernel<TT, 2><<<blocks, 256, 0, s>>>(d, p); break; \
+                  default: shrinkk_kernel<TT, 3><<<blocks, 256, 0, s>>>(d, p); break; }
+    if (prec == 0) { OWQS_SK(float) } else { OWQS_SK(double) }
+#undef OWQS_SK
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return cudaMemcpyAsync(p.state, p.scratch, (size_t)(prec == 0 ? 8 : 16) << (d.width - d.jk), cudaMemcpyDeviceToDevice, s);
