@@ -1609,15 +1609,16 @@ std::string compile_tu(const std::string& src, std::vector<char>& cubin) {
   nvrtcResult r = nv.create(&prog, src.c_str(), "owqs_pass_jit.cu", 0, nullptr, nullptr);
   if (r != NVRTC_SUCCESS) return std::string("nvrtcCreateProgram: ") + nv.errstr(r);
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DOWQS_JIT=1"};
-  // ptxas -O1 by default: at -O2/-O3 ptxas interleaves the butterflies of a phase and
-  // rematerialises every coefficient load per use (C3 heavy pass: 582 LDCU, 3152 instructions =
-  // 50 KB of SASS, instruction-cache hit rate 63 %, "no instruction" the top warp stall); -O1 keeps
-  // 49 LDCU, 2632 instructions: C3 37.6 -> 36.0 ms, C3W 171.4 -> 164.5 ms. OWQS_PTXAS overrides
-  // ("default" = ptxas' own level).
+  // ptxas options (OWQS_PTXAS, e.g. "-O1"; default: ptxas' own -O3). Found on C3's heavy passes:
+  // with the own-tile L2 prefetch (asm volatile, memory clobber) ahead of griddepcontrol.wait, -O3
+  // rematerialised every coefficient load per use (582 LDCU, 3152 instructions = 50 KB of SASS,
+  // instruction-cache hit rate 63 %, "no instruction" 46 % of the warp-stall samples); -O1 kept 49
+  // LDCU / 2632 instructions (C3 37.6 -> 36.0 ms). Without that prefetch (now off by default) -O1
+  // and -O3 emit the same SASS for C3's tile kernels (tools/jit_dump.py + cuobjdump), and -O3 is
+  // 2 % faster on C4's several-tiles-per-CTA kernels (793 vs 811 ms).
   static const std::string ptxas = [] {
     const char* e = getenv("OWQS_PTXAS");
-    if (!e) return std::string("-O1");
-    return std::string(strcmp(e, "default") ? e : "");
+    return std::string(e && strcmp(e, "default") ? e : "");
   }();
   const std::string ptxas_opt = "--ptxas-options=" + ptxas;
   if (!ptxas.empty()) opts.push_back(ptxas_opt.c_str());

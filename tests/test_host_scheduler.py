@@ -199,3 +199,46 @@ def test_substate_split_host():
     cross = W.Pattern(ci, co + [501], cc + [W.N(500), W.N(501), W.E(500, 501), W.M(500, 0.4, sdom=(ci[0],))])
     assert substates(cross) == []
     assert substates(W.config_pattern("C1", seed=1)) == []
+
+
+def _tile_invariants(hp, SB=6, kmax=6):
+    """Every 2x2 op of a tile-engine pass lies in its tile (segment positions or group slots), a
+    pass has at most kmax group slots, and a store remap only trades a group slot of the pass with
+    a segment position (complex64 keeps position 0)."""
+    for i, st in enumerate(hp.steps):
+        if st.kind != 0 or st.width < SB + kmax:
+            continue
+        grp = [st.bhi[j] for j in range(st.nb_hi)]
+        assert len(grp) <= kmax, i
+        for k in range(st.n_ops):
+            o = st.ops[k]
+            if o.type in (3, 4):
+                assert o.a < SB or o.a in grp, (i, o.a, grp)
+        for k in range(st.n_remap):
+            assert st.remap_a[k] in grp, i
+            assert (1 if SB == 6 else 0) <= st.remap_b[k] < SB, i
+
+
+def test_tile_planner_pass_counts_and_invariants():
+    """Tile planning (look-ahead tiles + matching store remap, wavefront pick order): config 3 in
+    at most 30 passes (38 with first-come slots), config 4 in at most 21 (34), each within the
+    tile-engine invariants."""
+    for name, cap in (("C3", 30), ("C3W", 31), ("C4", 21)):
+        hp = compile_host(W.config_pattern(name), "sampled", precision=64)
+        assert hp.info["n_passes"] <= cap, (name, hp.info["n_passes"])
+        assert sum(st.n_bfly for st in hp.steps) == hp.info["n_measure"]
+        _tile_invariants(hp)
+
+
+@pytest.mark.parametrize("shape,mode", [("BW:16x10", "sampled"), ("BW:15x12", "eowqs"), ("BW:16x8", "forced")])
+def test_tile_planned_program_vs_oracle(shape, mode):
+    """Programs whose passes are tile-planned and remapped (width >= 12, complex64) executed by the
+    interpreter equal the oracle: the planner's remaps and pick order keep the program exact."""
+    p = W.config_pattern(shape, seed=4)
+    n = len(p.inputs)
+    hp = compile_host(p, mode if mode != "forced" else "sampled", precision=64)
+    assert any(st.n_remap > 0 for st in hp.steps)
+    _tile_invariants(hp)
+    psi = haar_state(n, 11)
+    forced = np.random.default_rng(3).integers(0, 2, p.n_measure) if mode == "forced" else None
+    _compare(p, psi, mode, 0, 64, seed=7, forced=forced)
