@@ -261,7 +261,8 @@ def run_batched_c1(args, rank, world, local_rank):
             "e2e": {"value": value, "unit": "commands/s", "h2d_bytes_per_step": B * 8 * 16,
                     "d2h_bytes_per_step": B * 4 * 16},
             "gpu_launches": args.steps}
-    sim.close()
+    if sim is not None:
+        sim.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
@@ -305,9 +306,13 @@ def run_ours(args, rank, world, local_rank):
     load_s = time.perf_counter() - t0
     st = sim.stats()
 
-    big = (N * (8 if prec == 64 else 16)) > (32 << 30)  # > 32 GiB: no second full-size buffer
+    state_bytes = N * (8 if prec == 64 else 16)
+    big = state_bytes > (32 << 30)  # > 32 GiB: no host buffers (e2e / cpu_baseline skipped)
+    # resident input copy whenever a second full-size buffer fits (config 4: 2 x 64 GiB of 180 GB);
+    # otherwise the device counter-Haar generator runs inside every step
+    resident = not shard and (not big or 2 * state_bytes <= 0.8 * torch.cuda.get_device_properties(dev).total_memory)
     x = None
-    if not shard and not big:
+    if resident:
         # resident input: device Haar generator of the library, copied into a torch-owned buffer
         x = torch.empty(N, dtype=cdt, device=dev)
         gen = Simulator(precision=prec, device=local_rank, stream=stream.cuda_stream)
@@ -319,7 +324,7 @@ def run_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
 
     def set_input(s, i):
-        if shard or big:  # device counter-Haar input (a second 2^33+ state is not materialised)
+        if x is None:  # device counter-Haar input (a second full-size state does not fit)
             s.set_input_random(1 + i)
         else:
             s.set_input_device(x.data_ptr(), prec, N)
@@ -379,6 +384,11 @@ def run_ours(args, rank, world, local_rank):
     # (k a) x1: 4 packed ops per pair), 2 (norm) or 4 (rho) for the
     # probability reduction. Its roofline time is max(bytes / HBM peak, ops / FP32
     # peak); light passes are HBM-bound, heavy ones FP32-bound.
+    if big:  # make room for the profiling context's state
+        sim.close()
+        sim = None
+        x = None
+        torch.cuda.empty_cache()
     peak, peak_src = peaks()
     # FP32 (complex64) / FP64 (complex128) lanes x SMs x max SM clock (B200: 128 FP32, 64 FP64 lanes/SM)
     fp_lanes = 128 if prec == 64 else 64
@@ -421,9 +431,12 @@ def run_ours(args, rank, world, local_rank):
     fp = ops_sum / (ms_sum / 1e3)
     hbm_bound = t_mem.sum() >= t_fp.sum()
     traffic = ncu_traffic()
+    if traffic and (traffic.get("workload") != args.workload or traffic.get("precision") != prec or n_shards > 1):
+        traffic = None  # the committed capture is of another workload
+    # alu in TFLOP/s: a lane-op is one FMA (2 FLOP) of the FP32 (complex64) / FP64 (complex128) pipe
     roofline = {"bound": "hbm" if hbm_bound else "alu",
-                "achieved": bw if hbm_bound else fp / 1e12, "peak": peak if hbm_bound else fp_peak / 1e12,
-                "unit": "GB/s" if hbm_bound else "Tlane-op/s",
+                "achieved": bw if hbm_bound else 2 * fp / 1e12, "peak": peak if hbm_bound else 2 * fp_peak / 1e12,
+                "unit": "GB/s" if hbm_bound else "TFLOP/s",
                 "frac": bw / peak if hbm_bound else fp / fp_peak,
                 "traffic": (traffic or {}).get("dram_bytes_per_launch"),
                 "kernel": f"owqs::{KCLASS_NAMES[dom]}_kernel (generated tile kernels)", "launches": cnt,
@@ -434,6 +447,7 @@ def run_ours(args, rank, world, local_rank):
                 "hbm": {"achieved_gbs": bw, "peak_gbs": peak, "frac": bw / peak,
                         "roofline_ms": float(t_mem.sum())},
                 "alu": {"achieved_tops": fp / 1e12, "peak_tops": fp_peak / 1e12, "frac": fp / fp_peak,
+                        "achieved_tflops": 2 * fp / 1e12, "peak_tflops": 2 * fp_peak / 1e12,
                         "unit": ("FP32-pipe lane-ops/s (FFMA2/FMUL2/FADD2 count 2)" if prec == 64 else
                                  "FP64-pipe ops/s (DFMA/DMUL/DADD)"), "roofline_ms": float(t_fp.sum()),
                         "peak_source": f"derived: 148 SMs x {fp_lanes} FP{32 if prec == 64 else 64} lanes x 1965 MHz"},
@@ -549,7 +563,7 @@ def run_ours(args, rank, world, local_rank):
                    "launches_per_run": st["n_launches"], "state_bytes": N * (8 if prec == 64 else 16),
                    "l2": "state (>= 2 GiB) larger than the 126 MB L2: no flush needed",
                    "parallelism": par,
-                   "input": "device counter-Haar per step" if (shard or big) else "resident copy per step",
+                   "input": "resident copy per step" if resident else "device counter-Haar per step",
                    "load_pattern_s": load_s, "schedule_ms": st["schedule_ms"]},
         "hbm_gbs": hbm_gbs, "hbm_frac": hbm_gbs / peak,
         "hbm_aggregate": (dict(hbm_agg, frac=hbm_agg["gbs_per_gpu"] / peak, ranks=world,
