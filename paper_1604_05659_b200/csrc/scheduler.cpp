@@ -987,7 +987,8 @@ struct Packer {
     };
     // grow the tile in_t (already holding `fixed`) to SB + kmax qubits; prev: the qubits the previous
     // pass held (nullptr: no limit), at most kmax of the result may lie outside it
-    auto plan_tile = [&](const std::vector<char>* prev) {
+    // greedy tile growth from the qubits already in in_t (the seed), limited by prev (see above)
+    auto grow_tile = [&](const std::vector<char>* prev) {
       const int WL = wl();
       std::vector<int> next_node(64, -1);  // first not-done 2x2 node per virtual slot
       for (int i = 0; i < (int)nodes.size(); ++i)
@@ -1023,6 +1024,94 @@ struct Packer {
         ++n_in;
         if (prev && !(*prev)[best]) ++n_out;
       }
+      return next_node;
+    };
+    // run the pass of tile in_t for real on the node state (npred / done / ready), with an undo log
+    struct Undo {
+      std::vector<int> dec, done, ready;
+    };
+    auto commit_run = [&](Undo& u) {
+      std::vector<int> rdy = ready;
+      int n_ops = 0, n_bfly = 0;
+      const int WL = wl();
+      while (2 * n_ops + 2 <= MAX_OPS) {
+        int best = -1;
+        for (int k = 0; k < (int)rdy.size(); ++k) {
+          const LOp& l = ops[nodes[rdy[k]].op];
+          if (l.type == 4 && n_bfly >= max_bfly) continue;
+          const bool diag = l.type == 1 || l.type == 2;
+          if (!diag && (pos[l.a] >= WL || !in_t[l.a])) continue;
+          if (best < 0 || before(rdy[k], rdy[best])) best = k;
+        }
+        if (best < 0) break;
+        const int id = rdy[best];
+        rdy[best] = rdy.back();
+        rdy.pop_back();
+        ++n_ops;
+        if (ops[nodes[id].op].type == 4) ++n_bfly;
+        nodes[id].done = true;
+        u.done.push_back(id);
+        for (int s2 : nodes[id].succ) {
+          u.dec.push_back(s2);
+          if (--nodes[s2].npred == 0) rdy.push_back(s2);
+        }
+      }
+      u.ready = ready;
+      ready = rdy;
+      return n_bfly;
+    };
+    auto undo_run = [&](Undo& u) {
+      for (int s2 : u.dec) ++nodes[s2].npred;
+      for (int id : u.done) nodes[id].done = false;
+      ready = u.ready;
+    };
+    // Two-pass look-ahead (OWQS_ENDGAME=B: only once at most B butterflies are left; 0: off): the
+    // greedy tile maximises its own pass and can leave the remaining work spread over more qubits
+    // than later tiles hold (C3's last 26 butterflies took passes of 16, 8 and 2). Every qubit with
+    // work seeds its own greedy tile, and the tile maximising this pass plus the greedy next pass
+    // wins. C3 30 -> 28 passes, C3W 31 -> 30, C4 21; about 1 s of host time per program.
+    static const int endgame_bfly = getenv("OWQS_ENDGAME") ? atoi(getenv("OWQS_ENDGAME")) : (1 << 30);
+    auto plan_tile = [&](const std::vector<char>* prev) {
+      const std::vector<char> seed = in_t;
+      int left = 0;
+      for (int i = 0; i < (int)nodes.size(); ++i)
+        if (!nodes[i].done && ops[nodes[i].op].type == 4) ++left;
+      if (left > endgame_bfly) {
+        grow_tile(prev);
+        return;
+      }
+      const int WL = wl();
+      std::vector<char> best_t;
+      int best_sum = -1, best_b1 = -1;
+      std::vector<int> seeds = {-1};
+      {
+        in_t = seed;
+        const std::vector<int> nn = grow_tile(nullptr);  // only for next_node
+        for (int p = 0; p < WL; ++p)
+          if (nn[at[p]] >= 0 && !seed[at[p]]) seeds.push_back(at[p]);
+      }
+      for (int sv : seeds) {
+        in_t = seed;
+        if (sv >= 0) {
+          if (prev && !(*prev)[sv] && kmax < 1) continue;
+          in_t[sv] = 1;
+        }
+        grow_tile(prev);
+        const std::vector<char> t1 = in_t;
+        Undo u;
+        const int b1 = commit_run(u);
+        in_t.assign(64, 0);
+        if (SB == 6) in_t[at[0]] = 1;
+        grow_tile(&t1);
+        const int b2 = dry_run(nullptr);
+        undo_run(u);
+        if (b1 + b2 > best_sum || (b1 + b2 == best_sum && b1 > best_b1)) {
+          best_sum = b1 + b2;
+          best_b1 = b1;
+          best_t = t1;
+        }
+      }
+      in_t = best_t;
     };
     std::vector<int> planned;  // group positions chosen for the next pass (valid when have_plan)
     bool have_plan = false;

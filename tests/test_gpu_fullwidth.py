@@ -171,7 +171,7 @@ def test_config3_measured_structural_prob(require_gpu, prec):
             x.set_input_random(7)
         oa, pa = a.run("sampled", seed=5)
         ob, pb = b.run("sampled", seed=5)
-        assert a.stats()["n_reduce"] >= 30 > b.stats()["n_reduce"]
+        assert a.stats()["n_reduce"] >= a.stats()["n_passes"] - 1 and b.stats()["n_reduce"] <= 2
         tol = 1e-12 if prec == 128 else 2e-6
         assert np.max(np.abs(pa - 0.5)) <= tol, np.max(np.abs(pa - 0.5))
         assert np.all(pb == 0.5)
