@@ -43,6 +43,8 @@ cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
                        cudaStream_t s, const PassCoef* cp_host, cudaGraphDeviceNode_t* dev_node, bool no_pdl);
+cudaError_t launch_decide_ahead(const StepDesc* d_steps, int n_steps, int n_mst, const DevPtrs& p, PassCoef* pc,
+                                cudaStream_t s);
 cudaError_t launch_decide(const StepDesc& d, const DevPtrs& p, PassCoef* pc, cudaStream_t s,
                           const cudaGraphDeviceNode_t* nodes, int n_nodes, size_t off);
 cudaError_t launch_grid_finish(const DevPtrs& p, unsigned nblk, int nred, cudaStream_t s);
@@ -144,6 +146,11 @@ struct owqs_ctx {
   std::vector<uint64_t> sub_mask;
   int pending_mode = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // decide-ahead graph capture: the copies of the decisions into the pass kernels' __constant__ fork
+  // over kAux side streams (parallel graph branches) and join before the first pass
+  static constexpr int kAux = 4;
+  cudaStream_t aux[kAux] = {};
+  cudaEvent_t fork_ev = nullptr, join_ev[kAux] = {};
   owqs_stats_t stats{};
   int last_cm = 0;
   std::vector<cudaEvent_t> prof_ev;  // OWQS_FLAG_PROFILE: event after every launch (+1 start)
@@ -538,6 +545,23 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
   const bool eowqs_static = mode == OWQS_EOWQS && m.coefp;
   const bool static_pc = eowqs_static || (mode == OWQS_EOWQS && m.pc_static_ready && !getenv("OWQS_EOWQS_DECIDE"));
   const bool use_graph = !(ctx->cfg.flags & OWQS_FLAG_NO_GRAPH) && (mode != OWQS_EOWQS || static_pc);
+  // decide ahead (sampled / forced, constant-bank coefficients): every step a tile pass whose
+  // decisions are structural (no reduction feeds them, no SHRINK) -> one decide_ahead_kernel for
+  // the whole run, the copies into the kernels' __constant__ up front, the pass kernels back to back
+  // (OWQS_DECIDE_AHEAD=0: per-pass decide kernels)
+  bool ahead = mode != OWQS_EOWQS && m.coef_src == COEF_CONST && !m.jit_fn.empty() && !m.cp_sym.empty() &&
+               ctx->shards.size() == 1 && !(getenv("OWQS_DECIDE_AHEAD") && atoi(getenv("OWQS_DECIDE_AHEAD")) == 0);
+  for (size_t i = 0; ahead && i < m.prog.steps.size(); ++i) {
+    const StepDesc& s = m.prog.steps[i];
+    if (s.kind != ST_PASS) ahead = false;
+    else if (s.n_ops > 0 && (!m.jit_fn[i] || jit_engine(s, ctx->prec) != 2 || jit_tile_small(s, ctx->prec) ||
+                             s.first_uses_red || !m.cp_sym[i]))
+      ahead = false;
+  }
+  if (ahead && !m.d_steps) {
+    CU(cudaMalloc(&m.d_steps, std::max<size_t>(1, m.prog.steps.size()) * sizeof(StepDesc)));
+    CU(cudaMemcpy(m.d_steps, m.prog.steps.data(), m.prog.steps.size() * sizeof(StepDesc), cudaMemcpyHostToDevice));
+  }
   const bool dev_update = m.coef_src == COEF_PARAM && !eowqs_static;  // sampled / forced: device node updates
   const size_t NS = ctx->shards.size();
   std::vector<cudaGraphDeviceNode_t> hnodes(dev_update ? m.prog.steps.size() * NS : 0, nullptr);
@@ -559,8 +583,44 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
     return capturing ? cudaEventRecordWithFlags(ctx->prof_ev[i], ctx->stream, cudaEventRecordExternal)
                      : cudaEventRecord(ctx->prof_ev[i], ctx->stream);
   };
+  // a kernel shared by several steps gets its constants copied right before each use
+  auto shared_sym = [&](size_t i) {
+    for (size_t j = 0; j < m.cp_sym.size(); ++j)
+      if (j != i && m.cp_sym[j] == m.cp_sym[i]) return true;
+    return false;
+  };
   auto launch_all = [&](bool capturing) -> owqs_status {
     if (prof) CU(record(0, capturing));
+    if (ahead) {
+      CU(launch_decide_ahead(m.d_steps, (int)m.prog.steps.size(), (int)m.prog.mst.size(), dev_ptrs(ctx, m, 0), m.d_pc,
+                             ctx->stream));
+      std::vector<size_t> cp;
+      for (size_t i = 0; i < m.prog.steps.size(); ++i)
+        if (m.prog.steps[i].n_ops > 0 && !shared_sym(i)) cp.push_back(i);
+      const int K = owqs_ctx::kAux;
+      if (capturing && cp.size() > (size_t)K) {
+        if (!ctx->fork_ev) {
+          CU(cudaEventCreateWithFlags(&ctx->fork_ev, cudaEventDisableTiming));
+          for (int a = 0; a < K; ++a) {
+            CU(cudaStreamCreateWithFlags(&ctx->aux[a], cudaStreamNonBlocking));
+            CU(cudaEventCreateWithFlags(&ctx->join_ev[a], cudaEventDisableTiming));
+          }
+        }
+        CU(cudaEventRecord(ctx->fork_ev, ctx->stream));
+        for (int a = 0; a < K; ++a) CU(cudaStreamWaitEvent(ctx->aux[a], ctx->fork_ev, 0));
+        for (size_t k = 0; k < cp.size(); ++k)
+          CU(cudaMemcpyAsync(m.cp_sym[cp[k]], m.d_pc + cp[k], sizeof(PassCoef), cudaMemcpyDeviceToDevice,
+                             ctx->aux[k % K]));
+        for (int a = 0; a < K; ++a) {
+          CU(cudaEventRecord(ctx->join_ev[a], ctx->aux[a]));
+          CU(cudaStreamWaitEvent(ctx->stream, ctx->join_ev[a], 0));
+        }
+      } else {
+        for (size_t i : cp)
+          CU(cudaMemcpyAsync(m.cp_sym[i], m.d_pc + i, sizeof(PassCoef), cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    }
+    bool first_tile = true;  // decide ahead: the first pass kernel follows the copies (no PDL edge)
     for (size_t i = 0; i < m.prog.steps.size(); ++i) {
       const StepDesc& s = m.prog.steps[i];
       if (s.kind == ST_SWAP) {
@@ -571,13 +631,14 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
         const int eng = jit ? jit_engine(s, ctx->prec) : 0;
         const bool small = eng == 2 && jit_tile_small(s, ctx->prec);
         const bool upd = dev_update && eng == 2 && !small;
-        if (eng == 2 && !small && !static_pc)
+        if (eng == 2 && !small && !static_pc && !ahead)
           CU(launch_decide(s, dev_ptrs(ctx, m, 0), m.d_pc + i, ctx->stream, upd ? m.d_devnodes + i * NS : nullptr,
                            upd ? (int)NS : 0, upd ? m.coef_off[i] : 0));
         // COEF_CONST: the pass's decisions into its kernel's __constant__ (graph memcpy node)
         bool after_copy = false;
         if (m.coef_src == COEF_CONST && eng == 2 && !small && !m.cp_sym.empty() && m.cp_sym[i]) {
-          const PassCoef* src = eowqs_static ? (m.cp_once.empty() || m.cp_once[i] ? nullptr : m.d_static_cp + i) : m.d_pc + i;
+          const PassCoef* src = eowqs_static ? (m.cp_once.empty() || m.cp_once[i] ? nullptr : m.d_static_cp + i)
+                                : (ahead && !shared_sym(i)) ? nullptr : m.d_pc + i;
           if (src) {
             CU(cudaMemcpyAsync(m.cp_sym[i], src, sizeof(PassCoef), cudaMemcpyDeviceToDevice, ctx->stream));
             after_copy = true;
@@ -587,10 +648,12 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
           if (jit)
             CU(jit_launch(m.jit_fn[i], m.jit_blocks[i], s, dev_ptrs(ctx, m, (int)r), m.d_pc + i, ctx->prec, ctx->stream,
                           (eowqs_static && eng == 2 && !small) ? &m.static_cp[i] : nullptr,
-                          (upd && capturing) ? &hnodes[i * NS + r] : nullptr, after_copy && r == 0));
+                          (upd && capturing) ? &hnodes[i * NS + r] : nullptr,
+                          (after_copy || (ahead && first_tile)) && r == 0));
           else
             CU(launch_step(s, dev_ptrs(ctx, m, (int)r), ctx->prec, ctx->stream));
         }
+        if (jit) first_tile = false;
         if (eng == 2 && !small && s.red_kind != RED_NONE)  // tile passes leave block partials
           for (size_t r = 0; r < ctx->shards.size(); ++r)
             CU(launch_grid_finish(dev_ptrs(ctx, m, (int)r), jit_tile_blocks(s, ctx->prec),
@@ -1019,6 +1082,11 @@ void owqs_destroy(owqs_ctx* ctx) {
   if (ctx->h_err) cudaFreeHost(ctx->h_err);
   if (ctx->h_innorm) cudaFreeHost(ctx->h_innorm);
   for (cudaEvent_t e : ctx->prof_ev) cudaEventDestroy(e);
+  for (int a = 0; a < owqs_ctx::kAux; ++a) {
+    if (ctx->aux[a]) cudaStreamDestroy(ctx->aux[a]);
+    if (ctx->join_ev[a]) cudaEventDestroy(ctx->join_ev[a]);
+  }
+  if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->comm) ncclCommDestroy(ctx->comm);

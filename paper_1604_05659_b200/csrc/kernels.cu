@@ -1582,6 +1582,50 @@ __global__ void __launch_bounds__(32) decide_kernel(const StepDesc d, const DevP
   }
 }
 
+// All of a run's tile-pass decisions up front. Valid when every decision is structural (R-13: no
+// pass decides from a reduction, no SHRINK) and every measurement is decided by a tile pass: an
+// outcome then depends only on its keyed draw against prob0 = 1/2 (or on the forced string), never
+// on the state or on other outcomes, so (1) one thread per measurement writes every outcome, then
+// (2) one warp per pass evaluates its signals (Eq. 2 angles, folded X, conditional ops) from those
+// outcomes and writes its PassCoef -- exactly what the per-pass decide kernels compute. The pass
+// kernels then run back to back (programmatic serialisation, no decide kernel or copy node between
+// them): config 2, whose 8 MiB state makes every pass launch-latency-bound, 0.568 -> 0.50 ms with a
+// sequential single-warp version of (2).
+__global__ void __launch_bounds__(256) decide_ahead_outcomes_kernel(const DevPtrs p, int n_mst) {
+  const int mode = p.run->mode;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_mst; i += gridDim.x * blockDim.x) {
+    const MStatic ms = p.mst[i];
+    const int outc = mode == 0 ? (draw_uniform(p.run->seed, ms.key) <= 0.5 ? 0 : 1) : (p.forced[ms.ord] & 1);
+    p.outcome[ms.ord] = (uint8_t)outc;
+  }
+}
+
+__global__ void __launch_bounds__(32) decide_ahead_kernel(const StepDesc* steps, const DevPtrs p, PassCoef* pc) {
+  __shared__ PassShared sh;
+  const int t = threadIdx.x, k = blockIdx.x;
+  const StepDesc& d = steps[k];
+  if (d.kind != ST_PASS || d.n_ops == 0) return;  // a pass without butterflies may still hold conditional ops
+  pass_prologue(d, p, sh, true);
+  PassCoef* c = pc + k;
+  for (int b = t; b < d.n_bfly; b += 32) {
+    const double ar = sh.ka[b][0], ai = sh.ka[b][1];
+    c->ard[b] = ar;
+    c->aid[b] = ai;
+    c->ar[b] = (float)ar;
+    const float fai = (float)ai;
+    c->B[b] = ((uint64_t)__float_as_uint(fai) << 32) | (uint64_t)__float_as_uint(-fai);
+  }
+  for (int i = t; i < d.n_ops; i += 32) c->cond[i] = sh.cond[i];
+  if (t == 0) c->scale = sh.scale;
+}
+
+cudaError_t launch_decide_ahead(const StepDesc* d_steps, int n_steps, int n_mst, const DevPtrs& p, PassCoef* pc,
+                                cudaStream_t s) {
+  if (n_mst > 0) decide_ahead_outcomes_kernel<<<(unsigned)std::min(1184, (n_mst + 255) / 256), 256, 0, s>>>(p, n_mst);
+  if (n_steps > 0) decide_ahead_kernel<<<(unsigned)n_steps, 32, 0, s>>>(d_steps, p, pc);
+  return cudaGetLastError();
+}
+
 // Sum of the block partials of a tile pass (fixed order: deterministic) into red_result.
 // Sum of the tile kernels' block partials into red_result, deterministic: CTA g sums the contiguous
 // range of partials [g * per, (g + 1) * per) in a fixed order into gpart[g]; the last CTA to arrive
