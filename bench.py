@@ -575,7 +575,8 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(round(st.get("n_kernels") or st["n_launches"])) * args.steps * n_shards // (n_shards if shard else 1),
         "clocks": clocks,
     }
-    sim.close()
+    if sim is not None:
+        sim.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     return 0
