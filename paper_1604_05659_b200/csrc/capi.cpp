@@ -37,8 +37,8 @@ cudaError_t launch_sample_out(const void* shard, int prec, const int64_t* idx, u
 cudaError_t launch_copy_norm(const DevPtrs& p, int prec, const void* src, uint64_t n, cudaStream_t s);
 cudaError_t launch_dot(const DevPtrs& p, const void* a, const void* b, uint64_t n, cudaStream_t s);
 cudaError_t launch_dot_t(const DevPtrs& p, int prec, const void* a, const void* b, uint64_t n, cudaStream_t s);
-cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_width, int pl, int bit, bool unpack,
-                             cudaStream_t s);
+cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int pl, int bit, bool unpack, uint64_t j0,
+                             uint64_t n, cudaStream_t s);
 cudaError_t launch_loopback_allreduce(double* red, int n_ranks, cudaStream_t s);
 int step_kclass(const StepDesc& d, int prec);
 cudaError_t jit_launch(cudaKernel_t k, int max_blocks, const StepDesc& d, const DevPtrs& p, const PassCoef* pc, int prec,
@@ -122,7 +122,10 @@ struct owqs_ctx {
   std::vector<Shard> shards;  // 1, or n_ranks in loopback mode
   double* d_red_all = nullptr;
   size_t shard_bytes = 0;
-  void* d_swap = nullptr;  // two half-shard buffers (send, receive)
+  void* d_swap = nullptr;  // one shard: the swap's chunk slots (2 send + 2 receive), or the gather buffer
+  // NCCL swaps: the transfers run on comm_stream, pack / unpack on stream, chunk by chunk (events)
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t sw_packed[2] = {}, sw_sent[2] = {}, sw_unpacked[2] = {};
   void* d_jscratch = nullptr;  // ST_SHRINKK output (joint k-outcome measurement), jscratch_bytes
   size_t jscratch_bytes = 0;
   // run state
@@ -480,29 +483,61 @@ owqs_status allreduce_red(owqs_ctx* ctx) {
 }
 
 // ST_SWAP: every rank trades the half of its shard whose bit `pl` = 1 - (its rank bit) with rank ^ m
+// swap chunk: a power of two of elements, ~256 MiB, at most 16 chunks per half-shard (OWQS_SWAP_CHUNK_MB)
+uint64_t swap_chunk_elems(const owqs_ctx* ctx, uint64_t half_elems) {
+  static const uint64_t mb = getenv("OWQS_SWAP_CHUNK_MB") ? (uint64_t)std::max(1, atoi(getenv("OWQS_SWAP_CHUNK_MB"))) : 256;
+  uint64_t c = 1;
+  while (c < half_elems && c * ctx->elem < (mb << 20)) c <<= 1;
+  while (half_elems / c > 16) c <<= 1;
+  return std::min(c, std::max<uint64_t>(1, half_elems / 2));  // >= 2 chunks: 4 slots fit in one shard
+}
+
+// ST_SWAP: every rank trades the half of its shard whose bit `pl` = 1 - (its rank bit) with
+// rank ^ 2^g, in chunks of swap_chunk_elems: pack chunk c into send slot c % 2 (stream), transfer it
+// (comm_stream: ncclSend of the slot, ncclRecv into receive slot c % 2), unpack it (stream) -- the
+// transfer of chunk c overlaps the pack of chunk c + 1 and the unpack of chunk c - 1, and a slot is
+// reused only after its transfer (send) or its unpack (receive) is done. The loopback backend runs
+// the same chunk loop with device copies on one stream.
 owqs_status do_swap(owqs_ctx* ctx, const StepDesc& d) {
   const int wl = d.width, pl = d.swap_local, gbit = d.swap_global - wl;
-  const size_t half = ((size_t)ctx->elem << wl) / 2;
-  char* sendb = (char*)ctx->d_swap;
-  char* recvb = sendb + half;
+  const uint64_t half_elems = 1ull << (wl - 1);
+  const uint64_t ce = swap_chunk_elems(ctx, half_elems), nch = half_elems / ce;
+  const size_t cb = (size_t)ce * ctx->elem;
+  char* base = (char*)ctx->d_swap;  // 4 slots of cb bytes: send 0, send 1, receive 0, receive 1 (4 cb <= one shard)
+  char* send[2] = {base, base + cb};
+  char* recv[2] = {base + 2 * cb, base + 3 * cb};
   if (ctx->loopback) {
     for (int r = 0; r < ctx->n_ranks; ++r) {
       const int p = r ^ (1 << gbit);
       if (p < r) continue;  // r has rank bit 0 (trades its bit-pl = 1 half), p has 1 (bit-pl = 0 half)
-      CU(launch_swap_pack(ctx->shards[r].d_state, sendb, ctx->prec, wl, pl, 1, false, ctx->stream));
-      CU(launch_swap_pack(ctx->shards[p].d_state, recvb, ctx->prec, wl, pl, 0, false, ctx->stream));
-      CU(launch_swap_pack(ctx->shards[r].d_state, recvb, ctx->prec, wl, pl, 1, true, ctx->stream));
-      CU(launch_swap_pack(ctx->shards[p].d_state, sendb, ctx->prec, wl, pl, 0, true, ctx->stream));
+      for (uint64_t c = 0; c < nch; ++c) {
+        const uint64_t j0 = c * ce;
+        CU(launch_swap_pack(ctx->shards[r].d_state, send[c & 1], ctx->prec, pl, 1, false, j0, ce, ctx->stream));
+        CU(launch_swap_pack(ctx->shards[p].d_state, recv[c & 1], ctx->prec, pl, 0, false, j0, ce, ctx->stream));
+        CU(launch_swap_pack(ctx->shards[r].d_state, recv[c & 1], ctx->prec, pl, 1, true, j0, ce, ctx->stream));
+        CU(launch_swap_pack(ctx->shards[p].d_state, send[c & 1], ctx->prec, pl, 0, true, j0, ce, ctx->stream));
+      }
     }
     return OWQS_OK;
   }
   const int b = (ctx->rank >> gbit) & 1, partner = ctx->rank ^ (1 << gbit);
-  CU(launch_swap_pack(ctx->shards[0].d_state, sendb, ctx->prec, wl, pl, 1 - b, false, ctx->stream));
-  NC(ncclGroupStart());
-  NC(ncclSend(sendb, half, ncclChar, partner, ctx->comm, ctx->stream));
-  NC(ncclRecv(recvb, half, ncclChar, partner, ctx->comm, ctx->stream));
-  NC(ncclGroupEnd());
-  CU(launch_swap_pack(ctx->shards[0].d_state, recvb, ctx->prec, wl, pl, 1 - b, true, ctx->stream));
+  for (uint64_t c = 0; c < nch; ++c) {
+    const int k = (int)(c & 1);
+    const uint64_t j0 = c * ce;
+    if (c >= 2) CU(cudaStreamWaitEvent(ctx->stream, ctx->sw_sent[k], 0));  // send slot k free again
+    CU(launch_swap_pack(ctx->shards[0].d_state, send[k], ctx->prec, pl, 1 - b, false, j0, ce, ctx->stream));
+    CU(cudaEventRecord(ctx->sw_packed[k], ctx->stream));
+    CU(cudaStreamWaitEvent(ctx->comm_stream, ctx->sw_packed[k], 0));
+    if (c >= 2) CU(cudaStreamWaitEvent(ctx->comm_stream, ctx->sw_unpacked[k], 0));  // receive slot k free
+    NC(ncclGroupStart());
+    NC(ncclSend(send[k], cb, ncclChar, partner, ctx->comm, ctx->comm_stream));
+    NC(ncclRecv(recv[k], cb, ncclChar, partner, ctx->comm, ctx->comm_stream));
+    NC(ncclGroupEnd());
+    CU(cudaEventRecord(ctx->sw_sent[k], ctx->comm_stream));
+    CU(cudaStreamWaitEvent(ctx->stream, ctx->sw_sent[k], 0));
+    CU(launch_swap_pack(ctx->shards[0].d_state, recv[k], ctx->prec, pl, 1 - b, true, j0, ce, ctx->stream));
+    CU(cudaEventRecord(ctx->sw_unpacked[k], ctx->stream));
+  }
   return OWQS_OK;
 }
 
@@ -1048,6 +1083,13 @@ owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out) {
   if (cudaMallocHost(&ctx->h_err, std::max<size_t>(1, ctx->shards.size()) * sizeof(int32_t)) != cudaSuccess)
     return bail(OWQS_E_NOMEM, "allocation/stream/event setup");
   if (nr > 1 && !loopback) {
+    if (cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking) != cudaSuccess)
+      return bail(OWQS_E_CUDA, "allocation/stream/event setup");
+    for (int k = 0; k < 2; ++k)
+      if (cudaEventCreateWithFlags(&ctx->sw_packed[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->sw_sent[k], cudaEventDisableTiming) != cudaSuccess ||
+          cudaEventCreateWithFlags(&ctx->sw_unpacked[k], cudaEventDisableTiming) != cudaSuccess)
+        return bail(OWQS_E_CUDA, "allocation/stream/event setup");
     ncclUniqueId id;
     memcpy(&id, cfg->nccl_id, sizeof(id));
     if (ncclCommInitRank(&ctx->comm, nr, id, cfg->rank) != ncclSuccess) return bail(OWQS_E_NCCL, "allocation/stream/event setup");
@@ -1087,6 +1129,12 @@ void owqs_destroy(owqs_ctx* ctx) {
     if (ctx->join_ev[a]) cudaEventDestroy(ctx->join_ev[a]);
   }
   if (ctx->fork_ev) cudaEventDestroy(ctx->fork_ev);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->sw_packed[k]) cudaEventDestroy(ctx->sw_packed[k]);
+    if (ctx->sw_sent[k]) cudaEventDestroy(ctx->sw_sent[k]);
+    if (ctx->sw_unpacked[k]) cudaEventDestroy(ctx->sw_unpacked[k]);
+  }
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   if (ctx->comm) ncclCommDestroy(ctx->comm);

@@ -1713,16 +1713,17 @@ static inline int log2i(int x) { int r = 0; while ((1 << r) < x) ++r; return r; 
 // ---- multi-rank: SWAP halves and reduction all-reduce ------------------------------------------
 // half of a shard whose bit `pl` equals `bit`, packed in index order (runs of 2^pl contiguous)
 template <typename T>
-__global__ void swap_pack_kernel(const void* state, void* buf, int local_width, int pl, int bit, int unpack) {
+__global__ void swap_pack_kernel(const void* state, void* buf, int pl, int bit, int unpack, uint64_t j0, uint64_t n) {
   typedef typename VT<T>::C C;
   const C* st = reinterpret_cast<const C*>(state);
   C* sm = reinterpret_cast<C*>(const_cast<void*>(state));
   C* b = reinterpret_cast<C*>(buf);
-  const uint64_t n = 1ull << (local_width - 1);
-  for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (uint64_t)gridDim.x * blockDim.x) {
+  // elements [j0, j0 + n) of the half with local bit pl = bit; buf holds them from index 0
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t j = j0 + i;
     const uint64_t L = ((j >> pl) << (pl + 1)) | ((uint64_t)bit << pl) | (j & ((1ull << pl) - 1));
-    if (unpack) sm[L] = b[j];
-    else b[j] = st[L];
+    if (unpack) sm[L] = b[i];
+    else b[i] = st[L];
   }
 }
 
@@ -1735,12 +1736,11 @@ __global__ void loopback_allreduce_kernel(double* red, int n_ranks) {
   }
 }
 
-cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int local_width, int pl, int bit, bool unpack,
-                             cudaStream_t s) {
-  const uint64_t n = 1ull << (local_width - 1);
+cudaError_t launch_swap_pack(const void* state, void* buf, int prec, int pl, int bit, bool unpack, uint64_t j0,
+                             uint64_t n, cudaStream_t s) {
   unsigned b = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, (uint64_t)(g_lim_ready ? g_lim.max_blocks_elem : 1184)));
-  if (prec == 0) swap_pack_kernel<float><<<b, 256, 0, s>>>(state, buf, local_width, pl, bit, unpack ? 1 : 0);
-  else swap_pack_kernel<double><<<b, 256, 0, s>>>(state, buf, local_width, pl, bit, unpack ? 1 : 0);
+  if (prec == 0) swap_pack_kernel<float><<<b, 256, 0, s>>>(state, buf, pl, bit, unpack ? 1 : 0, j0, n);
+  else swap_pack_kernel<double><<<b, 256, 0, s>>>(state, buf, pl, bit, unpack ? 1 : 0, j0, n);
   return cudaGetLastError();
 }
 
