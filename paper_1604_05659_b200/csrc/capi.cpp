@@ -167,8 +167,29 @@ struct owqs_ctx {
 
 namespace {
 
+// decisions ahead for a sampled / forced run of m: constant-bank coefficients, one
+// shard, every step a tile pass whose decisions are structural (no reduction feeds them, no SHRINK)
+bool decide_ahead_ok(const owqs_ctx* ctx, const CompiledMode& m) {
+  if (m.coef_src != COEF_CONST || m.jit_fn.empty() || m.cp_sym.empty() || ctx->shards.size() != 1) return false;
+  if (getenv("OWQS_DECIDE_AHEAD") && atoi(getenv("OWQS_DECIDE_AHEAD")) == 0) return false;
+  for (size_t i = 0; i < m.prog.steps.size(); ++i) {
+    const StepDesc& s = m.prog.steps[i];
+    if (s.kind != ST_PASS) return false;
+    if (s.n_ops > 0 && (!m.jit_fn[i] || jit_engine(s, ctx->prec) != 2 || jit_tile_small(s, ctx->prec) ||
+                        s.first_uses_red || !m.cp_sym[i]))
+      return false;
+  }
+  return true;
+}
+
 // kernel launches of one run (per shard): every step, plus the decide kernel of each tile pass
+// (or, with decisions ahead, the two decide-ahead kernels per run)
 double kernels_per_run(const owqs_ctx* ctx, const CompiledMode& m) {
+  if (&m == &ctx->cm[0] && !m.jit_fn.empty() && decide_ahead_ok(ctx, m)) {
+    double n = 2;
+    for (const StepDesc& s : m.prog.steps) n += 1 + (s.red_kind != RED_NONE ? 1 : 0);
+    return n + 1.0 + ((ctx->hp.n_measure > 0 ? 2.0 : 0.0) + 1.0);
+  }
   double n = 0;
   for (size_t i = 0; i < m.prog.steps.size(); ++i) {
     const StepDesc& s = m.prog.steps[i];
@@ -584,15 +605,7 @@ owqs_status run_enqueue(owqs_ctx* ctx, int cmi, int mode, uint64_t seed, const u
   // decisions are structural (no reduction feeds them, no SHRINK) -> one decide_ahead_kernel for
   // the whole run, the copies into the kernels' __constant__ up front, the pass kernels back to back
   // (OWQS_DECIDE_AHEAD=0: per-pass decide kernels)
-  bool ahead = mode != OWQS_EOWQS && m.coef_src == COEF_CONST && !m.jit_fn.empty() && !m.cp_sym.empty() &&
-               ctx->shards.size() == 1 && !(getenv("OWQS_DECIDE_AHEAD") && atoi(getenv("OWQS_DECIDE_AHEAD")) == 0);
-  for (size_t i = 0; ahead && i < m.prog.steps.size(); ++i) {
-    const StepDesc& s = m.prog.steps[i];
-    if (s.kind != ST_PASS) ahead = false;
-    else if (s.n_ops > 0 && (!m.jit_fn[i] || jit_engine(s, ctx->prec) != 2 || jit_tile_small(s, ctx->prec) ||
-                             s.first_uses_red || !m.cp_sym[i]))
-      ahead = false;
-  }
+  const bool ahead = mode != OWQS_EOWQS && decide_ahead_ok(ctx, m);
   if (ahead && !m.d_steps) {
     CU(cudaMalloc(&m.d_steps, std::max<size_t>(1, m.prog.steps.size()) * sizeof(StepDesc)));
     CU(cudaMemcpy(m.d_steps, m.prog.steps.data(), m.prog.steps.size() * sizeof(StepDesc), cudaMemcpyHostToDevice));

@@ -311,3 +311,34 @@ def test_joint_measurement_matches_sequential(require_gpu, monkeypatch, shape):
         assert np.max(np.abs(a[2] - b[2])) <= TOL[prec]["prob"]
         assert np.max(np.abs(a[0] - b[0])) <= TOL[prec]["amp"]
         assert a[3] < b[3]  # fewer launches
+
+
+@pytest.mark.parametrize("shape", ["BW:16x12", "CL:14x4"])
+def test_decide_ahead_vs_oracle_and_per_pass(require_gpu, monkeypatch, shape):
+    """Decisions ahead (one decide launch per run, pass kernels back to back) on
+    tile-engine programs at widths 14-16: sampled and forced runs equal the oracle, and equal the
+    same program with per-pass decide kernels (OWQS_DECIDE_AHEAD=0) bit for bit -- outcomes, prob0
+    and amplitudes -- in both precisions."""
+    p = W.config_pattern(shape, seed=3)
+    psi = haar_state(len(p.inputs), 5)
+    forced = np.random.default_rng(6).integers(0, 2, p.n_measure)
+    res, kern = {}, {}
+    for ahead in ("1", "0"):
+        monkeypatch.setenv("OWQS_DECIDE_AHEAD", ahead)
+        for prec in (128, 64):
+            s = Simulator(precision=prec)
+            try:
+                out_s, ref_s = check(s, p, psi, "sampled", seed=9)
+                out_f, ref_f = check(s, p, psi, "forced", forced=forced)
+                s.load(p)
+                s.set_input(psi)
+                oc, p0 = s.run("sampled", seed=9)
+                res[(ahead, prec)] = (out_s, out_f, np.array(oc), np.array(p0))
+                kern[(ahead, prec)] = s.stats()["n_kernels"]
+            finally:
+                s.close()
+    for prec in (128, 64):
+        assert kern[("1", prec)] < kern[("0", prec)], kern  # the ahead path ran (fewer launches)
+        a, b = res[("1", prec)], res[("0", prec)]
+        for x, y in zip(a, b):
+            assert np.array_equal(x, y)
