@@ -310,24 +310,34 @@ def run_ours(args, rank, world, local_rank):
     big = state_bytes > (32 << 30)  # > 32 GiB: no host buffers (e2e / cpu_baseline skipped)
     # resident input copy whenever a second full-size buffer fits (config 4: 2 x 64 GiB of 180 GB);
     # otherwise the device counter-Haar generator runs inside every step
-    resident = not shard and (not big or 2 * state_bytes <= 0.8 * torch.cuda.get_device_properties(dev).total_memory)
+    total_mem = torch.cuda.get_device_properties(dev).total_memory
+    if shard:
+        # this rank's shard (+ its swap buffer) + a resident input shard + the generator's transient state
+        resident = 4 * (state_bytes // world) <= 0.8 * total_mem
+    else:
+        resident = not big or 2 * state_bytes <= 0.8 * total_mem
     x = None
     if resident:
-        # resident input: device Haar generator of the library, copied into a torch-owned buffer
-        x = torch.empty(N, dtype=cdt, device=dev)
+        # resident input: device Haar generator of the library, copied into a torch-owned buffer.
+        # Sharded: every rank draws its own normalised shard and scales it by 1/sqrt(world), so the
+        # ranks' shards together are one normalised state (owqs_set_input_device takes the shard).
+        n_loc = n_in - (world.bit_length() - 1 if shard else 0)
+        x = torch.empty(2 ** n_loc, dtype=cdt, device=dev)
         gen = Simulator(precision=prec, device=local_rank, stream=stream.cuda_stream)
-        gen.load(Pattern(list(range(n_in)), list(range(n_in)), []))
+        gen.load(Pattern(list(range(n_loc)), list(range(n_loc)), []))
         gen.set_input_random(1 + rank)
         gen.run("eowqs", want=False)
-        gen.get_output_device(x.data_ptr(), prec, N)
+        gen.get_output_device(x.data_ptr(), prec, 2 ** n_loc)
         gen.close()
+        if shard:
+            x.mul_(world ** -0.5)
         torch.cuda.synchronize()
 
     def set_input(s, i):
         if x is None:  # device counter-Haar input (a second full-size state does not fit)
             s.set_input_random(1 + i)
         else:
-            s.set_input_device(x.data_ptr(), prec, N)
+            s.set_input_device(x.data_ptr(), prec, x.numel())
 
     def step(i):
         set_input(sim, i)
@@ -387,7 +397,8 @@ def run_ours(args, rank, world, local_rank):
     if big:  # make room for the profiling context's state
         sim.close()
         sim = None
-        x = None
+        if not shard:
+            x = None
         torch.cuda.empty_cache()
     peak, peak_src = peaks()
     # FP32 (complex64) / FP64 (complex128) lanes x SMs x max SM clock (B200: 128 FP32, 64 FP64 lanes/SM)
