@@ -430,12 +430,6 @@ struct Gen {
     static const bool v = getenv("OWQS_PDL_PREFETCH") && atoi(getenv("OWQS_PDL_PREFETCH")) != 0;
     return v;
   }
-  // first-wave stagger (experiment, off): CTA b < 148 * CTAs/SM sleeps (b / 148) * OWQS_STAGGER ns after
-  // the PDL wait, so the CTAs sharing an SM start their load phases apart
-  static int stagger_ns() {
-    static const int v = getenv("OWQS_STAGGER") ? atoi(getenv("OWQS_STAGGER")) : 0;
-    return v;
-  }
   static int prefetch_distance() {
     // 13-bit tiles (2 CTAs per SM): one wave ahead, 148 x 2, measured C3 49.8 -> 49.3 ms, C3W 219 ->
     // 213 ms. 12-bit tiles (4 CTAs per SM, default): off -- the extra resident CTAs already hide the
@@ -1488,9 +1482,6 @@ struct Gen {
         o << ";\n      asm volatile(\"cp.async.bulk.prefetch.L2.global [%0], 512;\" :: \"l\"(st + ((gb0 | wsl | ap) << 5)) : \"memory\");\n    }\n";
       }
       o << "    asm volatile(\"griddepcontrol.wait;\" ::: \"memory\");\n";
-      if (stagger_ns() > 0 && iters == 1)
-        o << "    if (blockIdx.x >= 148u && blockIdx.x < " << 148 * tile_minb() << "u) __nanosleep((blockIdx.x / 148u) * "
-          << stagger_ns() << "u);\n";
     }
     if (prec == 0)
       for (int q = 0; q < P; q += 2)

@@ -98,7 +98,7 @@ struct PassCoef {
 
 // Grid-reduction scratch sizes (per shard): block partials and group partials (deterministic
 // two-level reduction of the generated pass kernels).
-constexpr int RED_MAX_BLOCKS = 1 << 20;  // one tile per CTA up to width 33 (complex64)
+constexpr int RED_MAX_BLOCKS = 1 << 22;  // one tile per CTA up to width 34 (complex64) / 33 (complex128)
 constexpr int KRON_MAX = 32;  // sub-states merged by one kron_merge launch
 constexpr int RED_GROUP = 256;
 constexpr int RED_MAX_GROUPS = RED_MAX_BLOCKS / RED_GROUP;
