@@ -1,6 +1,7 @@
 // C-ABI implementation (include/owqs.h): context, device memory, CUDA-graph executor, sharding.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <string.h>
 
@@ -55,6 +56,14 @@ cudaError_t launch_batch(const StepDesc* steps, int n_steps, const DevPtrs& base
 using namespace owqs;
 
 namespace {
+// NVTX range over a C-ABI call (SURVEY §5 tracing): host-side, shows load / input / run / output
+// phases in an nsys or ncu --nvtx timeline; a no-op without an attached tool
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 struct CompiledMode {
   bool valid = false;
   Plan plan;
@@ -520,6 +529,7 @@ uint64_t swap_chunk_elems(const owqs_ctx* ctx, uint64_t half_elems) {
 // reused only after its transfer (send) or its unpack (receive) is done. The loopback backend runs
 // the same chunk loop with device copies on one stream.
 owqs_status do_swap(owqs_ctx* ctx, const StepDesc& d) {
+  NvtxRange nvtx_("owqs: global<->local qubit swap");
   const int wl = d.width, pl = d.swap_local, gbit = d.swap_global - wl;
   const uint64_t half_elems = 1ull << (wl - 1);
   const uint64_t ce = swap_chunk_elems(ctx, half_elems), nch = half_elems / ce;
@@ -1204,6 +1214,7 @@ owqs_status load_substates(owqs_ctx* ctx, std::vector<HostPattern>& parts) {
 owqs_status owqs_load_pattern(owqs_ctx* ctx, const int32_t* inputs, int32_t n_in, const int32_t* outputs,
                               int32_t n_out, const owqs_cmd* cmds, int64_t n_cmds, const int32_t* domain_pool,
                               int64_t pool_len) {
+  NvtxRange nvtx_("owqs_load_pattern");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   ctx->loaded = false;
@@ -1284,6 +1295,7 @@ owqs_status owqs_set_input(owqs_ctx* ctx, const double* amps, int64_t n_amps) {
 owqs_status input_from_host_enqueue(owqs_ctx* ctx, const void* amps, int32_t precision);
 
 owqs_status owqs_set_input_host(owqs_ctx* ctx, const void* amps, int32_t precision, int64_t n_amps) {
+  NvtxRange nvtx_("owqs_set_input_host");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->subs.empty()) {  // the caller's input is the inputs' sub-state (PAPER §4.1)
@@ -1335,6 +1347,7 @@ owqs_status input_from_host_enqueue(owqs_ctx* ctx, const void* amps, int32_t pre
 }
 
 owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t precision, int64_t n_amps) {
+  NvtxRange nvtx_("owqs_set_input_device");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->subs.empty()) {  // the caller's input is the inputs' sub-state (PAPER §4.1)
@@ -1373,6 +1386,7 @@ owqs_status owqs_set_input_device(owqs_ctx* ctx, const void* dev_amps, int32_t p
 }
 
 owqs_status owqs_set_input_random(owqs_ctx* ctx, uint64_t seed) {
+  NvtxRange nvtx_("owqs_set_input_random");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->subs.empty()) {  // the caller's input is the inputs' sub-state (PAPER §4.1)
@@ -1405,6 +1419,7 @@ owqs_status run_substates(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const ui
 
 owqs_status owqs_run(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, uint8_t* outcomes_out,
                      double* prob0_out) {
+  NvtxRange nvtx_("owqs_run");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "run before load_pattern");
@@ -1509,6 +1524,7 @@ owqs_status finish_run(owqs_ctx* ctx, int cmi, int mode, owqs_status s, uint8_t*
 owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const uint8_t* forced, const void* in_amps,
                              int32_t in_precision, int64_t n_in, void* out_amps, int32_t out_precision,
                              int64_t n_out) {
+  NvtxRange nvtx_("owqs_submit_host");
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_submit_host");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "submit before load_pattern");
@@ -1547,6 +1563,7 @@ owqs_status owqs_submit_host(owqs_ctx* ctx, owqs_mode mode, uint64_t seed, const
 }
 
 owqs_status owqs_wait(owqs_ctx* ctx, uint8_t* outcomes_out, double* prob0_out) {
+  NvtxRange nvtx_("owqs_wait");
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->pending) return fail(ctx, OWQS_E_STATE, "nothing submitted");
   const int cmi = ctx->pending - 1;
@@ -1565,6 +1582,7 @@ owqs_status owqs_wait(owqs_ctx* ctx, uint8_t* outcomes_out, double* prob0_out) {
 owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const double* inputs,
                            const uint64_t* seeds, const uint8_t* forced, double* outputs, uint8_t* outcomes,
                            double* prob0) {
+  NvtxRange nvtx_("owqs_run_batch");
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_run_batch");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "run_batch before load_pattern");
@@ -1579,6 +1597,7 @@ owqs_status owqs_run_batch(owqs_ctx* ctx, owqs_mode mode, int64_t n_batch, const
 }
 
 owqs_status owqs_get_output(owqs_ctx* ctx, double* amps, int64_t n_amps) {
+  NvtxRange nvtx_("owqs_get_output");
   return owqs_get_output_host(ctx, amps, 128, n_amps);
 }
 
@@ -1622,6 +1641,7 @@ owqs_status output_merged(owqs_ctx* ctx, void* dst, int out_prec, bool dst_devic
 }
 
 owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, int64_t n_amps) {
+  NvtxRange nvtx_("owqs_get_output_host");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
@@ -1634,6 +1654,7 @@ owqs_status owqs_get_output_host(owqs_ctx* ctx, void* amps, int32_t precision, i
 }
 
 owqs_status owqs_get_output_device(owqs_ctx* ctx, void* dev_amps, int32_t precision, int64_t n_amps) {
+  NvtxRange nvtx_("owqs_get_output_device");
   if (!ctx) return OWQS_E_ARG;
   if (ctx->pending) return fail(ctx, OWQS_E_STATE, "a submitted run is pending: owqs_wait first");
   if (!ctx->has_output) return fail(ctx, OWQS_E_STATE, "no output: run first");
@@ -1756,6 +1777,7 @@ owqs_status owqs_output_inner(owqs_ctx* a, owqs_ctx* b, double* re, double* im) 
 }
 
 owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
+  NvtxRange nvtx_("owqs_recognize");
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_recognize");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "recognize before load_pattern");
@@ -1809,6 +1831,7 @@ owqs_status owqs_recognize(owqs_ctx* ctx, double* U, int64_t n, double* max_unit
 // sqrt(d): with outputs O in bits 0..|O|-1 and R above them, the output array IS U in column-major
 // order up to the factor 1/sqrt(d). One run at width + |I| instead of 2^|I| runs.
 owqs_status owqs_recognize_choi(owqs_ctx* ctx, double* U, int64_t n, double* max_unitarity_err) {
+  NvtxRange nvtx_("owqs_recognize_choi");
   if (!ctx) return OWQS_E_ARG;
   if (!ctx->subs.empty()) return substates_unsupported(ctx, "owqs_recognize_choi");
   if (!ctx->loaded) return fail(ctx, OWQS_E_STATE, "recognize before load_pattern");
