@@ -144,7 +144,12 @@ typedef struct {
  * Multi-rank: n_ranks = G (power of two) shards the state on its top log2(G) slot
  * positions (rank bits); every rank makes the same call sequence (SPMD). With NCCL, nccl_id points
  * to a 128-byte ncclUniqueId made by owqs_nccl_unique_id on one rank and broadcast by the caller;
- * the library owns the communicator. Errors: OWQS_E_ARG, OWQS_E_CUDA, OWQS_E_NCCL. */
+ * the library owns the communicator. A sharded program must keep a constant physical width:
+ * patterns whose compiled program has GROW or SHRINK steps (an N without a measurement to reuse
+ * its slot, a measurement without a fresh neighbour) are refused at owqs_load_pattern with
+ * OWQS_E_ARG -- the J/CZ circuit patterns and flow clusters of configs 2-5 are constant-width
+ * after slot reuse; other patterns run on one rank (or as replicas).
+ * Errors: OWQS_E_ARG, OWQS_E_CUDA, OWQS_E_NCCL. */
 owqs_status owqs_create(const owqs_config* cfg, owqs_ctx** out);
 /* Write a fresh 128-byte ncclUniqueId to out (call on one rank, broadcast to the others). */
 owqs_status owqs_nccl_unique_id(void* out);
